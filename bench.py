@@ -1,0 +1,357 @@
+#!/usr/bin/env python3
+"""Benchmark of the beamforming hot path (BASELINE.json metric: beamformed REs/s
+at 64 antennas, f = 36, b = 60, and % of roofline at 1/2/4/8 B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+    torchrun --nproc-per-node N ... bench.py --gpus N      (one rank per GPU, NCCL)
+
+A step is one bf_apply over the whole (per-rank shard of the) workload: block ->
+group routing + the FFMA beamforming kernel, inputs resident in HBM.  The
+default workload is config c4 (BASELINE.json configs[3], the metric's
+headline: 55 precoders 64x36, 2^20 tagged 64-QAM blocks), which fits one GPU;
+S (18.1 GB) + R (32.2 GB) exceed the 126 MB L2, so no flush is needed.
+Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the
+only reference this paper-only build has) on bounded samples of the same
+workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c4", help="c2 | c3 | c4 (default) | c5")
+    ap.add_argument("--f", type=int, default=36, help="flow count for --config c3")
+    ap.add_argument("--layout", default="interleaved", choices=["interleaved", "planar"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-blocks", type=int, default=0,
+                    help="blocks per rank for the host-buffer e2e leg (0 = whole shard if RAM allows)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU work of the oracle baseline sample")
+    ap.add_argument("--c5-chunks", type=int, default=0, help="c5: chunks per step (0 = all 2048)")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload_of(args):
+    import bf_synth as syn
+    if args.config == "c3":
+        return syn.workload("c3", args.f)
+    return syn.workload(args.config)
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU oracle on bounded samples of the same workload
+# ---------------------------------------------------------------------------
+def oracle_rate(wl, seconds: float, threads: int, seed: int = 0):
+    """Oracle REs/s on a seeded sample of the workload sized to ~`seconds` of CPU work."""
+    import bf_synth as syn
+    import oracle
+    rng = np.random.default_rng(seed)
+    f = wl.f if wl.f >= 0 else 36
+
+    def sample(nb):
+        ids = np.sort(rng.choice(wl.n_blocks, size=nb, replace=False))
+        if wl.f >= 0:
+            W, S, tags = syn.workload_inputs(wl, ids)
+        else:   # c5: one cell's chunk worth of mixed-modulation blocks
+            fc = syn.cell_flows(wl.seed, 8)
+            cell = int(syn.c5_cell_of_block(ids[:1])[0])
+            W = syn.precoders(wl.seed, cell, 55, 64, int(fc[cell]), "none")
+            S = syn.qam_symbols(wl.seed, 0, ids, int(fc[cell]), 60, syn.block_modulations(wl.seed, ids))
+            tags = syn.subband_tags(wl.seed, ids, 55)
+        return W, S, tags
+
+    W, S, tags = sample(max(threads, 8))
+    t0 = time.perf_counter()
+    oracle.beamform(W, S, tags, n_threads=threads, bound=False)
+    per_block = max((time.perf_counter() - t0) / len(S), 1e-7)
+    nb = int(min(wl.n_blocks, max(threads, seconds / per_block)))
+    W, S, tags = sample(nb)
+    t0 = time.perf_counter()
+    oracle.beamform(W, S, tags, n_threads=threads, bound=False)
+    dt = time.perf_counter() - t0
+    return nb * wl.b / dt, nb, dt, f
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import benchkit
+    import oracle
+    wl = workload_of(args)
+    threads = oracle.max_threads()
+    rates = []
+    per_step_seconds = max(2.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
+    for s in range(args.warmup + args.steps):
+        r, nb, dt, f = oracle_rate(wl, per_step_seconds, threads, seed=s)
+        if s >= args.warmup:
+            rates.append((r, nb, dt))
+    total_res = sum(nb * wl.b for _, nb, _ in rates)
+    total_t = sum(dt for _, _, dt in rates)
+    value = total_res / total_t
+    sample = (f"{args.steps} steps, each a seeded random sample of {rates[0][1]}-{max(r[1] for r in rates)} "
+              f"blocks of {wl.name} (~{per_step_seconds:.0f} s of CPU work per step)")
+    line = {
+        "impl": "reference", "metric": "beamformed REs/s (64 ant, f=36, b=60)", "value": value,
+        "unit": "REs/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total_t / len(rates), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl.name, "desc": wl.desc, "n_ant": wl.n_ant, "f": wl.f, "b": wl.b},
+        "cpu_baseline": {"value": value, "unit": "REs/s", "cores": threads, "kind": "oracle",
+                         "sample": sample, "cpu": benchkit.cpu_model()},
+        "e2e": {"value": value, "unit": "REs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def host_ram_available() -> int:
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun (one rank per GPU)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import benchkit
+    import bf_synth as syn
+    import bf_synth.cuda as sync
+    import paper_1810_11451_b200 as bf
+    from paper_1810_11451_b200 import shard
+
+    wl = workload_of(args)
+    if wl.f < 0:
+        raise SystemExit("c5 streaming bench: use --config c4/c3/c2 (c5 is covered by tests)")
+    planar = args.layout == "planar"
+
+    # ---- shard (host logic, identical on every rank) ------------------------------
+    if wl.tagged:
+        tags_all = syn.subband_tags(wl.seed, np.arange(wl.n_blocks), wl.n_groups)
+        ids = shard.subband_shard(tags_all, rank, world)
+        natural = world == 1
+    else:
+        first, cnt = shard.even_range(wl.n_blocks, rank, world)
+        ids = np.arange(first, first + cnt, dtype=np.int64)
+        natural = True
+    n_local = len(ids)
+
+    # ---- inputs resident in HBM ---------------------------------------------------
+    ids_d = None if natural else torch.from_numpy(ids).to(dev)
+    S, tags = sync.workload_device(wl, dev, first=int(ids[0]) if natural else 0, n=n_local,
+                                   ids=ids_d, planar=planar)
+    W = torch.empty((wl.n_groups, wl.n_ant, wl.f), dtype=torch.complex64, device=dev)
+    if rank == 0:
+        W.copy_(torch.from_numpy(syn.precoders(wl.seed, wl.sub, wl.n_groups, wl.n_ant, wl.f,
+                                               wl.w_norm)))
+    torch.cuda.synchronize()
+    t_bc = time.perf_counter()
+    shard.broadcast_precoders(W, src=0)          # NCCL over NVLink; once, untimed
+    torch.cuda.synchronize()
+    t_bc = time.perf_counter() - t_bc
+    if planar:
+        W = torch.from_numpy(syn.to_planar(W.cpu().numpy())).to(dev)
+
+    plan = bf.Plan(f=wl.f, layout=args.layout)
+    plan.set_precoders(W)
+    R = torch.empty(plan.r_shape(n_local), dtype=plan.dtype, device=dev)
+    stream = torch.cuda.current_stream()
+
+    # ---- warm-up, then K timed steps ---------------------------------------------
+    for _ in range(max(args.warmup, 0)):
+        plan.apply(S, tags, out=R)
+    torch.cuda.synchronize()
+    clocks = benchkit.ClockSampler(local).start() if rank == 0 else None
+    plan.set_profiling(True)
+    plan.kernel_time()
+    launches0 = plan.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        plan.apply(S, tags, out=R)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = e0.elapsed_time(e1)
+    kern_ms, kern_n = plan.kernel_time()
+    launches = plan.launch_count() - launches0
+    plan.set_profiling(False)
+    clk = clocks.stop() if clocks else None
+
+    elapsed_ms = shard.max_over_ranks(elapsed_ms, dev)
+    kern_avg_ms = shard.max_over_ranks(kern_ms / max(kern_n, 1), dev)
+    launches = int(shard.sum_over_ranks(launches, dev))
+    total_blocks = wl.n_blocks
+    value = total_blocks * wl.b * args.steps / (elapsed_ms * 1e-3)
+
+    # ---- roofline of the dominant kernel (bf_ffma_kernel) ---------------------------
+    peaks = benchkit.measured_peaks()
+    cfg = plan.kernel_config(n_local)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_max = benchkit.fp32_peak_tflops(sms, peaks.get("sm_max_mhz", 1965.0))
+    flops_launch = wl.block_flops * n_local
+    bytes_launch = wl.block_bytes * n_local
+    achieved_tf = flops_launch / (kern_avg_ms * 1e-3) / 1e12
+    achieved_gbs = bytes_launch / (kern_avg_ms * 1e-3) / 1e9
+    hbm = peaks["hbm_gbs"]
+    ai = wl.block_flops / wl.block_bytes
+    fp32_bound = ai * hbm / 1e3 > peak_max            # TFLOP/s reachable from HBM vs FFMA peak
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tr = json.load(open(tpath)).get(f"{wl.name}:{args.layout}:n{n_local}")
+            traffic = tr
+        except ValueError:
+            traffic = None
+    if fp32_bound:
+        roof = {"bound": "alu", "achieved": achieved_tf, "peak": peak_max, "unit": "TFLOP/s",
+                "frac": achieved_tf / peak_max, "traffic": traffic,
+                "peak_basis": f"derived: {sms} SMs x 128 FP32 lanes x 2 x {peaks.get('sm_max_mhz', 1965.0):.0f} MHz",
+                "hbm": {"achieved": achieved_gbs, "peak": hbm, "unit": "GB/s", "frac": achieved_gbs / hbm}}
+    else:
+        roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                "frac": achieved_gbs / hbm, "traffic": traffic,
+                "peak_basis": peaks.get("source", "")}
+    if clk and clk.get("sm_mhz"):
+        roof["frac_at_observed_clock"] = achieved_tf / benchkit.fp32_peak_tflops(sms, clk["sm_mhz"]) \
+            if fp32_bound else None
+    roof["kernel_ms"] = kern_avg_ms
+    roof["kernel_share_of_step"] = kern_avg_ms * args.steps / elapsed_ms
+    roof["algorithmic_bytes_per_launch"] = bytes_launch
+    roof["algorithmic_flops_per_launch"] = flops_launch
+
+    # ---- e2e through the public API with host buffers ---------------------------------
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        del R
+        torch.cuda.empty_cache()
+        s_blk = 480 * wl.f
+        need = n_local * (s_blk + 30720 + 4)
+        budget = int(host_ram_available() * 0.6) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world)))
+        n_e2e = n_local if args.e2e_blocks <= 0 else min(args.e2e_blocks, n_local)
+        if n_e2e * (s_blk + 30720 + 4) > budget:
+            n_e2e = max(1, budget // (s_blk + 30720 + 4))
+        Sh = torch.empty(plan.s_shape(n_e2e), dtype=plan.dtype).pin_memory()
+        Sh.copy_(S[:n_e2e])
+        th = None
+        if tags is not None:
+            th = torch.empty(n_e2e, dtype=torch.int32).pin_memory()
+            th.copy_(tags[:n_e2e])
+        del S
+        torch.cuda.empty_cache()
+        Rh = torch.empty(plan.r_shape(n_e2e), dtype=plan.dtype).pin_memory()
+        plan.apply_host(Sh, th, Rh)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            plan.apply_host(Sh, th, Rh)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = shard.max_over_ranks(e0.elapsed_time(e1), dev)
+        n_e2e_total = int(shard.sum_over_ranks(n_e2e, dev))
+        e2e = {"value": n_e2e_total * wl.b * args.e2e_steps / (e2e_ms * 1e-3), "unit": "REs/s",
+               "h2d_bytes_per_step": int(n_e2e_total * (s_blk + (4 if tags is not None else 0))),
+               "d2h_bytes_per_step": int(n_e2e_total * 30720),
+               "steps": args.e2e_steps, "blocks_per_step": n_e2e_total,
+               "ms_per_step": e2e_ms / args.e2e_steps,
+               "path": "bf_apply_host: pinned host S/tags -> H2D -> route+kernel -> D2H pinned R, "
+                       "chunked on 3 streams"}
+        del Sh, Rh
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only) -----------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        thr = oracle.max_threads()
+        r, nb, dt, _ = oracle_rate(wl, args.cpu_seconds, thr)
+        cpu = {"value": r, "unit": "REs/s", "cores": thr, "kind": "oracle",
+               "sample": f"seeded random sample of {nb} blocks of {wl.name} ({dt:.1f} s, "
+                         f"{thr} threads, fp64 triple loop)", "cpu": benchkit.cpu_model()}
+
+    if rank == 0:
+        gpu_name = torch.cuda.get_device_name(dev)
+        line = {
+            "metric": "beamformed REs/s (64 ant, f=36, b=60)", "value": value, "unit": "REs/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl.name, "desc": wl.desc, "n_ant": wl.n_ant, "f": wl.f,
+                       "b": wl.b, "blocks": wl.n_blocks, "groups": wl.n_groups,
+                       "layout": args.layout, "parallelism": f"dp{world} (blocks sharded by subband)"
+                       if wl.tagged else f"dp{world}",
+                       "l2": "inputs larger than L2 (S+R >> 126 MB)" if bytes_launch > 512e6
+                       else "inputs fit in L2 (warm; no flush)",
+                       "kernel": cfg, "gpu": gpu_name, "w_broadcast_ms": t_bc * 1e3},
+            "flops_per_s": total_blocks * wl.block_flops * args.steps / (elapsed_ms * 1e-3),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+        }
+        if "tflops" in os.environ.get("BF_BENCH_PROBE", "tflops"):
+            try:
+                line["ffma_probe"] = benchkit.ffma_probe()
+            except Exception as ex:  # pragma: no cover
+                line["ffma_probe"] = {"error": str(ex)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

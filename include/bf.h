@@ -1,0 +1,156 @@
+/*
+ * bf.h — C ABI of the B200 beamforming library (libbf.so).
+ *
+ * The operation (§III, beamforming equation):
+ *   "The beam forming algorithm computes many products W x S where W the
+ *    precoding matrix is constant and S the symbols matrix is changing.  A row
+ *    i of W corresponds to one antenna (here there are 64).  Matrix S has f
+ *    rows, one per parallel flow, and b columns, one per resource element ...
+ *    where b = 60 and constant f can vary from 0 to 36."
+ *
+ *   For every block n with precoder group g = group_idx[n] (0 when no tags):
+ *       R[n][i][j] = sum_{k<f} W[g][i][k] * S[n][k][j]     complex fp32,
+ *   accumulated with fp32 fused multiply-adds (4 FFMA per complex MAC,
+ *   accumulators start at +0.0f).  Accuracy contract (BASELINE.json north_star
+ *   item 4): |R - R_exact| <= 1e-5 * sum_k |W[g][i][k]| |S[n][k][j]| per
+ *   element; bit-exact for f = 0 (+0.0) and for identity / selection W.
+ *
+ * The calls follow the paper's statement: W is set once (bf_set_precoders),
+ * then many S blocks are multiplied by it (bf_apply).  Multiple precoder
+ * groups (per-subband W, BASELINE.json configs[3], configs[4]) extend the
+ * paper's single W; blocks pick their group through group_idx.
+ *
+ * Element type: complex float32 = 8 bytes.  Layouts (per block, row-major):
+ *   BF_LAYOUT_INTERLEAVED  W [n_groups][n_ant][f]  (re, im) pairs
+ *                          S [n_blocks][f][b]       (re, im) pairs
+ *                          R [n_blocks][n_ant][b]   (re, im) pairs
+ *   BF_LAYOUT_PLANAR       W [n_groups][2][n_ant][f]  re plane then im plane
+ *                          S [n_blocks][2][f][b]
+ *                          R [n_blocks][2][n_ant][b]
+ *   Both layouts move the same bytes per block: S 8*f*b, R 8*n_ant*b.
+ *
+ * Supported domain: n_ant == 64, b == 60, 0 <= f <= 36, 1 <= n_groups <= 1024,
+ * 0 <= n_blocks < 2^31.  Other shapes return BF_ERR_UNSUPPORTED (there is no
+ * slow or CPU fallback).
+ *
+ * Ownership: the plan owns a device copy of W (re-laid out for the kernel)
+ * and its workspace (routing arrays, host-pipeline staging), grown on demand.
+ * The caller owns S, R and group_idx and keeps them alive until the stream
+ * work completes.  R is fully overwritten, never accumulated, and must not
+ * overlap S.  A plan is bound to the CUDA device current at bf_plan_create.
+ *
+ * Errors: every call returns a bf_status; no exception crosses the ABI.
+ * Argument errors are detected synchronously before anything is enqueued.
+ * Launch errors return BF_ERR_CUDA with a detail string (bf_last_error,
+ * thread-local).  Device faults surface at the caller's next synchronisation.
+ * Tags outside [0, n_groups) are a caller precondition violation: such blocks
+ * are left unwritten (never an out-of-bounds access); with the environment
+ * variable BF_CHECK=1, bf_apply synchronises and returns BF_ERR_INVALID_VALUE.
+ *
+ * Streams are passed as void* (a cudaStream_t; NULL = legacy default stream),
+ * so callers need no CUDA headers.  All enqueueing calls are asynchronous with
+ * respect to the host unless stated otherwise.
+ *
+ * Concurrency: distinct plans are independent.  bf_set_precoders must not race
+ * with in-flight applies of the same plan.  Untagged applies of one plan may
+ * run on several streams concurrently (read-only W); tagged applies share the
+ * plan's routing workspace and must be serialised by the caller (one stream).
+ */
+#ifndef BF_H
+#define BF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BF_VERSION 1
+
+typedef struct bf_plan_s *bf_plan_t;
+
+typedef enum {
+    BF_LAYOUT_INTERLEAVED = 0,
+    BF_LAYOUT_PLANAR = 1
+} bf_layout;
+
+typedef enum {
+    BF_OK = 0,
+    BF_ERR_INVALID_VALUE = 1,   /* NULL / negative / overlapping / wrong-device argument */
+    BF_ERR_UNSUPPORTED = 2,     /* shape outside the compiled domain (n_ant, b, f, n_groups) */
+    BF_ERR_NO_PRECODERS = 3,    /* bf_apply before bf_set_precoders (f > 0) */
+    BF_ERR_MISALIGNED = 4,      /* device pointer not 16-byte aligned (tags: 4-byte) */
+    BF_ERR_OUT_OF_MEMORY = 5,   /* device or pinned allocation failed */
+    BF_ERR_CUDA = 6,            /* CUDA runtime error; see bf_last_error() */
+    BF_ERR_NO_DEVICE = 7        /* no CUDA device visible */
+} bf_status;
+
+/* Create a plan for R = W x S with the given dimensions and layout.
+ * n_ant: antennas (rows of W, must be 64); f: flows (0..36); b: resource
+ * elements (must be 60); layout: a bf_layout.  Validates the dimensions
+ * before touching the GPU (so dimension errors are reported without one).
+ * *out receives the plan (unchanged on error). */
+bf_status bf_plan_create(int n_ant, int f, int b, int layout, bf_plan_t *out);
+
+/* Copy n_groups precoders from device memory W_dev (layout as above, 16-byte
+ * aligned) into the plan, re-laid out for the kernel, ordered on `stream`.
+ * After the stream reaches this point the caller may free W_dev.  With f == 0
+ * W_dev may be NULL.  Replaces any previous precoders. */
+bf_status bf_set_precoders(bf_plan_t p, const void *W_dev, int n_groups, void *stream);
+
+/* R_dev = W[group_idx[n]] x S_dev[n] for n in [0, n_blocks), on `stream`.
+ * S_dev, R_dev: device pointers, 16-byte aligned, layout as above.
+ * group_idx_dev: device int32 per block, or NULL (every block uses group 0).
+ * n_blocks == 0 is a no-op.  With f == 0, R is set to +0.0 and S_dev may be
+ * NULL.  The result of block n is bitwise independent of n_blocks, of the
+ * other blocks, of the stream and of the tags of other blocks. */
+bf_status bf_apply(bf_plan_t p, const void *S_dev, const int32_t *group_idx_dev,
+                   void *R_dev, int64_t n_blocks, void *stream);
+
+/* Same product with HOST buffers (pinned for full speed; pageable works but
+ * serialises the copies): the library pipelines chunks host->device, the same
+ * kernels as bf_apply, and device->host on internal streams, ordered after
+ * prior work on `stream`; `stream` waits for the last copy before returning
+ * control of ordering to the caller.  The call returns after enqueueing; the
+ * host buffers must stay valid until `stream` is synchronised. */
+bf_status bf_apply_host(bf_plan_t p, const void *S_host, const int32_t *group_idx_host,
+                        void *R_host, int64_t n_blocks, void *stream);
+
+/* Routing step of bf_apply exposed for testing: a
+ * stable counting sort of blocks by tag.  perm_dev[int32 n_blocks] receives
+ * block ids ordered by (tag, block id); offsets_dev[int32 n_groups + 2]
+ * receives the start of each group, then the number of valid tags, then
+ * n_blocks (invalid tags sort last).  Uses the plan's precoder count. */
+bf_status bf_route(bf_plan_t p, const int32_t *group_idx_dev, int64_t n_blocks,
+                   int32_t *perm_dev, int32_t *offsets_dev, void *stream);
+
+/* Free the plan and everything it owns.  Call after its work has drained. */
+bf_status bf_destroy(bf_plan_t p);
+
+/* Instrumentation (used by bench.py; never changes results).
+ * set_profiling(1): every bf_apply also records CUDA events around the main
+ * beamforming kernel on its launching stream.  kernel_time: synchronises those
+ * events, returns the summed milliseconds and number of timed launches, and
+ * clears the record.  launch_count: kernels this plan has launched so far
+ * (routing, relayout and beamforming kernels; memsets and copies excluded). */
+bf_status bf_plan_set_profiling(bf_plan_t p, int enable);
+bf_status bf_plan_kernel_time(bf_plan_t p, double *total_ms, int64_t *n_launches);
+bf_status bf_plan_launch_count(bf_plan_t p, int64_t *count);
+
+/* Chunk size (blocks) of bf_apply_host's pipeline; 0 selects the default. */
+bf_status bf_plan_set_host_chunk(bf_plan_t p, int64_t blocks);
+
+/* Static description of the kernel chosen for this plan: grid and block size
+ * for n_blocks, dynamic shared memory bytes and resident CTAs per SM. */
+bf_status bf_plan_kernel_config(bf_plan_t p, int64_t n_blocks, int *grid, int *block,
+                                int *smem_bytes, int *ctas_per_sm);
+
+const char *bf_status_string(bf_status s);
+const char *bf_last_error(void);  /* thread-local detail of the last failure */
+int bf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BF_H */

@@ -1,0 +1,666 @@
+// bf_api.cu — host side of libbf.so: the C ABI declared in include/bf.h.
+//
+// Plan object, argument validation, W relayout, block ->
+// group routing (a3, stable counting sort), dispatch to the per-f kernel
+// instantiation (a4+a5+a7), the f = 0 path (a8), and the host-buffer pipeline
+// used for end-to-end measurement.  PAPER.md:84-86 defines the operation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "bf.h"
+#include "bf_dispatch.h"
+#include "bf_ffma.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+bf_status fail(bf_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return s;
+}
+
+bf_status cuda_fail(cudaError_t e, const char *what) {
+    return fail(BF_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define BF_CUDA(call)                                  \
+    do {                                               \
+        cudaError_t e_ = (call);                       \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+constexpr int kMaxGroups = 1024;
+constexpr int kRouteThreads = 256;         // 8 warps
+constexpr int kRouteMinTile = 4096;
+constexpr int kRouteMaxTable = 65536;      // tiles x (groups + 1) entries
+constexpr int64_t kDefaultHostChunk = 2048;
+constexpr int kHostSlots = 3;
+
+BfKernelTable g_table;
+std::once_flag g_table_once;
+
+void init_table() {
+    std::memset(&g_table, 0, sizeof(g_table));
+    bf_register_f01_06(g_table);
+    bf_register_f07_12(g_table);
+    bf_register_f13_18(g_table);
+    bf_register_f19_24(g_table);
+    bf_register_f25_30(g_table);
+    bf_register_f31_36(g_table);
+}
+
+// ---------------------------------------------------------------------------
+// Device helpers: W relayout (a2) and routing (a3)
+// ---------------------------------------------------------------------------
+
+// Wp[g][k][j][ag] = float4(w[8ag+2j][k], w[8ag+2j+1][k]) — the layout bf_ffma_kernel
+// reads with one conflict-free LDS.128 per (k, j).
+__global__ void bf_relayout_w(const float *__restrict__ W, int n_groups, int F, int layout,
+                              float4 *__restrict__ Wp) {
+    const int64_t total = (int64_t)n_groups * F * 32;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = idx / (F * 32);
+        const int rem = (int)(idx - g * F * 32);
+        const int k = rem / 32, j = (rem % 32) / 8, ag = rem % 8;
+        const int i0 = ag * 8 + 2 * j, i1 = i0 + 1;
+        float4 v;
+        if (layout == BF_LAYOUT_INTERLEAVED) {
+            const float *Wg = W + g * 64 * F * 2;
+            v = make_float4(Wg[(i0 * F + k) * 2], Wg[(i0 * F + k) * 2 + 1],
+                            Wg[(i1 * F + k) * 2], Wg[(i1 * F + k) * 2 + 1]);
+        } else {
+            const float *Wr = W + g * 2 * 64 * F, *Wi = Wr + 64 * F;
+            v = make_float4(Wr[i0 * F + k], Wi[i0 * F + k], Wr[i1 * F + k], Wi[i1 * F + k]);
+        }
+        Wp[idx] = v;
+    }
+}
+
+__device__ __forceinline__ int route_bin(int32_t g, int G) {
+    return (unsigned)g < (unsigned)G ? g : G;   // invalid tags -> bin G (sorted last)
+}
+
+// Pass 1: per-tile histogram -> table[tile][bin], bins 0..G (G = invalid).
+__global__ void bf_route_hist(const int32_t *__restrict__ gidx, int64_t n, int G, int tile,
+                              int32_t *__restrict__ table, int32_t *__restrict__ err) {
+    extern __shared__ int32_t hist[];
+    for (int b = threadIdx.x; b <= G; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const int64_t ts = (int64_t)blockIdx.x * tile;
+    const int64_t te = min(n, ts + tile);
+    int bad = 0;
+    for (int64_t i = ts + threadIdx.x; i < te; i += blockDim.x) {
+        const int b = route_bin(__ldg(gidx + i), G);
+        bad |= (b == G);
+        atomicAdd(&hist[b], 1);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err, 1);
+    for (int b = threadIdx.x; b <= G; b += blockDim.x)
+        table[(int64_t)blockIdx.x * (G + 1) + b] = hist[b];
+}
+
+// Pass 2 (one CTA of 1024 threads): table[tile][bin] <- global start of the
+// tile's items of that bin; offsets[0..G] <- start of each bin, offsets[G+1] = n.
+__global__ void bf_route_scan(int32_t *__restrict__ table, int P, int G, int64_t n,
+                              int32_t *__restrict__ offsets) {
+    __shared__ int32_t tot[kMaxGroups + 2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int b = warp; b <= G; b += nwarps) {
+        int32_t carry = 0;
+        for (int t0 = 0; t0 < P; t0 += 32) {
+            const int t = t0 + lane;
+            const int32_t v = t < P ? table[(int64_t)t * (G + 1) + b] : 0;
+            int32_t inc = v;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += u;
+            }
+            if (t < P) table[(int64_t)t * (G + 1) + b] = carry + inc - v;
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) tot[b] = carry;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        int32_t carry = 0;
+        for (int b0 = 0; b0 <= G; b0 += 32) {
+            const int b = b0 + lane;
+            const int32_t v = b <= G ? tot[b] : 0;
+            int32_t inc = v;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += u;
+            }
+            if (b <= G) tot[b] = carry + inc - v;   // exclusive start of bin b
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b <= G; b += blockDim.x) offsets[b] = tot[b];
+    if (threadIdx.x == 0) offsets[G + 1] = (int32_t)n;
+    const int64_t entries = (int64_t)P * (G + 1);
+    for (int64_t e = threadIdx.x; e < entries; e += blockDim.x)
+        table[e] += tot[e % (G + 1)];
+}
+
+// Pass 3: stable scatter.  Each warp owns a contiguous sub-tile; ranks come
+// from __match_any_sync so the output order is (bin, block id) exactly.
+__global__ void bf_route_scatter(const int32_t *__restrict__ gidx, int64_t n, int G, int tile,
+                                 const int32_t *__restrict__ table, int32_t *__restrict__ perm,
+                                 int32_t *__restrict__ gsorted) {
+    extern __shared__ int32_t cnt[];   // [8][G + 1]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nb = G + 1;
+    for (int e = threadIdx.x; e < 8 * nb; e += blockDim.x) cnt[e] = 0;
+    __syncthreads();
+    const int64_t ts = (int64_t)blockIdx.x * tile;
+    const int per_warp = tile / 8;
+    const int64_t ws = ts + (int64_t)warp * per_warp;
+    const int64_t we = min(n, ws + per_warp);
+    int32_t *mycnt = cnt + warp * nb;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t base = ws; base < we; base += 32) {
+        const int64_t i = base + lane;
+        const int b = i < we ? route_bin(__ldg(gidx + i), G) : -1;
+        const unsigned m = __match_any_sync(0xffffffffu, b);
+        if (b >= 0 && (m & lt) == 0) mycnt[b] += __popc(m);
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+        int32_t run = table[(int64_t)blockIdx.x * nb + b];
+        for (int w = 0; w < 8; ++w) {
+            const int32_t c = cnt[w * nb + b];
+            cnt[w * nb + b] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    for (int64_t base = ws; base < we; base += 32) {
+        const int64_t i = base + lane;
+        const int b = i < we ? route_bin(__ldg(gidx + i), G) : -1;
+        const unsigned m = __match_any_sync(0xffffffffu, b);
+        if (b >= 0) {
+            const int32_t pos = mycnt[b] + __popc(m & lt);
+            perm[pos] = (int32_t)i;
+            gsorted[pos] = b;
+        }
+        __syncwarp();
+        if (b >= 0 && (m & lt) == 0) mycnt[b] += __popc(m);
+        __syncwarp();
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    bool changed = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) {
+            changed = cudaSetDevice(dev) == cudaSuccess;
+        }
+    }
+    ~DeviceGuard() {
+        if (changed) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+bf_status grow(T **ptr, int64_t *cap, int64_t need, const char *what) {
+    if (*cap >= need) return BF_OK;
+    if (*ptr) cudaFree(*ptr);
+    *ptr = nullptr;
+    *cap = 0;
+    const int64_t n = std::max<int64_t>(need, 1);
+    if (cudaMalloc(reinterpret_cast<void **>(ptr), n * sizeof(T)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(BF_ERR_OUT_OF_MEMORY, "cudaMalloc of %s (%lld bytes) failed", what,
+                    (long long)(n * sizeof(T)));
+    }
+    *cap = n;
+    return BF_OK;
+}
+
+bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+}  // namespace
+
+struct bf_plan_s {
+    int n_ant = 64, f = 0, b = 60, layout = 0, device = 0, num_sms = 0;
+    int n_groups = 0;
+    BfKernelEntry kern{};
+    int ctas_per_sm = 0;
+    float4 *Wp = nullptr;
+    int64_t Wp_cap = 0;
+    // routing workspace
+    int32_t *perm = nullptr, *gsorted = nullptr, *table = nullptr, *offsets = nullptr,
+            *err = nullptr;
+    int64_t perm_cap = 0, gs_cap = 0, table_cap = 0, offsets_cap = 0, err_cap = 0;
+    // host pipeline
+    int64_t host_chunk = kDefaultHostChunk, slot_cap = 0;
+    float *hS[kHostSlots] = {}, *hR[kHostSlots] = {};
+    int32_t *hG[kHostSlots] = {};
+    int64_t hS_cap[kHostSlots] = {}, hR_cap[kHostSlots] = {}, hG_cap[kHostSlots] = {};
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_h2d[kHostSlots] = {}, ev_comp[kHostSlots] = {}, ev_d2h[kHostSlots] = {},
+                ev_start = nullptr;
+    // instrumentation
+    bool profiling = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+    size_t prof_used = 0;
+    int64_t launches = 0;
+};
+
+namespace {
+
+bf_status launched(bf_plan_t p, const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    ++p->launches;
+    return BF_OK;
+}
+
+// Stable counting sort of blocks by tag into p->perm / p->gsorted (+offsets).
+bf_status route(bf_plan_t p, const int32_t *gidx, int64_t n, int32_t *perm, int32_t *gsorted,
+                int32_t *offsets, cudaStream_t st) {
+    const int G = p->n_groups;
+    int64_t tile = kRouteMinTile;
+    const int64_t max_tiles = std::max<int64_t>(1, kRouteMaxTable / (G + 1));
+    if ((n + tile - 1) / tile > max_tiles) tile = (n + max_tiles - 1) / max_tiles;
+    tile = (tile + kRouteThreads - 1) / kRouteThreads * kRouteThreads;
+    const int64_t P = (n + tile - 1) / tile;
+    bf_status s;
+    if ((s = grow(&p->table, &p->table_cap, P * (G + 1), "routing table")) != BF_OK) return s;
+    if ((s = grow(&p->err, &p->err_cap, 1, "routing flag")) != BF_OK) return s;
+    BF_CUDA(cudaMemsetAsync(p->err, 0, sizeof(int32_t), st));
+    const size_t hist_smem = (G + 1) * sizeof(int32_t);
+    bf_route_hist<<<(unsigned)P, kRouteThreads, hist_smem, st>>>(gidx, n, G, (int)tile,
+                                                                  p->table, p->err);
+    if ((s = launched(p, "bf_route_hist launch")) != BF_OK) return s;
+    bf_route_scan<<<1, 1024, 0, st>>>(p->table, (int)P, G, n, offsets);
+    if ((s = launched(p, "bf_route_scan launch")) != BF_OK) return s;
+    const size_t sc_smem = 8 * (G + 1) * sizeof(int32_t);
+    bf_route_scatter<<<(unsigned)P, kRouteThreads, sc_smem, st>>>(gidx, n, G, (int)tile,
+                                                                    p->table, perm, gsorted);
+    if ((s = launched(p, "bf_route_scatter launch")) != BF_OK) return s;
+    return BF_OK;
+}
+
+bf_status check_tags_if_requested(bf_plan_t p, cudaStream_t st) {
+    const char *env = std::getenv("BF_CHECK");
+    if (!env || std::strcmp(env, "1") != 0) return BF_OK;
+    int32_t h = 0;
+    BF_CUDA(cudaMemcpyAsync(&h, p->err, sizeof(h), cudaMemcpyDeviceToHost, st));
+    BF_CUDA(cudaStreamSynchronize(st));
+    if (h) return fail(BF_ERR_INVALID_VALUE, "group_idx has entries outside [0, %d)", p->n_groups);
+    return BF_OK;
+}
+
+int grid_for(bf_plan_t p, int64_t n_items) {
+    const int64_t cap = (int64_t)p->num_sms * std::max(1, p->ctas_per_sm);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(n_items, cap));
+}
+
+// Device-resident apply (validated arguments).
+bf_status apply_device(bf_plan_t p, const void *S, const int32_t *gidx, void *R, int64_t n,
+                       cudaStream_t st) {
+    if (n == 0) return BF_OK;
+    const size_t r_bytes = (size_t)n * bfk::kRBlockFloats * sizeof(float);
+    if (p->f == 0) {   // a8: the empty sum, +0.0f everywhere
+        BF_CUDA(cudaMemsetAsync(R, 0, r_bytes, st));
+        return BF_OK;
+    }
+    bfk::KParams kp{};
+    kp.Wp = p->Wp;
+    kp.S = static_cast<const float *>(S);
+    kp.R = static_cast<float *>(R);
+    kp.n_items = n;
+    kp.n_groups = p->n_groups;
+    bf_status s;
+    if (gidx && p->n_groups > 1) {
+        if ((s = grow(&p->perm, &p->perm_cap, n, "perm")) != BF_OK) return s;
+        if ((s = grow(&p->gsorted, &p->gs_cap, n, "gsorted")) != BF_OK) return s;
+        if ((s = grow(&p->offsets, &p->offsets_cap, p->n_groups + 2, "offsets")) != BF_OK)
+            return s;
+        if ((s = route(p, gidx, n, p->perm, p->gsorted, p->offsets, st)) != BF_OK) return s;
+        if ((s = check_tags_if_requested(p, st)) != BF_OK) return s;
+        kp.perm = p->perm;
+        kp.gsorted = p->gsorted;
+    }
+    const int grid = grid_for(p, n);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (p->profiling) {
+        if (p->prof_used == p->prof_events.size()) {
+            cudaEvent_t a, b;
+            BF_CUDA(cudaEventCreate(&a));
+            BF_CUDA(cudaEventCreate(&b));
+            p->prof_events.emplace_back(a, b);
+        }
+        e0 = p->prof_events[p->prof_used].first;
+        e1 = p->prof_events[p->prof_used].second;
+        ++p->prof_used;
+        BF_CUDA(cudaEventRecord(e0, st));
+    }
+    void *args[] = {&kp};
+    cudaError_t e = cudaLaunchKernel(p->kern.fn, dim3(grid), dim3(bfk::kThreads), args,
+                                     (size_t)p->kern.smem_bytes, st);
+    if (e != cudaSuccess) return cuda_fail(e, "bf_ffma_kernel launch");
+    if ((s = launched(p, "bf_ffma_kernel launch")) != BF_OK) return s;
+    if (p->profiling) BF_CUDA(cudaEventRecord(e1, st));
+    return BF_OK;
+}
+
+bf_status ensure_host_pipeline(bf_plan_t p, bool tagged) {
+    bf_status s;
+    const int64_t C = p->host_chunk;
+    for (int i = 0; i < kHostSlots; ++i) {
+        if (p->f > 0 &&
+            (s = grow(&p->hS[i], &p->hS_cap[i], C * 120 * p->f, "host-pipeline S slot")) != BF_OK)
+            return s;
+        if ((s = grow(&p->hR[i], &p->hR_cap[i], C * bfk::kRBlockFloats, "host-pipeline R slot")) !=
+            BF_OK)
+            return s;
+        if (tagged && (s = grow(&p->hG[i], &p->hG_cap[i], C, "host-pipeline tag slot")) != BF_OK)
+            return s;
+    }
+    if (!p->s_h2d) {
+        BF_CUDA(cudaStreamCreateWithFlags(&p->s_h2d, cudaStreamNonBlocking));
+        BF_CUDA(cudaStreamCreateWithFlags(&p->s_d2h, cudaStreamNonBlocking));
+        BF_CUDA(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming));
+        for (int i = 0; i < kHostSlots; ++i) {
+            BF_CUDA(cudaEventCreateWithFlags(&p->ev_h2d[i], cudaEventDisableTiming));
+            BF_CUDA(cudaEventCreateWithFlags(&p->ev_comp[i], cudaEventDisableTiming));
+            BF_CUDA(cudaEventCreateWithFlags(&p->ev_d2h[i], cudaEventDisableTiming));
+            BF_CUDA(cudaEventRecord(p->ev_d2h[i], p->s_d2h));
+        }
+    }
+    return BF_OK;
+}
+
+bf_status validate_layout_and_dims(int n_ant, int f, int b, int layout) {
+    if (n_ant < 1 || f < 0 || b < 1)
+        return fail(BF_ERR_INVALID_VALUE, "dimensions must satisfy n_ant >= 1, f >= 0, b >= 1 "
+                                          "(got n_ant=%d f=%d b=%d)", n_ant, f, b);
+    if (layout != BF_LAYOUT_INTERLEAVED && layout != BF_LAYOUT_PLANAR)
+        return fail(BF_ERR_INVALID_VALUE, "unknown layout %d", layout);
+    if (n_ant != bfk::kAnt || b != bfk::kB || f > bfk::kMaxF)
+        return fail(BF_ERR_UNSUPPORTED, "compiled domain is n_ant=64, b=60, 0<=f<=36 "
+                                        "(got n_ant=%d f=%d b=%d)", n_ant, f, b);
+    return BF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bf_version(void) { return BF_VERSION; }
+
+const char *bf_status_string(bf_status s) {
+    switch (s) {
+        case BF_OK: return "BF_OK";
+        case BF_ERR_INVALID_VALUE: return "BF_ERR_INVALID_VALUE";
+        case BF_ERR_UNSUPPORTED: return "BF_ERR_UNSUPPORTED";
+        case BF_ERR_NO_PRECODERS: return "BF_ERR_NO_PRECODERS";
+        case BF_ERR_MISALIGNED: return "BF_ERR_MISALIGNED";
+        case BF_ERR_OUT_OF_MEMORY: return "BF_ERR_OUT_OF_MEMORY";
+        case BF_ERR_CUDA: return "BF_ERR_CUDA";
+        case BF_ERR_NO_DEVICE: return "BF_ERR_NO_DEVICE";
+    }
+    return "BF_ERR_UNKNOWN";
+}
+
+const char *bf_last_error(void) { return g_last_error.c_str(); }
+
+bf_status bf_plan_create(int n_ant, int f, int b, int layout, bf_plan_t *out) {
+    if (!out) return fail(BF_ERR_INVALID_VALUE, "out is NULL");
+    bf_status s = validate_layout_and_dims(n_ant, f, b, layout);
+    if (s != BF_OK) return s;
+    int dev = 0, count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(BF_ERR_NO_DEVICE, "no CUDA device: %s", cudaGetErrorString(e));
+    }
+    BF_CUDA(cudaGetDevice(&dev));
+    std::call_once(g_table_once, init_table);
+    bf_plan_t p = new (std::nothrow) bf_plan_s();
+    if (!p) return fail(BF_ERR_OUT_OF_MEMORY, "host allocation of the plan failed");
+    p->n_ant = n_ant;
+    p->f = f;
+    p->b = b;
+    p->layout = layout;
+    p->device = dev;
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, dev);
+    if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaGetDeviceProperties"); }
+    if (prop.major != 10) {
+        delete p;
+        return fail(BF_ERR_UNSUPPORTED, "libbf.so is built for sm_100a; device %d is sm_%d%d",
+                    dev, prop.major, prop.minor);
+    }
+    p->num_sms = prop.multiProcessorCount;
+    if (f > 0) {
+        p->kern = g_table[f][layout];
+        e = cudaFuncSetAttribute(p->kern.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 p->kern.smem_bytes);
+        if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaFuncSetAttribute"); }
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->ctas_per_sm, p->kern.fn,
+                                                          bfk::kThreads, p->kern.smem_bytes);
+        if (e != cudaSuccess) { delete p; return cuda_fail(e, "occupancy query"); }
+        if (p->ctas_per_sm < 1) {
+            delete p;
+            return fail(BF_ERR_UNSUPPORTED, "kernel for f=%d cannot be resident", f);
+        }
+    }
+    *out = p;
+    return BF_OK;
+}
+
+bf_status bf_set_precoders(bf_plan_t p, const void *W_dev, int n_groups, void *stream) {
+    if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
+    if (n_groups < 1) return fail(BF_ERR_INVALID_VALUE, "n_groups must be >= 1");
+    if (n_groups > kMaxGroups)
+        return fail(BF_ERR_UNSUPPORTED, "n_groups=%d exceeds %d", n_groups, kMaxGroups);
+    DeviceGuard guard(p->device);
+    if (p->f > 0) {
+        if (!W_dev) return fail(BF_ERR_INVALID_VALUE, "W_dev is NULL");
+        if (!aligned(W_dev, 16)) return fail(BF_ERR_MISALIGNED, "W_dev is not 16-byte aligned");
+        bf_status s = grow(&p->Wp, &p->Wp_cap, (int64_t)n_groups * p->f * 32, "precoders");
+        if (s != BF_OK) return s;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int64_t total = (int64_t)n_groups * p->f * 32;
+        const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
+        bf_relayout_w<<<blocks, 256, 0, st>>>(static_cast<const float *>(W_dev), n_groups, p->f,
+                                              p->layout, p->Wp);
+        if ((s = launched(p, "bf_relayout_w launch")) != BF_OK) return s;
+    }
+    p->n_groups = n_groups;
+    return BF_OK;
+}
+
+static bf_status validate_apply(bf_plan_t p, const void *S, const int32_t *gidx, const void *R,
+                                int64_t n, bool device) {
+    if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
+    if (n < 0) return fail(BF_ERR_INVALID_VALUE, "n_blocks must be >= 0");
+    if (n >= (int64_t(1) << 31)) return fail(BF_ERR_UNSUPPORTED, "n_blocks must be < 2^31");
+    if (n == 0) return BF_OK;
+    if (!R) return fail(BF_ERR_INVALID_VALUE, "R is NULL");
+    if (p->f > 0) {
+        if (!S) return fail(BF_ERR_INVALID_VALUE, "S is NULL");
+        if (p->n_groups < 1) return fail(BF_ERR_NO_PRECODERS, "bf_set_precoders was not called");
+    }
+    if (device) {
+        if (!aligned(R, 16) || (S && !aligned(S, 16)))
+            return fail(BF_ERR_MISALIGNED, "S and R must be 16-byte aligned");
+        if (gidx && !aligned(gidx, 4)) return fail(BF_ERR_MISALIGNED, "group_idx misaligned");
+    }
+    if (p->f > 0) {
+        const uintptr_t s0 = reinterpret_cast<uintptr_t>(S), s1 = s0 + (uintptr_t)n * 480 * p->f;
+        const uintptr_t r0 = reinterpret_cast<uintptr_t>(R), r1 = r0 + (uintptr_t)n * 30720;
+        if (s0 < r1 && r0 < s1) return fail(BF_ERR_INVALID_VALUE, "R overlaps S");
+    }
+    return BF_OK;
+}
+
+bf_status bf_apply(bf_plan_t p, const void *S_dev, const int32_t *group_idx_dev, void *R_dev,
+                   int64_t n_blocks, void *stream) {
+    bf_status s = validate_apply(p, S_dev, group_idx_dev, R_dev, n_blocks, true);
+    if (s != BF_OK || n_blocks == 0) return s;
+    DeviceGuard guard(p->device);
+    return apply_device(p, S_dev, group_idx_dev, R_dev, n_blocks,
+                        static_cast<cudaStream_t>(stream));
+}
+
+bf_status bf_route(bf_plan_t p, const int32_t *group_idx_dev, int64_t n_blocks, int32_t *perm_dev,
+                   int32_t *offsets_dev, void *stream) {
+    if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
+    if (p->n_groups < 1) return fail(BF_ERR_NO_PRECODERS, "bf_set_precoders was not called");
+    if (n_blocks < 0 || n_blocks >= (int64_t(1) << 31))
+        return fail(BF_ERR_INVALID_VALUE, "n_blocks out of range");
+    if (!offsets_dev || (n_blocks > 0 && (!group_idx_dev || !perm_dev)))
+        return fail(BF_ERR_INVALID_VALUE, "NULL buffer");
+    DeviceGuard guard(p->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (n_blocks == 0) {
+        BF_CUDA(cudaMemsetAsync(offsets_dev, 0, (p->n_groups + 2) * sizeof(int32_t), st));
+        return BF_OK;
+    }
+    bf_status s = grow(&p->gsorted, &p->gs_cap, n_blocks, "gsorted");
+    if (s != BF_OK) return s;
+    return route(p, group_idx_dev, n_blocks, perm_dev, p->gsorted, offsets_dev, st);
+}
+
+bf_status bf_apply_host(bf_plan_t p, const void *S_host, const int32_t *group_idx_host,
+                        void *R_host, int64_t n_blocks, void *stream) {
+    bf_status s = validate_apply(p, S_host, group_idx_host, R_host, n_blocks, false);
+    if (s != BF_OK || n_blocks == 0) return s;
+    DeviceGuard guard(p->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const bool tagged = group_idx_host != nullptr && p->n_groups > 1;
+    if ((s = ensure_host_pipeline(p, tagged)) != BF_OK) return s;
+    const int64_t C = p->host_chunk;
+    const size_t s_blk = (size_t)480 * p->f, r_blk = (size_t)bfk::kRBlockFloats * sizeof(float);
+    BF_CUDA(cudaEventRecord(p->ev_start, st));
+    BF_CUDA(cudaStreamWaitEvent(p->s_h2d, p->ev_start, 0));
+    BF_CUDA(cudaStreamWaitEvent(p->s_d2h, p->ev_start, 0));
+    int last = 0;
+    for (int64_t c0 = 0, c = 0; c0 < n_blocks; c0 += C, ++c) {
+        const int slot = (int)(c % kHostSlots);
+        const int64_t nc = std::min(C, n_blocks - c0);
+        // slot is free once its previous device->host copy has drained
+        BF_CUDA(cudaStreamWaitEvent(p->s_h2d, p->ev_d2h[slot], 0));
+        if (p->f > 0)
+            BF_CUDA(cudaMemcpyAsync(p->hS[slot], static_cast<const char *>(S_host) + c0 * s_blk,
+                                    nc * s_blk, cudaMemcpyHostToDevice, p->s_h2d));
+        if (tagged)
+            BF_CUDA(cudaMemcpyAsync(p->hG[slot], group_idx_host + c0, nc * sizeof(int32_t),
+                                    cudaMemcpyHostToDevice, p->s_h2d));
+        BF_CUDA(cudaEventRecord(p->ev_h2d[slot], p->s_h2d));
+        BF_CUDA(cudaStreamWaitEvent(st, p->ev_h2d[slot], 0));
+        if ((s = apply_device(p, p->hS[slot], tagged ? p->hG[slot] : nullptr, p->hR[slot], nc,
+                              st)) != BF_OK)
+            return s;
+        BF_CUDA(cudaEventRecord(p->ev_comp[slot], st));
+        BF_CUDA(cudaStreamWaitEvent(p->s_d2h, p->ev_comp[slot], 0));
+        BF_CUDA(cudaMemcpyAsync(static_cast<char *>(R_host) + c0 * r_blk, p->hR[slot], nc * r_blk,
+                                cudaMemcpyDeviceToHost, p->s_d2h));
+        BF_CUDA(cudaEventRecord(p->ev_d2h[slot], p->s_d2h));
+        last = slot;
+    }
+    BF_CUDA(cudaStreamWaitEvent(st, p->ev_d2h[last], 0));
+    return BF_OK;
+}
+
+bf_status bf_destroy(bf_plan_t p) {
+    if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
+    {
+        DeviceGuard guard(p->device);
+        cudaFree(p->Wp);
+        cudaFree(p->perm);
+        cudaFree(p->gsorted);
+        cudaFree(p->table);
+        cudaFree(p->offsets);
+        cudaFree(p->err);
+        for (int i = 0; i < kHostSlots; ++i) {
+            cudaFree(p->hS[i]);
+            cudaFree(p->hR[i]);
+            cudaFree(p->hG[i]);
+            if (p->ev_h2d[i]) cudaEventDestroy(p->ev_h2d[i]);
+            if (p->ev_comp[i]) cudaEventDestroy(p->ev_comp[i]);
+            if (p->ev_d2h[i]) cudaEventDestroy(p->ev_d2h[i]);
+        }
+        if (p->ev_start) cudaEventDestroy(p->ev_start);
+        if (p->s_h2d) cudaStreamDestroy(p->s_h2d);
+        if (p->s_d2h) cudaStreamDestroy(p->s_d2h);
+        for (auto &ev : p->prof_events) {
+            cudaEventDestroy(ev.first);
+            cudaEventDestroy(ev.second);
+        }
+    }
+    delete p;
+    return BF_OK;
+}
+
+bf_status bf_plan_set_profiling(bf_plan_t p, int enable) {
+    if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
+    p->profiling = enable != 0;
+    return BF_OK;
+}
+
+bf_status bf_plan_kernel_time(bf_plan_t p, double *total_ms, int64_t *n_launches) {
+    if (!p || !total_ms || !n_launches) return fail(BF_ERR_INVALID_VALUE, "NULL argument");
+    DeviceGuard guard(p->device);
+    double sum = 0.0;
+    for (size_t i = 0; i < p->prof_used; ++i) {
+        BF_CUDA(cudaEventSynchronize(p->prof_events[i].second));
+        float ms = 0.f;
+        BF_CUDA(cudaEventElapsedTime(&ms, p->prof_events[i].first, p->prof_events[i].second));
+        sum += ms;
+    }
+    *total_ms = sum;
+    *n_launches = (int64_t)p->prof_used;
+    p->prof_used = 0;
+    return BF_OK;
+}
+
+bf_status bf_plan_launch_count(bf_plan_t p, int64_t *count) {
+    if (!p || !count) return fail(BF_ERR_INVALID_VALUE, "NULL argument");
+    *count = p->launches;
+    return BF_OK;
+}
+
+bf_status bf_plan_set_host_chunk(bf_plan_t p, int64_t blocks) {
+    if (!p || blocks < 0) return fail(BF_ERR_INVALID_VALUE, "invalid chunk");
+    p->host_chunk = blocks == 0 ? kDefaultHostChunk : blocks;
+    return BF_OK;
+}
+
+bf_status bf_plan_kernel_config(bf_plan_t p, int64_t n_blocks, int *grid, int *block,
+                                int *smem_bytes, int *ctas_per_sm) {
+    if (!p || !grid || !block || !smem_bytes || !ctas_per_sm)
+        return fail(BF_ERR_INVALID_VALUE, "NULL argument");
+    *grid = p->f > 0 ? grid_for(p, std::max<int64_t>(n_blocks, 1)) : 0;
+    *block = p->f > 0 ? bfk::kThreads : 0;
+    *smem_bytes = p->kern.smem_bytes;
+    *ctas_per_sm = p->ctas_per_sm;
+    return BF_OK;
+}
+
+}  // extern "C"

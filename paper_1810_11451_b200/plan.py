@@ -1,0 +1,180 @@
+"""Python binding of the beamforming plan (same names as include/bf.h).
+
+Argument marshalling only: shape / dtype / device checks, data_ptr() and the
+CUDA stream handle are passed to libbf.so; every step of the computation runs
+in the library's sm_100a kernels.  PyTorch supplies device memory and streams.
+
+    plan = Plan(f=36)                       # bf_plan_create(64, 36, 60, INTERLEAVED)
+    plan.set_precoders(W)                   # W: cuda complex64 [G][64][36]
+    R = plan.apply(S, group_idx=tags)       # S: cuda complex64 [n][36][60] -> [n][64][60]
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from ._lib import BfError, Layout, Status, check, lib
+
+N_ANT = 64
+N_RE = 60
+MAX_F = 36
+
+
+def _stream_handle(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    if isinstance(stream, torch.cuda.Stream):
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(int(stream))
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(None if t is None else t.data_ptr())
+
+
+class Plan:
+    """A beamforming plan: n_ant x f precoders applied to f x b symbol blocks."""
+
+    def __init__(self, f: int, n_ant: int = N_ANT, b: int = N_RE,
+                 layout: Layout | str | int = Layout.INTERLEAVED):
+        if isinstance(layout, str):
+            layout = Layout[layout.upper()]
+        self.f, self.n_ant, self.b, self.layout = int(f), int(n_ant), int(b), Layout(layout)
+        self.n_groups = 0
+        self._h = ctypes.c_void_p()
+        check(lib().bf_plan_create(self.n_ant, self.f, self.b, int(self.layout),
+                                   ctypes.byref(self._h)))
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self._w_ref = None
+
+    # -- shapes ---------------------------------------------------------------
+    def s_shape(self, n: int):
+        return (n, self.f, self.b) if self.layout == Layout.INTERLEAVED else (n, 2, self.f, self.b)
+
+    def r_shape(self, n: int):
+        return ((n, self.n_ant, self.b) if self.layout == Layout.INTERLEAVED
+                else (n, 2, self.n_ant, self.b))
+
+    def w_shape(self, g: int):
+        return ((g, self.n_ant, self.f) if self.layout == Layout.INTERLEAVED
+                else (g, 2, self.n_ant, self.f))
+
+    @property
+    def dtype(self):
+        return torch.complex64 if self.layout == Layout.INTERLEAVED else torch.float32
+
+    def _check(self, t: torch.Tensor, name: str, shape, device=True):
+        if t.dtype != self.dtype:
+            raise TypeError(f"{name} must be {self.dtype}, got {t.dtype}")
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        if device and t.device != self.device:
+            raise ValueError(f"{name} must be on {self.device}, got {t.device}")
+        if not device and t.device.type != "cpu":
+            raise ValueError(f"{name} must be a host tensor")
+
+    # -- the calls of include/bf.h ------------------------------------------------
+    def set_precoders(self, W: torch.Tensor, stream=None) -> "Plan":
+        """bf_set_precoders: W [G][64][f] complex64 (interleaved) or [G][2][64][f] float32."""
+        if W.dim() == (2 if self.layout == Layout.INTERLEAVED else 3):
+            W = W.unsqueeze(0)
+        G = W.shape[0]
+        self._check(W, "W", self.w_shape(G))
+        check(lib().bf_set_precoders(self._h, _ptr(W), G, _stream_handle(stream)))
+        self.n_groups = G
+        self._w_ref = W          # keep alive until the relayout has run
+        return self
+
+    def apply(self, S: torch.Tensor, group_idx: torch.Tensor | None = None,
+              out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """bf_apply on device tensors; returns R (allocated if out is None)."""
+        n = S.shape[0]
+        self._check(S, "S", self.s_shape(n))
+        if out is None:
+            out = torch.empty(self.r_shape(n), dtype=self.dtype, device=self.device)
+        self._check(out, "out", self.r_shape(n))
+        if group_idx is not None:
+            if group_idx.dtype != torch.int32 or tuple(group_idx.shape) != (n,) \
+                    or group_idx.device != self.device or not group_idx.is_contiguous():
+                raise ValueError("group_idx must be a contiguous int32 [n] tensor on the plan device")
+        check(lib().bf_apply(self._h, _ptr(S), _ptr(group_idx), _ptr(out), n,
+                             _stream_handle(stream)))
+        return out
+
+    def apply_host(self, S: torch.Tensor, group_idx: torch.Tensor | None, out: torch.Tensor,
+                   stream=None) -> torch.Tensor:
+        """bf_apply_host on host tensors (pinned for full speed)."""
+        n = S.shape[0]
+        self._check(S, "S", self.s_shape(n), device=False)
+        self._check(out, "out", self.r_shape(n), device=False)
+        if group_idx is not None and (group_idx.dtype != torch.int32 or
+                                      tuple(group_idx.shape) != (n,) or group_idx.is_cuda):
+            raise ValueError("group_idx must be a host int32 [n] tensor")
+        check(lib().bf_apply_host(self._h, _ptr(S), _ptr(group_idx), _ptr(out), n,
+                                  _stream_handle(stream)))
+        return out
+
+    def route(self, group_idx: torch.Tensor, stream=None):
+        """bf_route: (perm int32 [n], offsets int32 [G + 2]) of the stable sort by tag."""
+        n = group_idx.shape[0]
+        perm = torch.empty(n, dtype=torch.int32, device=self.device)
+        offsets = torch.empty(self.n_groups + 2, dtype=torch.int32, device=self.device)
+        check(lib().bf_route(self._h, _ptr(group_idx), n, _ptr(perm), _ptr(offsets),
+                             _stream_handle(stream)))
+        return perm, offsets
+
+    # -- instrumentation --------------------------------------------------------------
+    def set_profiling(self, enable: bool = True) -> None:
+        check(lib().bf_plan_set_profiling(self._h, int(bool(enable))))
+
+    def kernel_time(self):
+        """(summed ms, launches) of the beamforming kernel since the last call."""
+        ms, nl = ctypes.c_double(), ctypes.c_int64()
+        check(lib().bf_plan_kernel_time(self._h, ctypes.byref(ms), ctypes.byref(nl)))
+        return ms.value, nl.value
+
+    def launch_count(self) -> int:
+        c = ctypes.c_int64()
+        check(lib().bf_plan_launch_count(self._h, ctypes.byref(c)))
+        return c.value
+
+    def set_host_chunk(self, blocks: int) -> None:
+        check(lib().bf_plan_set_host_chunk(self._h, int(blocks)))
+
+    def kernel_config(self, n_blocks: int) -> dict:
+        g, b, s, c = (ctypes.c_int() for _ in range(4))
+        check(lib().bf_plan_kernel_config(self._h, int(n_blocks), ctypes.byref(g), ctypes.byref(b),
+                                          ctypes.byref(s), ctypes.byref(c)))
+        return {"grid": g.value, "block": b.value, "smem_bytes": s.value, "ctas_per_sm": c.value}
+
+    def close(self) -> None:
+        if self._h:
+            check(lib().bf_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def plan_create_status(n_ant: int, f: int, b: int, layout: int = 0) -> Status:
+    """bf_plan_create's status for the given dimensions (destroys the plan on success)."""
+    h = ctypes.c_void_p()
+    s = lib().bf_plan_create(n_ant, f, b, layout, ctypes.byref(h))
+    if s == 0:
+        lib().bf_destroy(h)
+    return Status(s)
+
+
+__all__ = ["Plan", "Layout", "Status", "BfError", "plan_create_status", "N_ANT", "N_RE", "MAX_F"]

@@ -1,0 +1,386 @@
+"""GPU parity: libbf.so (through the C ABI binding) against the CPU oracle.
+
+Every case uses seeded bf_synth inputs.  Small cases compare every element;
+full BASELINE.json sizes run in the bench's launch configuration and compare
+sampled blocks (regenerated on the host by block id) plus properties.
+Tolerance: |R_gpu - R_ref| <= 1e-5 * T element-wise (BASELINE.json north_star
+item 4); bitwise for f = 0 and copy-like W (identity, selection, permutation).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import bf_synth as syn
+import oracle
+from helpers import TOL, assert_bitwise, assert_parity
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():   # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import bf_synth.cuda as sync  # noqa: E402
+import paper_1810_11451_b200 as bf  # noqa: E402
+from paper_1810_11451_b200 import Layout, Plan  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+NT = oracle.max_threads()
+
+
+def run_plan(W, S, tags=None, layout=Layout.INTERLEAVED):
+    """Device run of the numpy inputs; returns R as complex64 numpy [n][64][60]."""
+    f = W.shape[-1]
+    plan = Plan(f=f, layout=layout)
+    if layout == Layout.PLANAR:
+        Wd = torch.from_numpy(syn.to_planar(W)).to(DEV)
+        Sd = torch.from_numpy(syn.to_planar(S)).to(DEV)
+    else:
+        Wd = torch.from_numpy(np.ascontiguousarray(W)).to(DEV)
+        Sd = torch.from_numpy(np.ascontiguousarray(S)).to(DEV)
+    plan.set_precoders(Wd)
+    td = None if tags is None else torch.from_numpy(tags).to(DEV)
+    R = plan.apply(Sd, td)
+    torch.cuda.synchronize()
+    R = R.cpu().numpy()
+    plan.close()
+    return syn.from_planar(R) if layout == Layout.PLANAR else R
+
+
+# ---------------------------------------------------------------------------
+# full-element parity at oracle-friendly sizes
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("layout", [Layout.INTERLEAVED, Layout.PLANAR])
+def test_c1_full(layout):
+    wl = syn.workload("c1")
+    W, S, _ = syn.workload_inputs(wl)
+    R_ref, T, _ = oracle.beamform(W, S, n_threads=NT)
+    R = run_plan(W, S, layout=layout)
+    assert_parity(R, R_ref, T, what="c1")
+
+
+def test_c2_full():
+    wl = syn.workload("c2")
+    W, S, _ = syn.workload_inputs(wl)
+    R_ref, T, _ = oracle.beamform(W, S, n_threads=NT)
+    R = run_plan(W, S)
+    worst = assert_parity(R, R_ref, T, what="c2")
+    assert worst < 1e-6     # FFMA path is far inside the bound
+
+
+@pytest.mark.parametrize("layout", [Layout.INTERLEAVED, Layout.PLANAR])
+@pytest.mark.parametrize("f", syn.C3_FLOWS)
+def test_c3_every_f_ragged(f, layout):
+    """Every f of the sweep at a ragged block count spanning several CTAs' ranges."""
+    wl = syn.workload("c3", f)
+    ids = np.arange(0, 1237)
+    W, S, _ = syn.workload_inputs(wl, ids)
+    R_ref, T, _ = oracle.beamform(W, S, n_threads=NT)
+    R = run_plan(W, S, layout=layout)
+    if f == 0:
+        assert not R.view(np.uint32).any()
+    assert_parity(R, R_ref, T, what=f"c3 f={f}")
+
+
+@pytest.mark.parametrize("f", list(range(1, 37)))
+def test_every_instantiation(f):
+    """Each of the 36 compiled f values (odd K, non-powers of two) against the oracle."""
+    W = syn.precoders(99, f, 3, 64, f, "unit_columns")
+    S = syn.qam_symbols(99, f, np.arange(40), f, 60, 64)
+    tags = syn.subband_tags(99, np.arange(40), 3)
+    R_ref, T, _ = oracle.beamform(W, S, tags, n_threads=NT)
+    assert_parity(run_plan(W, S, tags), R_ref, T, what=f"f={f}")
+    assert_parity(run_plan(W, S, tags, Layout.PLANAR), R_ref, T, what=f"f={f} planar")
+
+
+def test_grouped_small_full():
+    """c4 shape (55 groups, tags) at a size the oracle covers completely."""
+    wl = syn.workload("c4")
+    ids = np.arange(3001)
+    W, S, tags = syn.workload_inputs(wl, ids)
+    R_ref, T, _ = oracle.beamform(W, S, tags, n_threads=NT)
+    assert_parity(run_plan(W, S, tags), R_ref, T, what="c4 small")
+
+
+# ---------------------------------------------------------------------------
+# exactness fixtures (bitwise)
+# ---------------------------------------------------------------------------
+def test_f0_is_positive_zero():
+    plan = Plan(f=0)
+    plan.set_precoders(torch.zeros((1, 64, 0), dtype=torch.complex64, device=DEV))
+    R = torch.full((7, 64, 60), float("nan"), dtype=torch.complex64, device=DEV)
+    plan.apply(torch.zeros((7, 0, 60), dtype=torch.complex64, device=DEV), out=R)
+    torch.cuda.synchronize()
+    assert not R.cpu().numpy().view(np.uint32).any()
+
+
+@pytest.mark.parametrize("layout", [Layout.INTERLEAVED, Layout.PLANAR])
+@pytest.mark.parametrize("f", [1, 8, 17, 36])
+def test_identity_and_selection_bitwise(f, layout):
+    S = syn.qam_symbols(5, 0, np.arange(50), f, 60, 64)
+    W = np.zeros((2, 64, f), np.complex64)
+    W[0, np.arange(f), np.arange(f)] = 1                   # identity [I_f; 0]
+    rng = np.random.default_rng(f)
+    sigma = rng.integers(0, f, size=64)
+    sigma[:f] = rng.permutation(f)
+    W[1, np.arange(64), sigma] = 1                          # selection / permutation
+    tags = (np.arange(50) % 2).astype(np.int32)
+    R = run_plan(W, S, tags, layout)
+    R_ref, _, _ = oracle.beamform(W, S, tags)
+    assert_bitwise(R, R_ref, "copy-like W vs oracle")
+    assert_bitwise(R[0::2, :f], S[0::2], "identity rows")
+    assert not R[0::2, f:].view(np.uint32).any()
+    assert_bitwise(R[1::2], S[1::2][:, sigma], "selection rows")
+
+
+def test_gaussian_integers_bitwise_at_full_shape():
+    """Integer partial sums < 2^24 are exact in any order: GPU == oracle bitwise."""
+    rng = np.random.default_rng(3)
+    G, f = 55, 36
+    W = (rng.integers(-3, 4, (G, 64, f)) + 1j * rng.integers(-3, 4, (G, 64, f))).astype(np.complex64)
+    S = syn.qam_symbols(11, 0, np.arange(500), f, 60, 64, normalised=False)
+    tags = syn.subband_tags(3, np.arange(500), G)
+    R_ref, _, _ = oracle.beamform(W, S, tags, n_threads=NT)
+    assert_bitwise(run_plan(W, S, tags), R_ref, "gaussian integers")
+
+
+def test_power_of_two_scaling_and_one_real_nonzero():
+    wl = syn.workload("c2")
+    W, S, _ = syn.workload_inputs(wl, np.arange(64))
+    R1 = run_plan(W, S)
+    R2 = run_plan((W * np.float32(4.0)).astype(np.complex64), S)
+    assert_bitwise(R2, R1 * np.float32(4.0), "2^e scaling")
+    f = 12
+    rng = np.random.default_rng(2)
+    sigma = rng.integers(0, f, size=64)
+    Wc = np.zeros((1, 64, f), np.complex64)
+    Wc[0, np.arange(64), sigma] = rng.standard_normal(64).astype(np.float32)
+    S = syn.qam_symbols(9, 0, np.arange(20), f, 60, 64)
+    R_ref, _, _ = oracle.beamform(Wc, S)
+    assert_bitwise(run_plan(Wc, S), R_ref, "one real nonzero per row")
+
+
+def test_conjugation_symmetry_bitwise():
+    wl = syn.workload("c2")
+    W, S, _ = syn.workload_inputs(wl, np.arange(32))
+    R = run_plan(W, S)
+    Rc = run_plan(np.conj(W), np.conj(S))
+    assert_bitwise(Rc, np.conj(R), "conjugation symmetry")
+
+
+def test_linearity_in_S_and_W():
+    wl = syn.workload("c3", 24)
+    W, S1, _ = syn.workload_inputs(wl, np.arange(30))
+    S2 = syn.qam_symbols(8, 1, np.arange(30), 24, 60, 64)
+    W2 = syn.precoders(8, 2, 1, 64, 24, "unit_columns")
+    R_ref, T, _ = oracle.beamform(W, S1 + S2, n_threads=NT)
+    R = run_plan(W, S1) + run_plan(W, S2)
+    assert_parity(R, R_ref, T, tol=2 * TOL, what="linearity in S")
+    R_ref, T, _ = oracle.beamform(W + W2, S1, n_threads=NT)
+    R = run_plan(W, S1) + run_plan(W2, S1)
+    assert_parity(R, R_ref, T, tol=2 * TOL, what="linearity in W")
+
+
+# ---------------------------------------------------------------------------
+# properties: determinism, batch independence, layouts, host path
+# ---------------------------------------------------------------------------
+def test_determinism_and_batch_independence():
+    wl = syn.workload("c4")
+    W, S, tags = syn.workload_inputs(wl, np.arange(2000))
+    a = run_plan(W, S, tags)
+    b = run_plan(W, S, tags)
+    assert_bitwise(a, b, "repeat")
+    c = run_plan(W, S[700:1300], tags[700:1300])
+    assert_bitwise(c, a[700:1300], "sub-batch")
+    d = run_plan(W, S[:1], tags[:1])
+    assert_bitwise(d, a[:1], "single block")
+
+
+def test_planar_equals_interleaved_bitwise():
+    wl = syn.workload("c3", 31)
+    W, S, _ = syn.workload_inputs(wl, np.arange(300))
+    assert_bitwise(run_plan(W, S, layout=Layout.PLANAR), run_plan(W, S), "layouts")
+
+
+def test_device_generator_matches_host_generator():
+    for wl, planar in ((syn.workload("c4"), False), (syn.workload("c3", 17), True),
+                       (syn.workload("c1"), False)):
+        ids = np.array([0, 1, 2, 777, wl.n_blocks - 1], dtype=np.int64)
+        Sd, td = sync.workload_device(wl, DEV, ids=torch.from_numpy(ids).to(DEV), planar=planar)
+        _, S, tags = syn.workload_inputs(wl, ids)
+        got = Sd.cpu().numpy()
+        assert_bitwise(syn.from_planar(got) if planar else got, S, f"generator {wl.name}")
+        if tags is not None:
+            assert np.array_equal(td.cpu().numpy(), tags)
+    ids = np.arange(5000, 5100, dtype=np.int64)
+    m = torch.empty(100, dtype=torch.int32, device=DEV)
+    sync.gen_modulations(m, 4, ids=torch.from_numpy(ids).to(DEV))
+    assert np.array_equal(m.cpu().numpy(), syn.block_modulations(4, ids))
+    S = torch.empty((100, 20, 60), dtype=torch.complex64, device=DEV)
+    sync.gen_symbols(S, 4, 3, 20, 60, 0, ids=torch.from_numpy(ids).to(DEV))
+    assert_bitwise(S.cpu().numpy(),
+                   syn.qam_symbols(4, 3, ids, 20, 60, syn.block_modulations(4, ids)), "mixed QAM")
+
+
+@pytest.mark.parametrize("tagged", [False, True])
+def test_apply_host_equals_apply(tagged):
+    wl = syn.workload("c4")
+    W, S, tags = syn.workload_inputs(wl, np.arange(5000))
+    if not tagged:
+        W, tags = W[:1], None
+    plan = Plan(f=36)
+    plan.set_host_chunk(1024)     # several chunks, ragged tail, all three slots
+    plan.set_precoders(torch.from_numpy(W).to(DEV))
+    S_h = torch.from_numpy(S).pin_memory()
+    t_h = None if tags is None else torch.from_numpy(tags).pin_memory()
+    R_h = torch.empty((5000, 64, 60), dtype=torch.complex64).pin_memory()
+    plan.apply_host(S_h, t_h, R_h)
+    torch.cuda.synchronize()
+    Rd = plan.apply(torch.from_numpy(S).to(DEV), None if tags is None else t_h.to(DEV))
+    torch.cuda.synchronize()
+    assert_bitwise(R_h.numpy(), Rd.cpu().numpy(), "host pipeline")
+    plan.close()
+
+
+# ---------------------------------------------------------------------------
+# routing (a3): bit-exact index work
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n,G", [(1, 55), (4095, 55), (4097, 2), (100_003, 55), (70_000, 1024)])
+def test_route_is_stable_counting_sort(n, G):
+    tags = syn.subband_tags(12, np.arange(n), G)
+    plan = Plan(f=4)
+    plan.set_precoders(torch.zeros((G, 64, 4), dtype=torch.complex64, device=DEV))
+    perm, offs = plan.route(torch.from_numpy(tags).to(DEV))
+    torch.cuda.synchronize()
+    assert np.array_equal(perm.cpu().numpy(), np.argsort(tags, kind="stable"))
+    starts = np.concatenate([[0], np.cumsum(np.bincount(tags, minlength=G))])
+    assert np.array_equal(offs.cpu().numpy(), np.concatenate([starts, [n]]))
+
+
+def test_invalid_tags_are_left_unwritten_and_checked(monkeypatch):
+    wl = syn.workload("c4")
+    W, S, tags = syn.workload_inputs(wl, np.arange(300))
+    tags = tags.copy()
+    tags[[5, 17]] = [55, -1]
+    plan = Plan(f=36)
+    plan.set_precoders(torch.from_numpy(W).to(DEV))
+    Sd, td = torch.from_numpy(S).to(DEV), torch.from_numpy(tags).to(DEV)
+    R = torch.full((300, 64, 60), 7.0, dtype=torch.complex64, device=DEV)
+    plan.apply(Sd, td, out=R)
+    torch.cuda.synchronize()
+    Rn = R.cpu().numpy()
+    assert (Rn[[5, 17]] == 7.0).all()
+    ok = np.setdiff1d(np.arange(300), [5, 17])
+    R_ref, T, _ = oracle.beamform(W, S[ok], tags[ok], n_threads=NT)
+    assert_parity(Rn[ok], R_ref, T, what="valid blocks beside invalid tags")
+    monkeypatch.setenv("BF_CHECK", "1")
+    with pytest.raises(bf.BfError) as e:
+        plan.apply(Sd, td, out=R)
+    assert e.value.status == bf.Status.INVALID_VALUE
+
+
+# ---------------------------------------------------------------------------
+# error paths of the C ABI
+# ---------------------------------------------------------------------------
+def test_error_paths():
+    L = bf.lib()
+    plan = Plan(f=8)
+    S = torch.zeros((4, 8, 60), dtype=torch.complex64, device=DEV)
+    with pytest.raises(bf.BfError) as e:
+        plan.apply(S)
+    assert e.value.status == bf.Status.NO_PRECODERS
+    plan.set_precoders(torch.zeros((64, 8), dtype=torch.complex64, device=DEV))
+    buf = torch.zeros(4 * 8 * 60 * 2 + 2, dtype=torch.float32, device=DEV)
+    R = torch.zeros((4, 64, 60), dtype=torch.complex64, device=DEV)
+    import ctypes
+    st = L.bf_apply(plan._h, ctypes.c_void_p(buf.data_ptr() + 8), None,
+                    ctypes.c_void_p(R.data_ptr()), 4, None)
+    assert st == bf.Status.MISALIGNED
+    big = torch.zeros(4 * 7680 + 4 * 960, dtype=torch.float32, device=DEV)
+    st = L.bf_apply(plan._h, ctypes.c_void_p(big.data_ptr()), None,
+                    ctypes.c_void_p(big.data_ptr() + 4 * 960 * 4 - 512), 4, None)
+    assert st == bf.Status.INVALID_VALUE                     # R overlaps S
+    assert L.bf_apply(plan._h, None, None, None, 0, None) == bf.Status.OK   # n = 0 no-op
+    assert L.bf_apply(plan._h, None, None, ctypes.c_void_p(R.data_ptr()), -1, None) == \
+        bf.Status.INVALID_VALUE
+    assert L.bf_set_precoders(plan._h, ctypes.c_void_p(R.data_ptr()), 1025, None) == \
+        bf.Status.UNSUPPORTED
+    with pytest.raises(ValueError):
+        plan.apply(torch.zeros((4, 7, 60), dtype=torch.complex64, device=DEV))
+    plan.close()
+
+
+# ---------------------------------------------------------------------------
+# full BASELINE.json sizes in the bench's launch configuration, sampled parity
+# ---------------------------------------------------------------------------
+def _sampled_check(wl, R_dev, n_sample=96, planar=False, seed=0):
+    rng = np.random.default_rng(seed)
+    n = wl.n_blocks
+    ids = np.unique(np.concatenate([[0, 1, n - 2, n - 1], rng.integers(0, n, n_sample)]))
+    W, S, tags = syn.workload_inputs(wl, ids)
+    R_ref, T, _ = oracle.beamform(W, S, tags, n_threads=NT)
+    got = R_dev[torch.from_numpy(ids).to(R_dev.device)].cpu().numpy()
+    if planar:
+        got = syn.from_planar(got)
+    return assert_parity(got, R_ref, T, what=f"{wl.name} sampled")
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled():
+    wl = syn.workload("c4")
+    W = syn.precoders(wl.seed, wl.sub, wl.n_groups, wl.n_ant, wl.f, wl.w_norm)
+    Sd, td = sync.workload_device(wl, DEV)
+    plan = Plan(f=36)
+    plan.set_precoders(torch.from_numpy(W).to(DEV))
+    R = plan.apply(Sd, td)
+    torch.cuda.synchronize()
+    del Sd
+    _sampled_check(wl, R, n_sample=160)
+    # property at full size: every block was written (no NaN sentinel survives)
+    assert torch.isfinite(torch.view_as_real(R)).all().item()
+    plan.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("f", [1, 7, 16, 36])
+@pytest.mark.parametrize("layout", [Layout.INTERLEAVED, Layout.PLANAR])
+def test_c3_full_size_sampled(f, layout):
+    wl = syn.workload("c3", f)
+    planar = layout == Layout.PLANAR
+    W = syn.precoders(wl.seed, wl.sub, 1, 64, f, wl.w_norm)
+    Sd, _ = sync.workload_device(wl, DEV, planar=planar)
+    plan = Plan(f=f, layout=layout)
+    plan.set_precoders(torch.from_numpy(syn.to_planar(W) if planar else W).to(DEV))
+    R = plan.apply(Sd)
+    torch.cuda.synchronize()
+    _sampled_check(wl, R, planar=planar)
+    plan.close()
+
+
+@pytest.mark.slow
+def test_c5_sampled_chunks():
+    """c5: 4096-block chunks of 8 cells with per-cell f and mixed modulation (sampled chunks)."""
+    wl = syn.workload("c5")
+    fc = syn.cell_flows(wl.seed, 8)
+    for chunk in (0, 5, 1234, 2047):
+        cell = chunk % 8
+        f = int(fc[cell])
+        ids = np.arange(chunk * 4096, (chunk + 1) * 4096, dtype=np.int64)
+        W = syn.precoders(wl.seed, cell, 55, 64, f, "none")
+        tags = syn.subband_tags(wl.seed, ids, 55)
+        mods = syn.block_modulations(wl.seed, ids)
+        Sd = torch.empty((4096, f, 60), dtype=torch.complex64, device=DEV)
+        sync.gen_symbols(Sd, wl.seed, 0, f, 60, 0, first=int(ids[0]))
+        td = torch.empty(4096, dtype=torch.int32, device=DEV)
+        sync.gen_tags(td, wl.seed, 55, first=int(ids[0]))
+        plan = Plan(f=f)
+        plan.set_precoders(torch.from_numpy(W).to(DEV))
+        R = plan.apply(Sd, td)
+        torch.cuda.synchronize()
+        sel = np.arange(0, 4096, 97)
+        S = syn.qam_symbols(wl.seed, 0, ids[sel], f, 60, mods[sel])
+        R_ref, T, _ = oracle.beamform(W, S, tags[sel], n_threads=NT)
+        assert_parity(R[torch.from_numpy(sel).to(DEV)].cpu().numpy(), R_ref, T,
+                      what=f"c5 chunk {chunk} (cell {cell}, f={f})")
+        plan.close()
