@@ -242,14 +242,20 @@ def run_ours(args):
     hbm = peaks["hbm_gbs"]
     ai = wl.block_flops / wl.block_bytes
     fp32_bound = ai * hbm / 1e3 > peak_max            # TFLOP/s reachable from HBM vs FFMA peak
-    traffic = None
+    # dram bytes of the same kernel from the committed `ncu --set full` capture
+    # (profiles/traffic.json, per block), scaled to this launch's block count
+    traffic, traffic_basis = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    kname = f"bf_ffma_kernel<{wl.f},{1 if planar else 0}>"
     if os.path.exists(tpath):
         try:
-            tr = json.load(open(tpath)).get(f"{wl.name}:{args.layout}:n{n_local}")
-            traffic = tr
+            tr = json.load(open(tpath)).get(kname)
         except ValueError:
-            traffic = None
+            tr = None
+        if tr:
+            traffic = tr["dram_bytes_per_block"] * n_local
+            traffic_basis = (f"{tr['capture']}: {tr['dram_bytes_per_block']:.0f} B/block "
+                             f"x {n_local} blocks")
     if fp32_bound:
         roof = {"bound": "alu", "achieved": achieved_tf, "peak": peak_max, "unit": "TFLOP/s",
                 "frac": achieved_tf / peak_max, "traffic": traffic,
@@ -262,6 +268,7 @@ def run_ours(args):
     if clk and clk.get("sm_mhz"):
         roof["frac_at_observed_clock"] = achieved_tf / benchkit.fp32_peak_tflops(sms, clk["sm_mhz"]) \
             if fp32_bound else None
+    roof["traffic_basis"] = traffic_basis
     roof["kernel_ms"] = kern_avg_ms
     roof["kernel_share_of_step"] = kern_avg_ms * args.steps / elapsed_ms
     roof["algorithmic_bytes_per_launch"] = bytes_launch

@@ -68,8 +68,9 @@ void init_table() {
 // Device helpers: W relayout (a2) and routing (a3)
 // ---------------------------------------------------------------------------
 
-// Wp[g][k][j][ag] = float4(w[8ag+2j][k], w[8ag+2j+1][k]) — the layout bf_ffma_kernel
-// reads with one conflict-free LDS.128 per (k, j).
+// Wp[g][k][j][ag] = float4(re w[8ag+2j][k], re w[8ag+2j+1][k], im w[8ag+2j][k],
+// im w[8ag+2j+1][k]) — the layout bf_ffma_kernel reads with one conflict-free
+// LDS.128 per (k, j); re and im of one antenna land in same-parity registers.
 __global__ void bf_relayout_w(const float *__restrict__ W, int n_groups, int F, int layout,
                               float4 *__restrict__ Wp) {
     const int64_t total = (int64_t)n_groups * F * 32;
@@ -82,11 +83,11 @@ __global__ void bf_relayout_w(const float *__restrict__ W, int n_groups, int F, 
         float4 v;
         if (layout == BF_LAYOUT_INTERLEAVED) {
             const float *Wg = W + g * 64 * F * 2;
-            v = make_float4(Wg[(i0 * F + k) * 2], Wg[(i0 * F + k) * 2 + 1],
-                            Wg[(i1 * F + k) * 2], Wg[(i1 * F + k) * 2 + 1]);
+            v = make_float4(Wg[(i0 * F + k) * 2], Wg[(i1 * F + k) * 2],
+                            Wg[(i0 * F + k) * 2 + 1], Wg[(i1 * F + k) * 2 + 1]);
         } else {
             const float *Wr = W + g * 2 * 64 * F, *Wi = Wr + 64 * F;
-            v = make_float4(Wr[i0 * F + k], Wi[i0 * F + k], Wr[i1 * F + k], Wi[i1 * F + k]);
+            v = make_float4(Wr[i0 * F + k], Wr[i1 * F + k], Wi[i0 * F + k], Wi[i1 * F + k]);
         }
         Wp[idx] = v;
     }

@@ -8,20 +8,25 @@
 //    a contiguous range of the (group-sorted) block list, so W changes at most
 //    a few times per CTA.
 //  * W of the current group lives in shared memory, pre-laid-out by
-//    bf_set_precoders as Wp[k][j][ag] float4 = (w[8ag+2j][k], w[8ag+2j+1][k]),
-//    512*F bytes, loaded with one cp.async.bulk (TMA bulk copy) per change.
+//    bf_set_precoders as Wp[k][j][ag] float4 = (re w[8ag+2j][k], re w[8ag+2j+1][k],
+//    im w[8ag+2j][k], im w[8ag+2j+1][k]), 512*F bytes, loaded with one
+//    cp.async.bulk (TMA bulk copy) per group change.
 //  * S blocks (480*F contiguous bytes, either layout) stream HBM -> shared
 //    through a 2-stage ring filled by cp.async.bulk with mbarrier completion,
 //    two blocks ahead of compute.
 //  * Each thread owns an 8-antenna x 5-RE register tile (80 fp32 accumulators):
 //    antennas 8ag..8ag+7, REs rg, rg+12, .., rg+48 (ag = t/12, rg = t%12).  Per
 //    k it reads 4 LDS.128 of W (conflict-free, broadcast across rg) and 5 S
-//    values, and issues 160 FFMA: re = fma(wr,sr,re); re = fma(-wi,si,re);
-//    im = fma(wr,si,im); im = fma(wi,sr,im).  The paper's three fixes carry
+//    values, and issues 160 FFMA: re = fma(wr,sr,re); im = fma(wi,sr,im) for all
+//    8 antennas per S value, then re = fma(-wi,si,re); im = fma(wr,si,im).  The
+//    order keeps one S operand in the reuse cache for runs of 16 FFMAs, so only
+//    W and the accumulator are read from the register file (register-bank
+//    conflicts were the top issue stall, see profiles/).  The paper's three fixes carry
 //    over: no extra FLOPs, every product fused, no permutes (re/im sit in
 //    separate registers).  Accumulators start at +0.0f (bit-exact identity).
-//  * Results go straight from registers to HBM with streaming stores; a warp's
-//    store instruction covers whole 32-byte sectors (12 consecutive REs of a row).
+//  * Results go straight from registers to HBM with streaming 32-bit stores
+//    (re and im separately, so no even/odd pairing constrains the accumulators);
+//    a warp's two stores of a row cover whole 32-byte sectors.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -193,18 +198,30 @@ __global__ void __launch_bounds__(kThreads, 4) bf_ffma_kernel(const KParams p) {
                         si[r] = S[F * kB + k * kB + rg + kRG * r];
                     }
                 }
+                // w[j] = (wr[2j], wr[2j+1], wi[2j], wi[2j+1]): wr[a] and wi[a] land in
+                // registers of the same parity, so with the S operand held in the
+                // reuse cache across a run of 16 FFMAs the two uncached operands
+                // (W and the accumulator) can sit in different register banks.
+                float wr[kTA], wi[kTA];
 #pragma unroll
-                for (int a = 0; a < kTA; ++a) {
-                    const float wr = (a & 1) ? w[a >> 1].z : w[a >> 1].x;
-                    const float wi = (a & 1) ? w[a >> 1].w : w[a >> 1].y;
-#pragma unroll
-                    for (int r = 0; r < kTR; ++r) {
-                        are[a][r] = fmaf(wr, sr[r], are[a][r]);
-                        are[a][r] = fmaf(-wi, si[r], are[a][r]);
-                        aim[a][r] = fmaf(wr, si[r], aim[a][r]);
-                        aim[a][r] = fmaf(wi, sr[r], aim[a][r]);
-                    }
+                for (int j = 0; j < 4; ++j) {
+                    wr[2 * j] = w[j].x; wr[2 * j + 1] = w[j].y;
+                    wi[2 * j] = w[j].z; wi[2 * j + 1] = w[j].w;
                 }
+#pragma unroll
+                for (int r = 0; r < kTR; ++r)
+#pragma unroll
+                    for (int a = 0; a < kTA; ++a) {
+                        are[a][r] = fmaf(wr[a], sr[r], are[a][r]);
+                        aim[a][r] = fmaf(wi[a], sr[r], aim[a][r]);
+                    }
+#pragma unroll
+                for (int r = 0; r < kTR; ++r)
+#pragma unroll
+                    for (int a = 0; a < kTA; ++a) {
+                        are[a][r] = fmaf(-wi[a], si[r], are[a][r]);
+                        aim[a][r] = fmaf(wr[a], si[r], aim[a][r]);
+                    }
             }
         }
         __syncthreads();                       // stage `stage` and meta are free again
@@ -219,8 +236,11 @@ __global__ void __launch_bounds__(kThreads, 4) bf_ffma_kernel(const KParams p) {
                 for (int r = 0; r < kTR; ++r) {
                     const int j = rg + kRG * r;
                     if (LAYOUT == 0) {
-                        __stcs(reinterpret_cast<float2 *>(Rb) + i * kB + j,
-                               make_float2(are[a][r], aim[a][r]));
+                        // two 32-bit stores instead of one float2: a 64-bit store would
+                        // pin (re, im) to an even/odd register pair for the whole k loop,
+                        // which forces register-bank conflicts in half of the FFMAs.
+                        __stcs(Rb + 2 * (i * kB + j), are[a][r]);
+                        __stcs(Rb + 2 * (i * kB + j) + 1, aim[a][r]);
                     } else {
                         __stcs(Rb + i * kB + j, are[a][r]);
                         __stcs(Rb + kAnt * kB + i * kB + j, aim[a][r]);
