@@ -75,6 +75,19 @@ typedef enum {
     BF_LAYOUT_PLANAR = 1
 } bf_layout;
 
+/* Kernel variant.  Both compute the same product within the same contract.
+ *   BF_VARIANT_FFMA    CUDA-core kernel: 4 fp32 FFMA per complex MAC.
+ *   BF_VARIANT_TENSOR  tcgen05 tensor-core kernel: S split into 3 tf32 terms,
+ *                      W into 2, four kind::tf32 MMAs per K step, fp32
+ *                      accumulation in TMEM (error-compensated split precision,
+ *                      BASELINE.json north_star item 2).
+ *   BF_VARIANT_AUTO    per-f choice from the measured variant table (default). */
+typedef enum {
+    BF_VARIANT_AUTO = 0,
+    BF_VARIANT_FFMA = 1,
+    BF_VARIANT_TENSOR = 2
+} bf_variant;
+
 typedef enum {
     BF_OK = 0,
     BF_ERR_INVALID_VALUE = 1,   /* NULL / negative / overlapping / wrong-device argument */
@@ -137,6 +150,12 @@ bf_status bf_destroy(bf_plan_t p);
 bf_status bf_plan_set_profiling(bf_plan_t p, int enable);
 bf_status bf_plan_kernel_time(bf_plan_t p, double *total_ms, int64_t *n_launches);
 bf_status bf_plan_launch_count(bf_plan_t p, int64_t *count);
+
+/* Select the kernel variant (a bf_variant) used by later applies of this plan;
+ * get_variant reports the variant AUTO resolves to for this plan's f
+ * (BF_VARIANT_AUTO itself when f == 0, which only writes zeros). */
+bf_status bf_plan_set_variant(bf_plan_t p, int variant);
+bf_status bf_plan_get_variant(bf_plan_t p, int *resolved);
 
 /* Chunk size (blocks) of bf_apply_host's pipeline; 0 selects the default. */
 bf_status bf_plan_set_host_chunk(bf_plan_t p, int64_t blocks);

@@ -5,9 +5,9 @@ f x 60 block of symbols, 0 <= f <= 36.  The computation runs in libbf.so
 (hand-written sm_100a CUDA, C ABI in include/bf.h); this package is its thin
 Python binding.  Importing it loads libbf.so and fails loudly if it is absent.
 """
-from ._lib import BfError, Layout, Status, lib
+from ._lib import BfError, Layout, Status, Variant, lib
 from .plan import MAX_F, N_ANT, N_RE, Plan, plan_create_status
 
 lib()   # load now: no silent fallback path exists
 
-__all__ = ["Plan", "Layout", "Status", "BfError", "plan_create_status", "N_ANT", "N_RE", "MAX_F"]
+__all__ = ["Plan", "Layout", "Status", "Variant", "BfError", "plan_create_status", "N_ANT", "N_RE", "MAX_F"]

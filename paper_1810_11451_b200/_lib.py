@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbf.so")
 EXPORTS = ("bf_plan_create", "bf_set_precoders", "bf_apply", "bf_apply_host", "bf_route",
            "bf_destroy", "bf_plan_set_profiling", "bf_plan_kernel_time",
            "bf_plan_launch_count", "bf_plan_set_host_chunk", "bf_plan_kernel_config",
+           "bf_plan_set_variant", "bf_plan_get_variant",
            "bf_status_string", "bf_last_error", "bf_version")
 
 
@@ -32,6 +33,12 @@ class Status(enum.IntEnum):
 class Layout(enum.IntEnum):
     INTERLEAVED = 0
     PLANAR = 1
+
+
+class Variant(enum.IntEnum):
+    AUTO = 0
+    FFMA = 1
+    TENSOR = 2
 
 
 class BfError(RuntimeError):
@@ -64,6 +71,8 @@ def lib() -> ctypes.CDLL:
         "bf_plan_kernel_time": (i32, [vp, P(ctypes.c_double), P(i64)]),
         "bf_plan_launch_count": (i32, [vp, P(i64)]),
         "bf_plan_set_host_chunk": (i32, [vp, i64]),
+        "bf_plan_set_variant": (i32, [vp, i32]),
+        "bf_plan_get_variant": (i32, [vp, P(i32)]),
         "bf_plan_kernel_config": (i32, [vp, i64, P(i32), P(i32), P(i32), P(i32)]),
         "bf_status_string": (ctypes.c_char_p, [i32]),
         "bf_last_error": (ctypes.c_char_p, []),

@@ -19,6 +19,7 @@
 #include "bf.h"
 #include "bf_dispatch.h"
 #include "bf_ffma.cuh"
+#include "bf_tc.cuh"
 
 namespace {
 
@@ -50,18 +51,21 @@ constexpr int kRouteMinTile = 4096;
 constexpr int kRouteMaxTable = 65536;      // tiles x (groups + 1) entries
 constexpr int64_t kDefaultHostChunk = 2048;
 constexpr int kHostSlots = 3;
+constexpr int kAutoTensorMinF = 99;         // AUTO = FFMA everywhere until measured
 
-BfKernelTable g_table;
+BfKernelTable g_table;      // FFMA kernels [f][layout]
+BfKernelTable g_table_tc;   // tcgen05 split-TF32 kernels [f][layout]
 std::once_flag g_table_once;
 
 void init_table() {
     std::memset(&g_table, 0, sizeof(g_table));
-    bf_register_f01_06(g_table);
-    bf_register_f07_12(g_table);
-    bf_register_f13_18(g_table);
-    bf_register_f19_24(g_table);
-    bf_register_f25_30(g_table);
-    bf_register_f31_36(g_table);
+    std::memset(&g_table_tc, 0, sizeof(g_table_tc));
+    bf_register_f01_06(g_table, g_table_tc);
+    bf_register_f07_12(g_table, g_table_tc);
+    bf_register_f13_18(g_table, g_table_tc);
+    bf_register_f19_24(g_table, g_table_tc);
+    bf_register_f25_30(g_table, g_table_tc);
+    bf_register_f31_36(g_table, g_table_tc);
 }
 
 // ---------------------------------------------------------------------------
@@ -92,6 +96,43 @@ __global__ void bf_relayout_w(const float *__restrict__ W, int n_groups, int F, 
         Wp[idx] = v;
     }
 }
+
+// Builds the pre-split B image of one or more groups (bf_set_precoders):
+// img[g][t][kc][ng][r][e] = term t of B'[n = 8 ng + r][kk = 4 kc + e].
+__global__ void bf_tc_build_wimg(const float *__restrict__ W, int n_groups, int F, int layout,
+                                 float *__restrict__ img) {
+    const int KP = bftc::kp_of(F);
+    const int64_t per_group = 2LL * KP * 128;
+    const int64_t total = (int64_t)n_groups * per_group;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = idx / per_group;
+        int rem = (int)(idx - g * per_group);
+        const int term = rem / (KP * 128);
+        rem -= term * KP * 128;
+        const int kc = rem / 512;           // 16 groups x 8 rows x 4 elements per K chunk
+        rem -= kc * 512;
+        const int ng = rem / 32, r = (rem / 4) % 8, e = rem % 4;
+        const int n = ng * 8 + r, kk = kc * 4 + e;
+        const int i = n >> 1, cout = n & 1, k = kk >> 1, cin = kk & 1;
+        float val = 0.0f;
+        if (k < F) {
+            float wr, wi;
+            if (layout == 0) {
+                wr = W[((g * 64 + i) * F + k) * 2];
+                wi = W[((g * 64 + i) * F + k) * 2 + 1];
+            } else {
+                wr = W[(g * 2 + 0) * 64 * F + i * F + k];
+                wi = W[(g * 2 + 1) * 64 * F + i * F + k];
+            }
+            // B'[2i][2k] = wr, B'[2i][2k+1] = -wi, B'[2i+1][2k] = wi, B'[2i+1][2k+1] = wr
+            val = cout == 0 ? (cin == 0 ? wr : -wi) : (cin == 0 ? wi : wr);
+        }
+        const float w1 = tc::to_tf32(val);
+        img[idx] = term == 0 ? w1 : tc::to_tf32(val - w1);
+    }
+}
+
 
 __device__ __forceinline__ int route_bin(int32_t g, int G) {
     return (unsigned)g < (unsigned)G ? g : G;   // invalid tags -> bin G (sorted last)
@@ -246,10 +287,14 @@ bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) %
 struct bf_plan_s {
     int n_ant = 64, f = 0, b = 60, layout = 0, device = 0, num_sms = 0;
     int n_groups = 0;
-    BfKernelEntry kern{};
+    BfKernelEntry kern{};       // FFMA kernel of this (f, layout)
+    BfKernelEntry kern_tc{};    // tensor-core kernel of this (f, layout)
     int ctas_per_sm = 0;
-    float4 *Wp = nullptr;
+    int variant = BF_VARIANT_AUTO;
+    float4 *Wp = nullptr;       // FFMA precoder image
     int64_t Wp_cap = 0;
+    float *Wimg = nullptr;      // tensor-core (pre-split B) precoder image
+    int64_t Wimg_cap = 0;
     // routing workspace
     int32_t *perm = nullptr, *gsorted = nullptr, *table = nullptr, *offsets = nullptr,
             *err = nullptr;
@@ -314,6 +359,13 @@ bf_status check_tags_if_requested(bf_plan_t p, cudaStream_t st) {
     return BF_OK;
 }
 
+// Per-f variant table: which kernel BF_VARIANT_AUTO runs.
+bool use_tensor(bf_plan_t p) {
+    if (p->variant == BF_VARIANT_TENSOR) return true;
+    if (p->variant == BF_VARIANT_FFMA) return false;
+    return p->f >= kAutoTensorMinF;
+}
+
 int grid_for(bf_plan_t p, int64_t n_items) {
     const int64_t cap = (int64_t)p->num_sms * std::max(1, p->ctas_per_sm);
     return (int)std::max<int64_t>(1, std::min<int64_t>(n_items, cap));
@@ -345,7 +397,17 @@ bf_status apply_device(bf_plan_t p, const void *S, const int32_t *gidx, void *R,
         kp.perm = p->perm;
         kp.gsorted = p->gsorted;
     }
-    const int grid = grid_for(p, n);
+    const bool tensor = use_tensor(p);
+    const int grid = tensor ? (int)std::min<int64_t>(n, p->num_sms) : grid_for(p, n);
+    const BfKernelEntry &kern = tensor ? p->kern_tc : p->kern;
+    bftc::TcParams tp{};
+    tp.Wimg = p->Wimg;
+    tp.S = kp.S;
+    tp.perm = kp.perm;
+    tp.gsorted = kp.gsorted;
+    tp.R = kp.R;
+    tp.n_items = n;
+    tp.n_groups = p->n_groups;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (p->profiling) {
         if (p->prof_used == p->prof_events.size()) {
@@ -359,11 +421,13 @@ bf_status apply_device(bf_plan_t p, const void *S, const int32_t *gidx, void *R,
         ++p->prof_used;
         BF_CUDA(cudaEventRecord(e0, st));
     }
-    void *args[] = {&kp};
-    cudaError_t e = cudaLaunchKernel(p->kern.fn, dim3(grid), dim3(bfk::kThreads), args,
-                                     (size_t)p->kern.smem_bytes, st);
-    if (e != cudaSuccess) return cuda_fail(e, "bf_ffma_kernel launch");
-    if ((s = launched(p, "bf_ffma_kernel launch")) != BF_OK) return s;
+    void *args_ffma[] = {&kp};
+    void *args_tc[] = {&tp};
+    cudaError_t e = cudaLaunchKernel(kern.fn, dim3(grid),
+                                     dim3(tensor ? bftc::kThreads : bfk::kThreads),
+                                     tensor ? args_tc : args_ffma, (size_t)kern.smem_bytes, st);
+    if (e != cudaSuccess) return cuda_fail(e, "beamforming kernel launch");
+    if ((s = launched(p, "beamforming kernel launch")) != BF_OK) return s;
     if (p->profiling) BF_CUDA(cudaEventRecord(e1, st));
     return BF_OK;
 }
@@ -469,6 +533,10 @@ bf_status bf_plan_create(int n_ant, int f, int b, int layout, bf_plan_t *out) {
             delete p;
             return fail(BF_ERR_UNSUPPORTED, "kernel for f=%d cannot be resident", f);
         }
+        p->kern_tc = g_table_tc[f][layout];
+        e = cudaFuncSetAttribute(p->kern_tc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 p->kern_tc.smem_bytes);
+        if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaFuncSetAttribute (tc)"); }
     }
     *out = p;
     return BF_OK;
@@ -491,6 +559,11 @@ bf_status bf_set_precoders(bf_plan_t p, const void *W_dev, int n_groups, void *s
         bf_relayout_w<<<blocks, 256, 0, st>>>(static_cast<const float *>(W_dev), n_groups, p->f,
                                               p->layout, p->Wp);
         if ((s = launched(p, "bf_relayout_w launch")) != BF_OK) return s;
+        const int64_t img = (int64_t)n_groups * 2 * bftc::kp_of(p->f) * 128;
+        if ((s = grow(&p->Wimg, &p->Wimg_cap, img, "tensor-core precoders")) != BF_OK) return s;
+        bf_tc_build_wimg<<<(int)std::min<int64_t>((img + 255) / 256, 4096), 256, 0, st>>>(
+            static_cast<const float *>(W_dev), n_groups, p->f, p->layout, p->Wimg);
+        if ((s = launched(p, "bf_tc_build_wimg launch")) != BF_OK) return s;
     }
     p->n_groups = n_groups;
     return BF_OK;
@@ -594,6 +667,7 @@ bf_status bf_destroy(bf_plan_t p) {
     {
         DeviceGuard guard(p->device);
         cudaFree(p->Wp);
+        cudaFree(p->Wimg);
         cudaFree(p->perm);
         cudaFree(p->gsorted);
         cudaFree(p->table);
@@ -647,6 +721,20 @@ bf_status bf_plan_launch_count(bf_plan_t p, int64_t *count) {
     return BF_OK;
 }
 
+bf_status bf_plan_set_variant(bf_plan_t p, int variant) {
+    if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
+    if (variant != BF_VARIANT_AUTO && variant != BF_VARIANT_FFMA && variant != BF_VARIANT_TENSOR)
+        return fail(BF_ERR_INVALID_VALUE, "unknown variant %d", variant);
+    p->variant = variant;
+    return BF_OK;
+}
+
+bf_status bf_plan_get_variant(bf_plan_t p, int *resolved) {
+    if (!p || !resolved) return fail(BF_ERR_INVALID_VALUE, "NULL argument");
+    *resolved = p->f == 0 ? BF_VARIANT_AUTO : (use_tensor(p) ? BF_VARIANT_TENSOR : BF_VARIANT_FFMA);
+    return BF_OK;
+}
+
 bf_status bf_plan_set_host_chunk(bf_plan_t p, int64_t blocks) {
     if (!p || blocks < 0) return fail(BF_ERR_INVALID_VALUE, "invalid chunk");
     p->host_chunk = blocks == 0 ? kDefaultHostChunk : blocks;
@@ -657,10 +745,12 @@ bf_status bf_plan_kernel_config(bf_plan_t p, int64_t n_blocks, int *grid, int *b
                                 int *smem_bytes, int *ctas_per_sm) {
     if (!p || !grid || !block || !smem_bytes || !ctas_per_sm)
         return fail(BF_ERR_INVALID_VALUE, "NULL argument");
-    *grid = p->f > 0 ? grid_for(p, std::max<int64_t>(n_blocks, 1)) : 0;
-    *block = p->f > 0 ? bfk::kThreads : 0;
-    *smem_bytes = p->kern.smem_bytes;
-    *ctas_per_sm = p->ctas_per_sm;
+    const bool tensor = p->f > 0 && use_tensor(p);
+    const int64_t nb = std::max<int64_t>(n_blocks, 1);
+    *grid = p->f == 0 ? 0 : (tensor ? (int)std::min<int64_t>(nb, p->num_sms) : grid_for(p, nb));
+    *block = p->f == 0 ? 0 : (tensor ? bftc::kThreads : bfk::kThreads);
+    *smem_bytes = tensor ? p->kern_tc.smem_bytes : p->kern.smem_bytes;
+    *ctas_per_sm = tensor ? 1 : p->ctas_per_sm;
     return BF_OK;
 }
 

@@ -4,15 +4,15 @@
 #pragma once
 
 struct BfKernelEntry {
-    const void *fn;      // __global__ bfk::bf_ffma_kernel<F, LAYOUT>
+    const void *fn;      // __global__ bfk::bf_ffma_kernel<F, LAYOUT> or bftc::bf_tc_kernel<F, LAYOUT>
     int smem_bytes;      // dynamic shared memory of that instantiation
 };
 
 using BfKernelTable = BfKernelEntry[37][2];
 
-void bf_register_f01_06(BfKernelTable &t);
-void bf_register_f07_12(BfKernelTable &t);
-void bf_register_f13_18(BfKernelTable &t);
-void bf_register_f19_24(BfKernelTable &t);
-void bf_register_f25_30(BfKernelTable &t);
-void bf_register_f31_36(BfKernelTable &t);
+void bf_register_f01_06(BfKernelTable &t, BfKernelTable &tc);
+void bf_register_f07_12(BfKernelTable &t, BfKernelTable &tc);
+void bf_register_f13_18(BfKernelTable &t, BfKernelTable &tc);
+void bf_register_f19_24(BfKernelTable &t, BfKernelTable &tc);
+void bf_register_f25_30(BfKernelTable &t, BfKernelTable &tc);
+void bf_register_f31_36(BfKernelTable &t, BfKernelTable &tc);

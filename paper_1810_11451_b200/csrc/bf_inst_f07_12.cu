@@ -1,18 +1,22 @@
-// Instantiations of bf_ffma_kernel for f = 7..12 (both layouts); see bf_ffma.cuh.
-#include "bf_ffma.cuh"
+// Instantiations of the beamforming kernels for f = 7..12 (both layouts):
+// the CUDA-core FFMA kernel (bf_ffma.cuh) and the tcgen05 split-TF32 kernel (bf_tc.cuh).
 #include "bf_dispatch.h"
+#include "bf_ffma.cuh"
+#include "bf_tc.cuh"
 
 template <int F>
-static void reg(BfKernelTable &t) {
+static void reg(BfKernelTable &t, BfKernelTable &tc) {
     t[F][0] = {reinterpret_cast<const void *>(&bfk::bf_ffma_kernel<F, 0>), bfk::Smem<F>::kBytes};
     t[F][1] = {reinterpret_cast<const void *>(&bfk::bf_ffma_kernel<F, 1>), bfk::Smem<F>::kBytes};
+    tc[F][0] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 0>), bftc::TcSmem<F>::kBytes};
+    tc[F][1] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 1>), bftc::TcSmem<F>::kBytes};
 }
 
-void bf_register_f07_12(BfKernelTable &t) {
-    reg<7>(t);
-    reg<8>(t);
-    reg<9>(t);
-    reg<10>(t);
-    reg<11>(t);
-    reg<12>(t);
+void bf_register_f07_12(BfKernelTable &t, BfKernelTable &tc) {
+    reg<7>(t, tc);
+    reg<8>(t, tc);
+    reg<9>(t, tc);
+    reg<10>(t, tc);
+    reg<11>(t, tc);
+    reg<12>(t, tc);
 }

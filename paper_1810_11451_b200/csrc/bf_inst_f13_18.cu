@@ -1,18 +1,22 @@
-// Instantiations of bf_ffma_kernel for f = 13..18 (both layouts); see bf_ffma.cuh.
-#include "bf_ffma.cuh"
+// Instantiations of the beamforming kernels for f = 13..18 (both layouts):
+// the CUDA-core FFMA kernel (bf_ffma.cuh) and the tcgen05 split-TF32 kernel (bf_tc.cuh).
 #include "bf_dispatch.h"
+#include "bf_ffma.cuh"
+#include "bf_tc.cuh"
 
 template <int F>
-static void reg(BfKernelTable &t) {
+static void reg(BfKernelTable &t, BfKernelTable &tc) {
     t[F][0] = {reinterpret_cast<const void *>(&bfk::bf_ffma_kernel<F, 0>), bfk::Smem<F>::kBytes};
     t[F][1] = {reinterpret_cast<const void *>(&bfk::bf_ffma_kernel<F, 1>), bfk::Smem<F>::kBytes};
+    tc[F][0] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 0>), bftc::TcSmem<F>::kBytes};
+    tc[F][1] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 1>), bftc::TcSmem<F>::kBytes};
 }
 
-void bf_register_f13_18(BfKernelTable &t) {
-    reg<13>(t);
-    reg<14>(t);
-    reg<15>(t);
-    reg<16>(t);
-    reg<17>(t);
-    reg<18>(t);
+void bf_register_f13_18(BfKernelTable &t, BfKernelTable &tc) {
+    reg<13>(t, tc);
+    reg<14>(t, tc);
+    reg<15>(t, tc);
+    reg<16>(t, tc);
+    reg<17>(t, tc);
+    reg<18>(t, tc);
 }

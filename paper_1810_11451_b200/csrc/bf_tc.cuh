@@ -1,0 +1,282 @@
+// bf_tc.cuh — sm_100a tensor-core (tcgen05, kind::tf32) beamforming kernel.
+//
+// Same operation as bf_ffma.cuh: R[n] = W[g(n)] x S[n], complex
+// fp32, 64 antennas, 60 REs, F flows.  SURVEY.md §8(f) row 2: a split-precision
+// tensor-core path kept only if it beats the FFMA path and meets the tolerance.
+//
+// Real embedding, transposed so that REs are the MMA's M rows:
+//   A [m][kk]  (TMEM)  m = RE of a 2-block tile (m = 60 b + j, 120 of 128 rows),
+//                      kk = 2k + c: S[blk][k][j] re (c = 0) / im (c = 1)
+//   B [n][kk]  (SMEM)  n = 2i + c_out (antenna i, re / im output):
+//                      n = 2i  : kk=2k -> Wr[i][k],  kk=2k+1 -> -Wi[i][k]
+//                      n = 2i+1: kk=2k -> Wi[i][k],  kk=2k+1 ->  Wr[i][k]
+//   D [m][n]   (TMEM)  = R[blk][i][j] re / im, fp32 accumulate.
+// Split precision (error-compensated 3xTF32 family, BASELINE.json north_star
+// item 2): S = S1 + S2 + S3 exactly (three tf32 terms), W' = W1 + W2 (+ 2^-22
+// residual), D = S1 W1 + S2 W1 + S3 W1 + S1 W2.  Dropped terms are <= 2^-21 T and
+// the fp32 (truncating) tensor accumulation over 4 x KP/8 MMAs stays below
+// ~3e-6 T at f = 36, inside the 1e-5 T contract; for
+// copy-like W (entries 0 / 1) W2 = 0 and S1 + S2 + S3 is accumulated exactly,
+// so identity / selection W reproduce S bit for bit.
+//
+// One CTA (9 warps) per SM, persistent over a contiguous range of the
+// group-sorted block list; tiles are 2 consecutive blocks of the same group.
+//   warps 0-3  split: LDG S (coalesced along j), split into 3 tf32 terms,
+//              tcgen05.st into the A region (one TMEM lane per RE);
+//   warp 4     MMA issuer (one thread) and W loader (cp.async.bulk of the
+//              group's pre-split B image into SMEM on a group change);
+//   warps 5-8  epilogue: tcgen05.ld of D rows, 64-bit stores of (re, im) —
+//              32 consecutive REs per warp = 256 contiguous bytes per antenna.
+// TMEM: A terms at columns [0, 3 KP), D double buffer at [256, 384), [384, 512).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "bf_ffma.cuh"
+#include "tc_ptx.cuh"
+
+namespace bftc {
+
+constexpr int kThreads = 288;
+constexpr int kSplitWarps = 4;
+constexpr int kMmaWarp = 4;
+constexpr int kEpiWarp0 = 5;
+constexpr int kDCol0 = 256;
+constexpr int kMinSmem = 120 * 1024;   // forces one CTA (and one TMEM owner) per SM
+
+__host__ __device__ constexpr int kp_of(int F) { return (2 * F + 7) / 8 * 8; }
+
+struct TcParams {
+    const float *Wimg;        // [n_groups][2][KP/4][16][8][4] floats (pre-split B image)
+    const float *S;
+    const int32_t *perm;      // NULL = identity order
+    const int32_t *gsorted;   // NULL = group 0
+    float *R;
+    int64_t n_items;
+    int n_groups;
+};
+
+template <int F>
+struct TcSmem {
+    static constexpr int KP = kp_of(F);
+    static constexpr int kWBytes = 2 * KP * 128 * 4;   // two tf32 terms
+    static constexpr int kOffBar = kWBytes;            // 8 mbarriers
+    static constexpr int kOffTmem = kOffBar + 8 * 8;
+    static constexpr int kBytesUsed = kOffTmem + 16;
+    static constexpr int kBytes = kBytesUsed > kMinSmem ? kBytesUsed : kMinSmem;
+};
+
+struct Tile {
+    int64_t item;
+    int cnt;      // 1 or 2 blocks
+    int g;
+};
+
+__device__ __forceinline__ int group_of(const TcParams &p, int64_t item) {
+    return p.gsorted ? __ldg(p.gsorted + item) : 0;
+}
+__device__ __forceinline__ int64_t block_of(const TcParams &p, int64_t item) {
+    return p.perm ? (int64_t)__ldg(p.perm + item) : item;
+}
+// Next tile starting at `item` (< end): two blocks when the next item has the same group.
+__device__ __forceinline__ Tile next_tile(const TcParams &p, int64_t item, int64_t end) {
+    Tile t;
+    t.item = item;
+    t.g = group_of(p, item);
+    t.cnt = (item + 1 < end && group_of(p, item + 1) == t.g) ? 2 : 1;
+    return t;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar))
+                 : "memory");
+}
+
+template <int F, int LAYOUT>
+__global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
+    using L = TcSmem<F>;
+    constexpr int KP = L::KP;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    float *Wsm = reinterpret_cast<float *>(smem);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::kOffBar);
+    uint64_t *bar_a_full = bars + 0, *bar_a_free = bars + 1, *bar_d_full = bars + 2,
+             *bar_d_free = bars + 4, *bar_w = bars + 6;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L::kOffTmem);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t n = p.n_items;
+    const int64_t begin = n * blockIdx.x / gridDim.x;
+    const int64_t end = n * (blockIdx.x + 1) / gridDim.x;
+    if (begin >= end) return;   // CTA-uniform, before any TMEM allocation
+
+    if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
+    if (threadIdx.x == 32) {
+        bfk::mbar_init(bar_a_full, 128);
+        bfk::mbar_init(bar_a_free, 1);
+        bfk::mbar_init(bar_d_full + 0, 1);
+        bfk::mbar_init(bar_d_full + 1, 1);
+        bfk::mbar_init(bar_d_free + 0, 128);
+        bfk::mbar_init(bar_d_free + 1, 128);
+        bfk::mbar_init(bar_w, 1);
+        bfk::mbar_fence_init();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < kSplitWarps) {
+        // ------------------------------------------------------------ split warps
+        const int m = warp * 32 + lane;                  // TMEM lane == A row
+        const int bsel = m >= 60 ? 1 : 0, j = m - 60 * bsel;
+        const uint32_t a_lane = tmem + ((uint32_t)(warp * 32) << 16);
+        int64_t t = 0;
+        for (int64_t item = begin; item < end; ++t) {
+            const Tile tl = next_tile(p, item, end);
+            item += tl.cnt;
+            if ((unsigned)tl.g >= (unsigned)p.n_groups) { --t; continue; }
+            const bool valid = m < 120 && bsel < tl.cnt;
+            float sr[F], si[F];
+#pragma unroll
+            for (int k = 0; k < F; ++k) { sr[k] = 0.0f; si[k] = 0.0f; }
+            if (valid) {
+                const int64_t blk = block_of(p, tl.item + bsel);
+                const float *Sb = p.S + blk * (int64_t)(120 * F);
+#pragma unroll
+                for (int k = 0; k < F; ++k) {
+                    if (LAYOUT == 0) {
+                        const float2 v = __ldcs(reinterpret_cast<const float2 *>(Sb) + k * 60 + j);
+                        sr[k] = v.x;
+                        si[k] = v.y;
+                    } else {
+                        sr[k] = __ldcs(Sb + k * 60 + j);
+                        si[k] = __ldcs(Sb + F * 60 + k * 60 + j);
+                    }
+                }
+            }
+            bfk::mbar_wait(bar_a_free, (uint32_t)((t & 1) ^ 1));
+            tc::fence_after_sync();
+            {   // tcgen05.st is warp-collective: every lane stores (invalid rows store zeros)
+#pragma unroll
+                for (int c0 = 0; c0 < KP; c0 += 8) {
+                    uint32_t v1[8], v2[8], v3[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int k = (c0 + e) >> 1;
+                        const float s = (k < F) ? (((c0 + e) & 1) ? si[k < F ? k : 0]
+                                                                 : sr[k < F ? k : 0])
+                                                : 0.0f;
+                        const float s1 = tc::to_tf32(s);
+                        const float r1 = s - s1;             // exact
+                        const float s2 = tc::to_tf32(r1);
+                        const float s3 = r1 - s2;            // exact, fits tf32
+                        v1[e] = __float_as_uint(s1);
+                        v2[e] = __float_as_uint(s2);
+                        v3[e] = __float_as_uint(s3);
+                    }
+                    tc::tmem_st8(a_lane + 0 * KP + c0, v1);
+                    tc::tmem_st8(a_lane + 1 * KP + c0, v2);
+                    tc::tmem_st8(a_lane + 2 * KP + c0, v3);
+                }
+            }
+            tc::tmem_st_wait();
+            tc::fence_before_sync();
+            mbar_arrive(bar_a_full);
+        }
+    } else if (warp == kMmaWarp) {
+        // ------------------------------------------------------------ MMA issuer
+        int cur_g = -1;
+        uint32_t wphase = 0;
+        constexpr uint32_t idesc = tc::idesc_tf32(128, 128);
+        const uint32_t w_base = tc::smem_u32(Wsm);
+        int64_t t = 0;
+        for (int64_t item = begin; item < end; ++t) {
+            const Tile tl = next_tile(p, item, end);
+            item += tl.cnt;
+            if ((unsigned)tl.g >= (unsigned)p.n_groups) { --t; continue; }
+            if (tl.g != cur_g) {
+                if (t > 0) bfk::mbar_wait(bar_a_free, (uint32_t)((t - 1) & 1));   // old W no longer read
+                if (lane == 0) {
+                    bfk::mbar_arrive_expect_tx(bar_w, L::kWBytes);
+                    bfk::bulk_g2s(Wsm, p.Wimg + (int64_t)tl.g * (L::kWBytes / 4), L::kWBytes, bar_w,
+                                  bfk::policy_evict_last());
+                }
+                bfk::mbar_wait(bar_w, wphase);
+                wphase ^= 1u;
+                cur_g = tl.g;
+            }
+            const int b = (int)(t & 1);
+            const uint32_t u = (uint32_t)(t >> 1);
+            bfk::mbar_wait(bar_a_full, (uint32_t)(t & 1));
+            bfk::mbar_wait(bar_d_free + b, (u & 1) ^ 1);
+            tc::fence_after_sync();
+            if (lane == 0) {
+                const uint32_t d = tmem + kDCol0 + 128 * b;
+#pragma unroll
+                for (int term = 0; term < 4; ++term) {
+                    const int at = term < 3 ? term : 0;      // S1, S2, S3, S1
+                    const int wt = term < 3 ? 0 : 1;         // W1, W1, W1, W2
+#pragma unroll
+                    for (int kb = 0; kb < KP / 8; ++kb) {
+                        const uint64_t desc = tc::smem_desc(
+                            w_base + (uint32_t)((wt * (KP / 4) + 2 * kb) * 16 * 128), 16 * 128, 128);
+                        tc::mma_tf32_ts(d, tmem + at * KP + kb * 8, desc, idesc,
+                                        (term | kb) != 0);
+                    }
+                }
+                tc::mma_commit(bar_a_free);
+                tc::mma_commit(bar_d_full + b);
+            }
+            __syncwarp();
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue warps
+        const int q = warp & 3;                          // TMEM lane quarter of this warp
+        const int m = q * 32 + lane;
+        const int bsel = m >= 60 ? 1 : 0, j = m - 60 * bsel;
+        int64_t t = 0;
+        for (int64_t item = begin; item < end; ++t) {
+            const Tile tl = next_tile(p, item, end);
+            item += tl.cnt;
+            if ((unsigned)tl.g >= (unsigned)p.n_groups) { --t; continue; }
+            const int b = (int)(t & 1);
+            const uint32_t u = (uint32_t)(t >> 1);
+            const bool valid = m < 120 && bsel < tl.cnt;
+            const int64_t blk = valid ? block_of(p, tl.item + bsel) : 0;
+            float *Rb = p.R + blk * (int64_t)bfk::kRBlockFloats;
+            bfk::mbar_wait(bar_d_full + b, u & 1);
+            tc::fence_after_sync();
+            const uint32_t d = tmem + ((uint32_t)(q * 32) << 16) + kDCol0 + 128 * b;
+#pragma unroll
+            for (int c0 = 0; c0 < 128; c0 += 16) {
+                uint32_t v[16];
+                tc::tmem_ld16(d + c0, v);
+                tc::tmem_ld_wait();
+                if (valid) {
+#pragma unroll
+                    for (int a = 0; a < 8; ++a) {
+                        const int ant = c0 / 2 + a;
+                        const float re = __uint_as_float(v[2 * a]);
+                        const float im = __uint_as_float(v[2 * a + 1]);
+                        if (LAYOUT == 0) {
+                            __stcs(reinterpret_cast<float2 *>(Rb) + ant * 60 + j, make_float2(re, im));
+                        } else {
+                            __stcs(Rb + ant * 60 + j, re);
+                            __stcs(Rb + 64 * 60 + ant * 60 + j, im);
+                        }
+                    }
+                }
+            }
+            tc::fence_before_sync();
+            mbar_arrive(bar_d_free + b);
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+        tc::fence_after_sync();
+        tc::tmem_free<512>(tmem);
+    }
+}
+
+}  // namespace bftc

@@ -14,7 +14,7 @@ import ctypes
 
 import torch
 
-from ._lib import BfError, Layout, Status, check, lib
+from ._lib import BfError, Layout, Status, Variant, check, lib
 
 N_ANT = 64
 N_RE = 60
@@ -37,7 +37,8 @@ class Plan:
     """A beamforming plan: n_ant x f precoders applied to f x b symbol blocks."""
 
     def __init__(self, f: int, n_ant: int = N_ANT, b: int = N_RE,
-                 layout: Layout | str | int = Layout.INTERLEAVED):
+                 layout: Layout | str | int = Layout.INTERLEAVED,
+                 variant: Variant | str | int = Variant.AUTO):
         if isinstance(layout, str):
             layout = Layout[layout.upper()]
         self.f, self.n_ant, self.b, self.layout = int(f), int(n_ant), int(b), Layout(layout)
@@ -47,6 +48,7 @@ class Plan:
                                    ctypes.byref(self._h)))
         self.device = torch.device("cuda", torch.cuda.current_device())
         self._w_ref = None
+        self.set_variant(variant)
 
     # -- shapes ---------------------------------------------------------------
     def s_shape(self, n: int):
@@ -141,6 +143,19 @@ class Plan:
         check(lib().bf_plan_launch_count(self._h, ctypes.byref(c)))
         return c.value
 
+    def set_variant(self, variant: Variant | str | int) -> None:
+        """bf_plan_set_variant: AUTO (per-f table), FFMA or TENSOR."""
+        if isinstance(variant, str):
+            variant = Variant[variant.upper()]
+        check(lib().bf_plan_set_variant(self._h, int(variant)))
+
+    @property
+    def variant(self) -> Variant:
+        """The kernel variant applies of this plan run (AUTO resolved)."""
+        v = ctypes.c_int()
+        check(lib().bf_plan_get_variant(self._h, ctypes.byref(v)))
+        return Variant(v.value)
+
     def set_host_chunk(self, blocks: int) -> None:
         check(lib().bf_plan_set_host_chunk(self._h, int(blocks)))
 
@@ -177,4 +192,4 @@ def plan_create_status(n_ant: int, f: int, b: int, layout: int = 0) -> Status:
     return Status(s)
 
 
-__all__ = ["Plan", "Layout", "Status", "BfError", "plan_create_status", "N_ANT", "N_RE", "MAX_F"]
+__all__ = ["Plan", "Layout", "Status", "Variant", "BfError", "plan_create_status", "N_ANT", "N_RE", "MAX_F"]
