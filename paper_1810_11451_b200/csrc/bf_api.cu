@@ -51,7 +51,10 @@ constexpr int kRouteMinTile = 4096;
 constexpr int kRouteMaxTable = 65536;      // tiles x (groups + 1) entries
 constexpr int64_t kDefaultHostChunk = 2048;
 constexpr int kHostSlots = 3;
-constexpr int kAutoTensorMinF = 99;         // AUTO = FFMA everywhere until measured
+// AUTO variant table (measured, profiles/r01_sweep_f_*.jsonl: c3, 100 000 blocks
+// per f, both layouts): the tensor-core kernel is at least as fast as the FFMA
+// kernel for every f >= 1 (equal at f = 4, 2.2x at f = 36), so AUTO picks it.
+constexpr int kAutoTensorMinF = 1;
 
 BfKernelTable g_table;      // FFMA kernels [f][layout]
 BfKernelTable g_table_tc;   // tcgen05 split-TF32 kernels [f][layout]

@@ -19,10 +19,13 @@
 // copy-like W (entries 0 / 1) W2 = 0 and S1 + S2 + S3 is accumulated exactly,
 // so identity / selection W reproduce S bit for bit.
 //
-// One CTA (9 warps) per SM, persistent over a contiguous range of the
+// One CTA (10 warps) per SM, persistent over a contiguous range of the
 // group-sorted block list; tiles are 2 consecutive blocks of the same group.
-//   warps 0-3  split: LDG S (coalesced along j), split into 3 tf32 terms,
-//              tcgen05.st into the A region (one TMEM lane per RE);
+//   warp 9     S producer: cp.async.bulk (TMA bulk engine) of each block's
+//              480 F contiguous bytes into a 4-stage shared-memory ring,
+//              completing on mbarriers, up to 4 tiles ahead of the split;
+//   warps 0-3  split: LDS S (conflict-free, one RE column per lane), split into
+//              3 tf32 terms, tcgen05.st into the A region (one TMEM lane per RE);
 //   warp 4     MMA issuer (one thread) and W loader (cp.async.bulk of the
 //              group's pre-split B image into SMEM on a group change);
 //   warps 5-8  epilogue: tcgen05.ld of D rows, 64-bit stores of (re, im) —
@@ -37,10 +40,12 @@
 
 namespace bftc {
 
-constexpr int kThreads = 288;
+constexpr int kThreads = 320;
 constexpr int kSplitWarps = 4;
 constexpr int kMmaWarp = 4;
 constexpr int kEpiWarp0 = 5;
+constexpr int kProdWarp = 9;
+constexpr int kStages = 4;             // S ring depth (tiles)
 constexpr int kDCol0 = 256;
 constexpr int kMinSmem = 120 * 1024;   // forces one CTA (and one TMEM owner) per SM
 
@@ -60,8 +65,10 @@ template <int F>
 struct TcSmem {
     static constexpr int KP = kp_of(F);
     static constexpr int kWBytes = 2 * KP * 128 * 4;   // two tf32 terms
-    static constexpr int kOffBar = kWBytes;            // 8 mbarriers
-    static constexpr int kOffTmem = kOffBar + 8 * 8;
+    static constexpr int kSBlock = 480 * F;            // one block of S
+    static constexpr int kOffS = kWBytes;              // kStages x 2 blocks
+    static constexpr int kOffBar = kOffS + kStages * 2 * kSBlock;   // 16 mbarriers
+    static constexpr int kOffTmem = kOffBar + 16 * 8;
     static constexpr int kBytesUsed = kOffTmem + 16;
     static constexpr int kBytes = kBytesUsed > kMinSmem ? kBytesUsed : kMinSmem;
 };
@@ -100,7 +107,9 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
     float *Wsm = reinterpret_cast<float *>(smem);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::kOffBar);
     uint64_t *bar_a_full = bars + 0, *bar_a_free = bars + 1, *bar_d_full = bars + 2,
-             *bar_d_free = bars + 4, *bar_w = bars + 6;
+             *bar_d_free = bars + 4, *bar_w = bars + 6, *bar_s_full = bars + 7,
+             *bar_s_empty = bars + 7 + kStages;
+    float *Ss = reinterpret_cast<float *>(smem + L::kOffS);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L::kOffTmem);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -118,6 +127,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
         bfk::mbar_init(bar_d_free + 0, 128);
         bfk::mbar_init(bar_d_free + 1, 128);
         bfk::mbar_init(bar_w, 1);
+        for (int i = 0; i < kStages; ++i) {
+            bfk::mbar_init(bar_s_full + i, 1);
+            bfk::mbar_init(bar_s_empty + i, 128);
+        }
         bfk::mbar_fence_init();
     }
     tc::fence_before_sync();
@@ -136,24 +149,26 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
             item += tl.cnt;
             if ((unsigned)tl.g >= (unsigned)p.n_groups) { --t; continue; }
             const bool valid = m < 120 && bsel < tl.cnt;
+            const int stage = (int)(t % kStages);
+            bfk::mbar_wait(bar_s_full + stage, (uint32_t)((t / kStages) & 1));
             float sr[F], si[F];
 #pragma unroll
             for (int k = 0; k < F; ++k) { sr[k] = 0.0f; si[k] = 0.0f; }
             if (valid) {
-                const int64_t blk = block_of(p, tl.item + bsel);
-                const float *Sb = p.S + blk * (int64_t)(120 * F);
+                const float *Sb = Ss + (stage * 2 + bsel) * (L::kSBlock / 4);
 #pragma unroll
                 for (int k = 0; k < F; ++k) {
                     if (LAYOUT == 0) {
-                        const float2 v = __ldcs(reinterpret_cast<const float2 *>(Sb) + k * 60 + j);
+                        const float2 v = reinterpret_cast<const float2 *>(Sb)[k * 60 + j];
                         sr[k] = v.x;
                         si[k] = v.y;
                     } else {
-                        sr[k] = __ldcs(Sb + k * 60 + j);
-                        si[k] = __ldcs(Sb + F * 60 + k * 60 + j);
+                        sr[k] = Sb[k * 60 + j];
+                        si[k] = Sb[F * 60 + k * 60 + j];
                     }
                 }
             }
+            mbar_arrive(bar_s_empty + stage);             // ring slot may be refilled
             bfk::mbar_wait(bar_a_free, (uint32_t)((t & 1) ^ 1));
             tc::fence_after_sync();
             {   // tcgen05.st is warp-collective: every lane stores (invalid rows store zeros)
@@ -182,6 +197,26 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
             tc::tmem_st_wait();
             tc::fence_before_sync();
             mbar_arrive(bar_a_full);
+        }
+    } else if (warp == kProdWarp) {
+        // ------------------------------------------------------------ S producer (TMA bulk)
+        const uint64_t pol = bfk::policy_evict_first();
+        int64_t t = 0;
+        for (int64_t item = begin; item < end; ++t) {
+            const Tile tl = next_tile(p, item, end);
+            item += tl.cnt;
+            if ((unsigned)tl.g >= (unsigned)p.n_groups) { --t; continue; }
+            const int stage = (int)(t % kStages);
+            bfk::mbar_wait(bar_s_empty + stage, (uint32_t)(((t / kStages) & 1) ^ 1));
+            if (lane == 0) {
+                bfk::mbar_arrive_expect_tx(bar_s_full + stage, (uint32_t)(tl.cnt * L::kSBlock));
+                for (int b = 0; b < tl.cnt; ++b) {
+                    const int64_t blk = block_of(p, tl.item + b);
+                    bfk::bulk_g2s(Ss + (stage * 2 + b) * (L::kSBlock / 4),
+                                  p.S + blk * (int64_t)(120 * F), L::kSBlock, bar_s_full + stage, pol);
+                }
+            }
+            __syncwarp();
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------------------ MMA issuer

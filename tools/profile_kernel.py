@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--blocks", type=int, default=131072)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--layout", default="interleaved")
+    ap.add_argument("--variant", default="auto")
     a = ap.parse_args()
     wl = syn.workload("c3", a.f) if a.config == "c3" else syn.workload(a.config)
     dev = torch.device("cuda", 0)
@@ -38,7 +39,7 @@ def main():
     planar = a.layout == "planar"
     S, tags = sync.workload_device(wl, dev, n=n, planar=planar)
     W = syn.precoders(wl.seed, wl.sub, wl.n_groups, wl.n_ant, wl.f, wl.w_norm)
-    plan = bf.Plan(f=wl.f, layout=a.layout)
+    plan = bf.Plan(f=wl.f, layout=a.layout, variant=a.variant)
     plan.set_precoders(torch.from_numpy(syn.to_planar(W) if planar else W).to(dev))
     R = torch.empty(plan.r_shape(n), dtype=plan.dtype, device=dev)
     for _ in range(a.reps):
@@ -46,7 +47,7 @@ def main():
     torch.cuda.synchronize()
     print(json.dumps({"workload": wl.name, "blocks": n, "layout": a.layout,
                       "bytes_per_block": wl.block_bytes, "flops_per_block": wl.block_flops,
-                      "kernel": plan.kernel_config(n)}))
+                      "variant": plan.variant.name, "kernel": plan.kernel_config(n)}))
 
 
 if __name__ == "__main__":
