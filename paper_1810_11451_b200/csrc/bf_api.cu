@@ -137,6 +137,17 @@ __global__ void bf_tc_build_wimg(const float *__restrict__ W, int n_groups, int 
 }
 
 
+// wexact[g] = 1 when group g's W is exactly representable in tf32 (its W2 half
+// of the image is all zero); the tensor kernel then multiplies S3 instead of W2.
+__global__ void bf_tc_wexact(const float *__restrict__ img, int KP, int32_t *__restrict__ wexact) {
+    const int64_t per_group = 2LL * KP * 128;
+    const float *w2 = img + blockIdx.x * per_group + per_group / 2;
+    int nz = 0;
+    for (int i = threadIdx.x; i < KP * 128; i += blockDim.x) nz |= (w2[i] != 0.0f);
+    nz = __syncthreads_or(nz);
+    if (threadIdx.x == 0) wexact[blockIdx.x] = nz ? 0 : 1;
+}
+
 __device__ __forceinline__ int route_bin(int32_t g, int G) {
     return (unsigned)g < (unsigned)G ? g : G;   // invalid tags -> bin G (sorted last)
 }
@@ -298,6 +309,8 @@ struct bf_plan_s {
     int64_t Wp_cap = 0;
     float *Wimg = nullptr;      // tensor-core (pre-split B) precoder image
     int64_t Wimg_cap = 0;
+    int32_t *wexact = nullptr;  // per group: W exactly tf32
+    int64_t wexact_cap = 0;
     // routing workspace
     int32_t *perm = nullptr, *gsorted = nullptr, *table = nullptr, *offsets = nullptr,
             *err = nullptr;
@@ -408,6 +421,8 @@ bf_status apply_device(bf_plan_t p, const void *S, const int32_t *gidx, void *R,
     tp.S = kp.S;
     tp.perm = kp.perm;
     tp.gsorted = kp.gsorted;
+    tp.offsets = kp.gsorted ? p->offsets : nullptr;
+    tp.wexact = p->wexact;
     tp.R = kp.R;
     tp.n_items = n;
     tp.n_groups = p->n_groups;
@@ -567,6 +582,9 @@ bf_status bf_set_precoders(bf_plan_t p, const void *W_dev, int n_groups, void *s
         bf_tc_build_wimg<<<(int)std::min<int64_t>((img + 255) / 256, 4096), 256, 0, st>>>(
             static_cast<const float *>(W_dev), n_groups, p->f, p->layout, p->Wimg);
         if ((s = launched(p, "bf_tc_build_wimg launch")) != BF_OK) return s;
+        if ((s = grow(&p->wexact, &p->wexact_cap, n_groups, "precoder flags")) != BF_OK) return s;
+        bf_tc_wexact<<<n_groups, 256, 0, st>>>(p->Wimg, bftc::kp_of(p->f), p->wexact);
+        if ((s = launched(p, "bf_tc_wexact launch")) != BF_OK) return s;
     }
     p->n_groups = n_groups;
     return BF_OK;
@@ -671,6 +689,7 @@ bf_status bf_destroy(bf_plan_t p) {
         DeviceGuard guard(p->device);
         cudaFree(p->Wp);
         cudaFree(p->Wimg);
+        cudaFree(p->wexact);
         cudaFree(p->perm);
         cudaFree(p->gsorted);
         cudaFree(p->table);

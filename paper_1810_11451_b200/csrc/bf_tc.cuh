@@ -11,13 +11,16 @@
 //                      n = 2i  : kk=2k -> Wr[i][k],  kk=2k+1 -> -Wi[i][k]
 //                      n = 2i+1: kk=2k -> Wi[i][k],  kk=2k+1 ->  Wr[i][k]
 //   D [m][n]   (TMEM)  = R[blk][i][j] re / im, fp32 accumulate.
-// Split precision (error-compensated 3xTF32 family, BASELINE.json north_star
-// item 2): S = S1 + S2 + S3 exactly (three tf32 terms), W' = W1 + W2 (+ 2^-22
-// residual), D = S1 W1 + S2 W1 + S3 W1 + S1 W2.  Dropped terms are <= 2^-21 T and
-// the fp32 (truncating) tensor accumulation over 4 x KP/8 MMAs stays below
-// ~3e-6 T at f = 36, inside the 1e-5 T contract; for
-// copy-like W (entries 0 / 1) W2 = 0 and S1 + S2 + S3 is accumulated exactly,
-// so identity / selection W reproduce S bit for bit.
+// Split precision (error-compensated 3xTF32, BASELINE.json north_star item 2):
+// S = S1 + S2 + S3 exactly (three tf32 terms, each rounded to 11 bits),
+// W' = W1 + W2 (+ 2^-22 residual, split once per W).  Three MMA terms per K
+// step: S2 W1 + S1 W1 + S1 W2 for general W; S2 W1 + S3 W1 + S1 W1 when the
+// group's W is exactly tf32 (W2 == 0: identity, selection, small integers),
+// which makes copy-like precoders bit-exact.  The split of tile t+1 rewrites
+// S2, S3, S1 (in the MMA's order) as soon as tile t's MMAs on each completed.
+// Dropped terms are <= ~2^-21 T; the fp32 (truncating) tensor accumulation
+// over 3 x KP/8 MMAs stays near 2e-6 T at f = 36, inside the
+// 1e-5 T contract.
 //
 // One CTA (10 warps) per SM, persistent over a contiguous range of the
 // group-sorted block list; tiles are 2 consecutive blocks of the same group.
@@ -28,8 +31,9 @@
 //              3 tf32 terms, tcgen05.st into the A region (one TMEM lane per RE);
 //   warp 4     MMA issuer (one thread) and W loader (cp.async.bulk of the
 //              group's pre-split B image into SMEM on a group change);
-//   warps 5-8  epilogue: tcgen05.ld of D rows, 64-bit stores of (re, im) —
-//              32 consecutive REs per warp = 256 contiguous bytes per antenna.
+//   warps 5-8  epilogue: tcgen05.ld of a whole D row (128 columns), release of
+//              the TMEM buffer, then stores of two adjacent REs per lane (lane
+//              pairs trade one shuffle) — 256 contiguous bytes per antenna row.
 // TMEM: A terms at columns [0, 3 KP), D double buffer at [256, 384), [384, 512).
 #pragma once
 #include <cstdint>
@@ -45,7 +49,8 @@ constexpr int kSplitWarps = 4;
 constexpr int kMmaWarp = 4;
 constexpr int kEpiWarp0 = 5;
 constexpr int kProdWarp = 9;
-constexpr int kStages = 4;             // S ring depth (tiles)
+constexpr int kMaxStages = 4;          // S ring depth (tiles), shared memory permitting
+constexpr int kSmemLimit = 232448;     // 227 KB per CTA
 constexpr int kDCol0 = 256;
 constexpr int kMinSmem = 120 * 1024;   // forces one CTA (and one TMEM owner) per SM
 
@@ -55,7 +60,9 @@ struct TcParams {
     const float *Wimg;        // [n_groups][2][KP/4][16][8][4] floats (pre-split B image)
     const float *S;
     const int32_t *perm;      // NULL = identity order
-    const int32_t *gsorted;   // NULL = group 0
+    const int32_t *gsorted;   // NULL = group 0 (unused: groups come from offsets)
+    const int32_t *offsets;   // [n_groups + 2] group starts of the sorted order, or NULL
+    const int32_t *wexact;    // [n_groups] 1 if the group's W is exactly tf32 (W2 == 0)
     float *R;
     int64_t n_items;
     int n_groups;
@@ -66,10 +73,15 @@ struct TcSmem {
     static constexpr int KP = kp_of(F);
     static constexpr int kWBytes = 2 * KP * 128 * 4;   // two tf32 terms
     static constexpr int kSBlock = 480 * F;            // one block of S
+    static constexpr int kFixed = kWBytes + 24 * 8 + 16 + 1028 * 4;
+    static constexpr int kStagesFit = (kSmemLimit - kFixed) / (2 * kSBlock);
+    static constexpr int kStages = kStagesFit < kMaxStages ? kStagesFit : kMaxStages;
+    static_assert(kStages >= 2, "S ring needs two stages");
     static constexpr int kOffS = kWBytes;              // kStages x 2 blocks
-    static constexpr int kOffBar = kOffS + kStages * 2 * kSBlock;   // 16 mbarriers
-    static constexpr int kOffTmem = kOffBar + 16 * 8;
-    static constexpr int kBytesUsed = kOffTmem + 16;
+    static constexpr int kOffBar = kOffS + kStages * 2 * kSBlock;   // 24 mbarrier slots
+    static constexpr int kOffTmem = kOffBar + 24 * 8;
+    static constexpr int kOffOffs = kOffTmem + 16;     // group offsets (<= 1026 ints)
+    static constexpr int kBytesUsed = kOffOffs + 1028 * 4;
     static constexpr int kBytes = kBytesUsed > kMinSmem ? kBytesUsed : kMinSmem;
 };
 
@@ -79,19 +91,46 @@ struct Tile {
     int g;
 };
 
-__device__ __forceinline__ int group_of(const TcParams &p, int64_t item) {
-    return p.gsorted ? __ldg(p.gsorted + item) : 0;
-}
 __device__ __forceinline__ int64_t block_of(const TcParams &p, int64_t item) {
     return p.perm ? (int64_t)__ldg(p.perm + item) : item;
 }
-// Next tile starting at `item` (< end): two blocks when the next item has the same group.
-__device__ __forceinline__ Tile next_tile(const TcParams &p, int64_t item, int64_t end) {
-    Tile t;
-    t.item = item;
-    t.g = group_of(p, item);
-    t.cnt = (item + 1 < end && group_of(p, item + 1) == t.g) ? 2 : 1;
-    return t;
+
+// Walks a CTA's item range in tiles of up to 2 consecutive blocks of one group.
+// Groups come from the routing offsets copied to shared memory (no global loads
+// on the critical path); every role runs the same walk, so tile t is the same
+// tile everywhere.  Items with invalid tags sort last and are skipped.
+struct TileIter {
+    const int32_t *offs;   // shared copy of offsets [G + 2], or nullptr (untagged)
+    int G;
+    int gi;
+    int64_t item, end;
+    __device__ bool next(Tile &t) {
+        if (item >= end) return false;
+        int64_t gend = end;
+        if (offs) {
+            while (gi < G && item >= offs[gi + 1]) ++gi;
+            if (gi >= G) { item = end; return false; }
+            gend = min(end, (int64_t)offs[gi + 1]);
+        }
+        t.item = item;
+        t.g = offs ? gi : 0;
+        t.cnt = (item + 1 < gend) ? 2 : 1;
+        item += t.cnt;
+        return true;
+    }
+};
+
+// Named barrier 1 over the 4 epilogue warps (128 threads).
+__device__ __forceinline__ void epi_bar_sync() {
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+// TMA bulk store shared -> global (bulk-group completion), L2 cache hint.
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+        ::"l"(dst), "r"(tc::smem_u32(src)), "r"(bytes), "l"(policy) : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -99,18 +138,23 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
                  : "memory");
 }
 
-template <int F, int LAYOUT>
+// DBG (0 in the library) disables pieces for bottleneck experiments only
+// (tools/tc_exp): 1 = no MMA issue, 2 = no R stores, 4 = no split/tcgen05.st,
+// 8 = no S loads.  Results are wrong with DBG != 0.
+template <int F, int LAYOUT, int DBG = 0>
 __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
     using L = TcSmem<F>;
     constexpr int KP = L::KP;
     extern __shared__ __align__(1024) unsigned char smem[];
     float *Wsm = reinterpret_cast<float *>(smem);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::kOffBar);
-    uint64_t *bar_a_full = bars + 0, *bar_a_free = bars + 1, *bar_d_full = bars + 2,
-             *bar_d_free = bars + 4, *bar_w = bars + 6, *bar_s_full = bars + 7,
-             *bar_s_empty = bars + 7 + kStages;
+    // a_full[t] / a_free[t]: TMEM A region of split term t (0: S1, 1: S2, 2: S3)
+    uint64_t *bar_a_full = bars + 0, *bar_a_free = bars + 3, *bar_d_full = bars + 6,
+             *bar_d_free = bars + 8, *bar_w = bars + 10, *bar_s_full = bars + 11,
+             *bar_s_empty = bars + 11 + L::kStages;
     float *Ss = reinterpret_cast<float *>(smem + L::kOffS);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L::kOffTmem);
+    int32_t *soffs = reinterpret_cast<int32_t *>(smem + L::kOffOffs);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t n = p.n_items;
@@ -120,103 +164,131 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
 
     if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
     if (threadIdx.x == 32) {
-        bfk::mbar_init(bar_a_full, 128);
-        bfk::mbar_init(bar_a_free, 1);
+        for (int i = 0; i < 3; ++i) {
+            bfk::mbar_init(bar_a_full + i, 128);
+            bfk::mbar_init(bar_a_free + i, 1);
+        }
         bfk::mbar_init(bar_d_full + 0, 1);
         bfk::mbar_init(bar_d_full + 1, 1);
         bfk::mbar_init(bar_d_free + 0, 128);
         bfk::mbar_init(bar_d_free + 1, 128);
         bfk::mbar_init(bar_w, 1);
-        for (int i = 0; i < kStages; ++i) {
+        for (int i = 0; i < L::kStages; ++i) {
             bfk::mbar_init(bar_s_full + i, 1);
             bfk::mbar_init(bar_s_empty + i, 128);
         }
         bfk::mbar_fence_init();
     }
+    if (p.offsets)
+        for (int i = threadIdx.x; i < p.n_groups + 2; i += blockDim.x) soffs[i] = p.offsets[i];
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = *tmem_slot;
+    TileIter it{p.offsets ? soffs : nullptr, p.n_groups, 0, begin, end};
+    Tile tl;
 
     if (warp < kSplitWarps) {
         // ------------------------------------------------------------ split warps
         const int m = warp * 32 + lane;                  // TMEM lane == A row
         const int bsel = m >= 60 ? 1 : 0, j = m - 60 * bsel;
         const uint32_t a_lane = tmem + ((uint32_t)(warp * 32) << 16);
-        int64_t t = 0;
-        for (int64_t item = begin; item < end; ++t) {
-            const Tile tl = next_tile(p, item, end);
-            item += tl.cnt;
-            if ((unsigned)tl.g >= (unsigned)p.n_groups) { --t; continue; }
+        int cur_g = -1;
+        bool cur_exact = false;
+        for (int64_t t = 0; it.next(tl); ++t) {
             const bool valid = m < 120 && bsel < tl.cnt;
-            const int stage = (int)(t % kStages);
-            bfk::mbar_wait(bar_s_full + stage, (uint32_t)((t / kStages) & 1));
-            float sr[F], si[F];
-#pragma unroll
-            for (int k = 0; k < F; ++k) { sr[k] = 0.0f; si[k] = 0.0f; }
-            if (valid) {
-                const float *Sb = Ss + (stage * 2 + bsel) * (L::kSBlock / 4);
-#pragma unroll
-                for (int k = 0; k < F; ++k) {
-                    if (LAYOUT == 0) {
-                        const float2 v = reinterpret_cast<const float2 *>(Sb)[k * 60 + j];
-                        sr[k] = v.x;
-                        si[k] = v.y;
-                    } else {
-                        sr[k] = Sb[k * 60 + j];
-                        si[k] = Sb[F * 60 + k * 60 + j];
-                    }
-                }
+            const int stage = (int)(t % L::kStages);
+            bfk::mbar_wait(bar_s_full + stage, (uint32_t)((t / L::kStages) & 1));
+            const float *Sb = Ss + (stage * 2 + (valid ? bsel : 0)) * (L::kSBlock / 4);
+            // Term order S2, S3, S1 mirrors the MMA order, so each region is rewritten
+            // as soon as the previous tile's MMAs on it have completed and the tensor
+            // pipe keeps running on the other terms meanwhile.  S is re-read from the
+            // ring for every term (cheap LDS) instead of being held in 2F registers.
+            // tcgen05.st is warp-collective: every lane stores (invalid rows store 0).
+            const uint32_t par = (uint32_t)((t & 1) ^ 1);
+            if (tl.g != cur_g) {
+                cur_g = tl.g;
+                cur_exact = __ldg(p.wexact + tl.g) != 0;
             }
-            mbar_arrive(bar_s_empty + stage);             // ring slot may be refilled
-            bfk::mbar_wait(bar_a_free, (uint32_t)((t & 1) ^ 1));
-            tc::fence_after_sync();
-            {   // tcgen05.st is warp-collective: every lane stores (invalid rows store zeros)
+#pragma unroll
+            for (int pass = 0; pass < 3; ++pass) {
+                const int term = pass == 2 ? 0 : pass + 1;
+                bfk::mbar_wait(bar_a_free + term, par);
+                tc::fence_after_sync();
+                if (term == 2 && !cur_exact) {   // S3 is only multiplied for tf32-exact W
+                    tc::fence_before_sync();
+                    mbar_arrive(bar_a_full + term);
+                    continue;
+                }
 #pragma unroll
                 for (int c0 = 0; c0 < KP; c0 += 8) {
-                    uint32_t v1[8], v2[8], v3[8];
+                    float x[8];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int k = c0 / 2 + q;
+                        float re = 0.0f, im = 0.0f;
+                        if (k < F && valid) {
+                            if (LAYOUT == 0) {
+                                const float2 v = reinterpret_cast<const float2 *>(Sb)[k * 60 + j];
+                                re = v.x;
+                                im = v.y;
+                            } else {
+                                re = Sb[k * 60 + j];
+                                im = Sb[F * 60 + k * 60 + j];
+                            }
+                        }
+                        x[2 * q] = re;
+                        x[2 * q + 1] = im;
+                    }
+                    uint32_t v[8];
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
-                        const int k = (c0 + e) >> 1;
-                        const float s = (k < F) ? (((c0 + e) & 1) ? si[k < F ? k : 0]
-                                                                 : sr[k < F ? k : 0])
-                                                : 0.0f;
-                        const float s1 = tc::to_tf32(s);
-                        const float r1 = s - s1;             // exact
-                        const float s2 = tc::to_tf32(r1);
-                        const float s3 = r1 - s2;            // exact, fits tf32
-                        v1[e] = __float_as_uint(s1);
-                        v2[e] = __float_as_uint(s2);
-                        v3[e] = __float_as_uint(s3);
+                        // exact 3-term split, each term rounded to 11 significant
+                        // bits (integer add + mask, 2 ops): x = x1 + x2 + x3 exactly,
+                        // |x - x1| <= 2^-11 |x|, |x3| <= 2^-22 |x|.
+                        const float x1 = tc::tf32_round(x[e]);
+                        const float r1 = x[e] - x1;          // exact
+                        const float x2 = tc::tf32_round(r1);
+                        const float x3 = r1 - x2;            // exact, fits tf32
+                        v[e] = __float_as_uint(term == 0 ? x1 : (term == 1 ? x2 : x3));
                     }
-                    tc::tmem_st8(a_lane + 0 * KP + c0, v1);
-                    tc::tmem_st8(a_lane + 1 * KP + c0, v2);
-                    tc::tmem_st8(a_lane + 2 * KP + c0, v3);
+                    if constexpr (!(DBG & 4)) tc::tmem_st8(a_lane + term * KP + c0, v);
                 }
+                tc::tmem_st_wait();
+                tc::fence_before_sync();
+                mbar_arrive(bar_a_full + term);
             }
-            tc::tmem_st_wait();
-            tc::fence_before_sync();
-            mbar_arrive(bar_a_full);
+            mbar_arrive(bar_s_empty + stage);             // ring slot may be refilled
         }
     } else if (warp == kProdWarp) {
         // ------------------------------------------------------------ S producer (TMA bulk)
         const uint64_t pol = bfk::policy_evict_first();
-        int64_t t = 0;
-        for (int64_t item = begin; item < end; ++t) {
-            const Tile tl = next_tile(p, item, end);
-            item += tl.cnt;
-            if ((unsigned)tl.g >= (unsigned)p.n_groups) { --t; continue; }
-            const int stage = (int)(t % kStages);
-            bfk::mbar_wait(bar_s_empty + stage, (uint32_t)(((t / kStages) & 1) ^ 1));
-            if (lane == 0) {
+        bool have = it.next(tl);
+        int64_t blk0 = have ? block_of(p, tl.item) : 0;
+        int64_t blk1 = have && tl.cnt > 1 ? block_of(p, tl.item + 1) : 0;
+        for (int64_t t = 0; have; ++t) {
+            Tile nx;                       // next tile's block ids load while we wait
+            const bool have_nx = it.next(nx);
+            const int64_t nb0 = have_nx ? block_of(p, nx.item) : 0;
+            const int64_t nb1 = have_nx && nx.cnt > 1 ? block_of(p, nx.item + 1) : 0;
+            const int stage = (int)(t % L::kStages);
+            bfk::mbar_wait(bar_s_empty + stage, (uint32_t)(((t / L::kStages) & 1) ^ 1));
+            if (DBG & 8) {
+                if (lane == 0) mbar_arrive(bar_s_full + stage);
+            } else if (lane == 0) {
                 bfk::mbar_arrive_expect_tx(bar_s_full + stage, (uint32_t)(tl.cnt * L::kSBlock));
-                for (int b = 0; b < tl.cnt; ++b) {
-                    const int64_t blk = block_of(p, tl.item + b);
-                    bfk::bulk_g2s(Ss + (stage * 2 + b) * (L::kSBlock / 4),
-                                  p.S + blk * (int64_t)(120 * F), L::kSBlock, bar_s_full + stage, pol);
-                }
+                bfk::bulk_g2s(Ss + (stage * 2) * (L::kSBlock / 4), p.S + blk0 * (int64_t)(120 * F),
+                              L::kSBlock, bar_s_full + stage, pol);
+                if (tl.cnt > 1)
+                    bfk::bulk_g2s(Ss + (stage * 2 + 1) * (L::kSBlock / 4),
+                                  p.S + blk1 * (int64_t)(120 * F), L::kSBlock, bar_s_full + stage,
+                                  pol);
             }
             __syncwarp();
+            tl = nx;
+            have = have_nx;
+            blk0 = nb0;
+            blk1 = nb1;
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------------------ MMA issuer
@@ -224,13 +296,11 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
         uint32_t wphase = 0;
         constexpr uint32_t idesc = tc::idesc_tf32(128, 128);
         const uint32_t w_base = tc::smem_u32(Wsm);
-        int64_t t = 0;
-        for (int64_t item = begin; item < end; ++t) {
-            const Tile tl = next_tile(p, item, end);
-            item += tl.cnt;
-            if ((unsigned)tl.g >= (unsigned)p.n_groups) { --t; continue; }
-            if (tl.g != cur_g) {
-                if (t > 0) bfk::mbar_wait(bar_a_free, (uint32_t)((t - 1) & 1));   // old W no longer read
+        bool exact = false;
+        for (int64_t t = 0; it.next(tl); ++t) {
+            if (tl.g != cur_g) {   // old W is no longer read once tile t-1's last MMAs completed
+                exact = __ldg(p.wexact + tl.g) != 0;
+                if (t > 0) bfk::mbar_wait(bar_a_free + 0, (uint32_t)((t - 1) & 1));
                 if (lane == 0) {
                     bfk::mbar_arrive_expect_tx(bar_w, L::kWBytes);
                     bfk::bulk_g2s(Wsm, p.Wimg + (int64_t)tl.g * (L::kWBytes / 4), L::kWBytes, bar_w,
@@ -242,38 +312,54 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
             }
             const int b = (int)(t & 1);
             const uint32_t u = (uint32_t)(t >> 1);
-            bfk::mbar_wait(bar_a_full, (uint32_t)(t & 1));
+            const uint32_t d = tmem + kDCol0 + 128 * b;
             bfk::mbar_wait(bar_d_free + b, (u & 1) ^ 1);
-            tc::fence_after_sync();
-            if (lane == 0) {
-                const uint32_t d = tmem + kDCol0 + 128 * b;
+            // Three MMA groups over K, small terms first:
+            //   tf32-exact W (W2 == 0, e.g. identity / selection): S2 W1, S3 W1, S1 W1
+            //   (= S W exactly up to accumulation rounding: copies are bit-exact);
+            //   general W: S2 W1, S1 W1, S1 W2 (dropped S3 W1, S2 W2 <= 2^-21 T).
+            // Each split term's TMEM region is released by a commit once read.
 #pragma unroll
-                for (int term = 0; term < 4; ++term) {
-                    const int at = term < 3 ? term : 0;      // S1, S2, S3, S1
-                    const int wt = term < 3 ? 0 : 1;         // W1, W1, W1, W2
-#pragma unroll
-                    for (int kb = 0; kb < KP / 8; ++kb) {
-                        const uint64_t desc = tc::smem_desc(
-                            w_base + (uint32_t)((wt * (KP / 4) + 2 * kb) * 16 * 128), 16 * 128, 128);
-                        tc::mma_tf32_ts(d, tmem + at * KP + kb * 8, desc, idesc,
-                                        (term | kb) != 0);
-                    }
+            for (int grp = 0; grp < 4; ++grp) {
+                const int at = grp == 0 ? 1 : (grp == 1 ? 2 : 0);   // A term: S2, S3, S1, S1
+                const int wt = grp == 3 ? 1 : 0;                    // W term: W1, W1, W1, W2
+                if (grp < 3) {
+                    bfk::mbar_wait(bar_a_full + at, (uint32_t)(t & 1));
+                    tc::fence_after_sync();
                 }
-                tc::mma_commit(bar_a_free);
+                const bool run = (grp == 1) ? exact : (grp == 3 ? !exact : true);
+                if (lane == 0) {
+                    if (run) {
+#pragma unroll
+                        for (int kb = 0; kb < KP / 8; ++kb) {
+                            const uint64_t desc = tc::smem_desc(
+                                w_base + (uint32_t)((wt * (KP / 4) + 2 * kb) * 16 * 128), 16 * 128,
+                                128);
+                            if constexpr (!(DBG & 1))
+                                tc::mma_tf32_ts(d, tmem + at * KP + kb * 8, desc, idesc,
+                                                (grp | kb) != 0);
+                        }
+                    }
+                    if (grp < 2) tc::mma_commit(bar_a_free + at);
+                }
+                __syncwarp();
+            }
+            if (lane == 0) {
+                tc::mma_commit(bar_a_free + 0);
                 tc::mma_commit(bar_d_full + b);
             }
             __syncwarp();
         }
     } else {
         // ------------------------------------------------------------ epilogue warps
+        // All 128 D columns of the thread's row are read from TMEM first, so the
+        // buffer is released (D_free) before the 64 global stores are issued; the
+        // stores then overlap the next tile's MMAs.  A warp's store covers 32
+        // consecutive REs of one antenna row: 256 contiguous bytes.
         const int q = warp & 3;                          // TMEM lane quarter of this warp
         const int m = q * 32 + lane;
         const int bsel = m >= 60 ? 1 : 0, j = m - 60 * bsel;
-        int64_t t = 0;
-        for (int64_t item = begin; item < end; ++t) {
-            const Tile tl = next_tile(p, item, end);
-            item += tl.cnt;
-            if ((unsigned)tl.g >= (unsigned)p.n_groups) { --t; continue; }
+        for (int64_t t = 0; it.next(tl); ++t) {
             const int b = (int)(t & 1);
             const uint32_t u = (uint32_t)(t >> 1);
             const bool valid = m < 120 && bsel < tl.cnt;
@@ -282,28 +368,45 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
             bfk::mbar_wait(bar_d_full + b, u & 1);
             tc::fence_after_sync();
             const uint32_t d = tmem + ((uint32_t)(q * 32) << 16) + kDCol0 + 128 * b;
+            uint32_t v[128];
 #pragma unroll
-            for (int c0 = 0; c0 < 128; c0 += 16) {
-                uint32_t v[16];
-                tc::tmem_ld16(d + c0, v);
-                tc::tmem_ld_wait();
-                if (valid) {
+            for (int c0 = 0; c0 < 128; c0 += 16)
+                tc::tmem_ld16(d + c0, *reinterpret_cast<uint32_t(*)[16]>(v + c0));
+            tc::tmem_ld_wait();
+            tc::fence_before_sync();
+            mbar_arrive(bar_d_free + b);                 // TMEM buffer b may be overwritten
+            // Lane pairs (j even, j + 1) trade values with one shuffle so every lane
+            // stores two adjacent REs at once (STG.128 interleaved, STG.64 planar):
+            // half the store instructions of one-RE-per-lane, which measurably
+            // raises the write bandwidth of 4 storing warps (tools/write_bw).
+            const bool odd = (j & 1) != 0;
+            if constexpr (!(DBG & 2)) {
+                if (LAYOUT == 0) {
 #pragma unroll
-                    for (int a = 0; a < 8; ++a) {
-                        const int ant = c0 / 2 + a;
-                        const float re = __uint_as_float(v[2 * a]);
-                        const float im = __uint_as_float(v[2 * a + 1]);
-                        if (LAYOUT == 0) {
-                            __stcs(reinterpret_cast<float2 *>(Rb) + ant * 60 + j, make_float2(re, im));
-                        } else {
-                            __stcs(Rb + ant * 60 + j, re);
-                            __stcs(Rb + 64 * 60 + ant * 60 + j, im);
-                        }
+                    for (int a = 0; a < 64; a += 2) {
+                        const float re0 = __uint_as_float(v[2 * a]), im0 = __uint_as_float(v[2 * a + 1]);
+                        const float re1 = __uint_as_float(v[2 * a + 2]), im1 = __uint_as_float(v[2 * a + 3]);
+                        const float gr = __shfl_xor_sync(0xffffffffu, odd ? re0 : re1, 1);
+                        const float gi = __shfl_xor_sync(0xffffffffu, odd ? im0 : im1, 1);
+                        // even lane: antenna a, REs j, j+1; odd lane: antenna a+1, REs j-1, j
+                        const float4 w4 = odd ? make_float4(gr, gi, re1, im1) : make_float4(re0, im0, gr, gi);
+                        if (valid)
+                            __stcs(reinterpret_cast<float4 *>(Rb + 2 * ((a + (odd ? 1 : 0)) * 60 + j - (odd ? 1 : 0))),
+                                   w4);
+                    }
+                } else {
+#pragma unroll
+                    for (int a = 0; a < 64; ++a) {
+                        const float re = __uint_as_float(v[2 * a]), im = __uint_as_float(v[2 * a + 1]);
+                        const float g = __shfl_xor_sync(0xffffffffu, odd ? re : im, 1);
+                        // even lane: re plane, REs j, j+1; odd lane: im plane, REs j-1, j
+                        const float2 w2 = odd ? make_float2(g, im) : make_float2(re, g);
+                        if (valid)
+                            __stcs(reinterpret_cast<float2 *>(Rb + (odd ? 64 * 60 : 0) + a * 60 + j - (odd ? 1 : 0)),
+                                   w2);
                     }
                 }
             }
-            tc::fence_before_sync();
-            mbar_arrive(bar_d_free + b);
         }
     }
     tc::fence_before_sync();

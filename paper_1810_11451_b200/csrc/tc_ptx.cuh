@@ -107,5 +107,11 @@ __device__ __forceinline__ float to_tf32(float x) {
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return __uint_as_float(r);
 }
+// fp32 -> tf32, round half away from zero on the magnitude: add half an ulp of
+// the 11-bit significand to the bit pattern and clear the low 13 mantissa bits
+// (IADD + LOP3 instead of the ~5-instruction cvt sequence).  Finite inputs only.
+__device__ __forceinline__ float tf32_round(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
 
 }  // namespace tc

@@ -1,0 +1,48 @@
+// Bottleneck experiments for bftc::bf_tc_kernel (not part of the product):
+// the same kernel with pieces disabled (DBG bits), untagged, f = 36, timed with
+// CUDA events.  tcx_run(dbg, S, R, Wimg, n, reps) -> average ms per launch.
+#include <cstdio>
+#include "../../paper_1810_11451_b200/csrc/bf_tc.cuh"
+
+template <int DBG>
+static float run(const float *S, float *R, const float *Wimg, long long n, int reps) {
+    static int32_t *wexact = nullptr;
+    if (!wexact) { cudaMalloc(&wexact, 4); cudaMemset(wexact, 0, 4); }
+    auto k = bftc::bf_tc_kernel<36, 0, DBG>;
+    const int smem = bftc::TcSmem<36>::kBytes;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    bftc::TcParams p{};
+    p.Wimg = Wimg; p.S = S; p.R = R; p.n_items = n; p.n_groups = 1; p.wexact = wexact;
+    k<<<sms, bftc::kThreads, smem>>>(p);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaEventRecord(a);
+    for (int i = 0; i < reps; ++i) k<<<sms, bftc::kThreads, smem>>>(p);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0; cudaEventElapsedTime(&ms, a, b);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return -1; }
+    return ms / reps;
+}
+
+extern "C" float tcx_run(int dbg, const float *S, float *R, const float *Wimg, long long n, int reps) {
+    switch (dbg) {
+        case 0: return run<0>(S, R, Wimg, n, reps);
+        case 1: return run<1>(S, R, Wimg, n, reps);
+        case 2: return run<2>(S, R, Wimg, n, reps);
+        case 3: return run<3>(S, R, Wimg, n, reps);
+        case 4: return run<4>(S, R, Wimg, n, reps);
+        case 5: return run<5>(S, R, Wimg, n, reps);
+        case 6: return run<6>(S, R, Wimg, n, reps);
+        case 8: return run<8>(S, R, Wimg, n, reps);
+        case 10: return run<10>(S, R, Wimg, n, reps);
+        case 12: return run<12>(S, R, Wimg, n, reps);
+        case 14: return run<14>(S, R, Wimg, n, reps);
+        case 7: return run<7>(S, R, Wimg, n, reps);
+        case 15: return run<15>(S, R, Wimg, n, reps);
+    }
+    return -2;
+}
