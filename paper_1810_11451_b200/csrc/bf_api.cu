@@ -47,7 +47,7 @@ bf_status cuda_fail(cudaError_t e, const char *what) {
 
 constexpr int kMaxGroups = 1024;
 constexpr int kRouteThreads = 256;         // 8 warps
-constexpr int kRouteMinTile = 4096;
+constexpr int kRouteMinTile = 512;          // small batches still spread over several CTAs
 constexpr int kRouteMaxTable = 65536;      // tiles x (groups + 1) entries
 constexpr int64_t kDefaultHostChunk = 2048;
 constexpr int kHostSlots = 3;
