@@ -43,6 +43,7 @@ KIND_S = 2
 KIND_TAG = 3
 KIND_MOD = 4
 KIND_CELLF = 5
+KIND_FSIG = 6     # filter-stage input signals
 
 W_STRIDE_I = 256
 W_STRIDE_K = 64
@@ -310,3 +311,58 @@ def workload_inputs(wl: Workload, block_ids=None):
     S = qam_symbols(wl.seed, wl.sub, block_ids, wl.f, wl.b, wl.M)
     tags = subband_tags(wl.seed, block_ids, wl.n_groups) if wl.tagged else None
     return W, S, tags
+
+
+# --------------------------------------------------------------------------
+# Filter stage: signals and the filter sequence
+# --------------------------------------------------------------------------
+FILTER_N = 2048      # "FFT sizes are all 2048"
+
+
+def filter_signals(seed: int, sub: int, sig_ids, n: int = FILTER_N, M: int = 64) -> np.ndarray:
+    """complex64 [n_sig][n] synthetic time samples: square M-QAM points, index e = sig*n + k."""
+    ids = np.asarray(sig_ids, dtype=np.uint64).reshape(-1, 1)
+    e = ids * np.uint64(n) + np.arange(n, dtype=np.uint64).reshape(1, -1)
+    h = counter_hash(stream_key(seed, KIND_FSIG, sub), e)
+    L = int(round(math.sqrt(M)))
+    lv = qam_levels(M)
+    out = np.empty(h.shape, dtype=np.complex64)
+    out.real = lv[(h & np.uint64(L - 1)).astype(np.int64)]
+    out.imag = lv[((h >> np.uint64(8)) & np.uint64(L - 1)).astype(np.int64)]
+    return out
+
+
+def filter_taps(n: int = FILTER_N, taps: int = 64, cutoff: float = 0.25) -> np.ndarray:
+    """The filter sequence h (complex64 [n]): a Hann-windowed sinc low-pass FIR of
+    `taps` real taps (normalised cutoff in cycles/sample, DC gain 1), zero-padded to n.
+    Computed in fp64, rounded once to fp32."""
+    k = np.arange(taps, dtype=np.float64) - (taps - 1) / 2.0
+    h = 2.0 * cutoff * np.sinc(2.0 * cutoff * k) * (0.5 - 0.5 * np.cos(2 * np.pi * np.arange(taps) / (taps - 1)))
+    h /= h.sum()
+    out = np.zeros(n, dtype=np.complex64)
+    out[:taps] = h.astype(np.float32)
+    return out
+
+
+@dataclass(frozen=True)
+class FilterWorkload:
+    name: str
+    n: int
+    n_signals: int
+    M: int
+    seed: int
+    desc: str = ""
+
+    @property
+    def signal_bytes(self) -> int:
+        """Algorithmic bytes per signal: read s + write y (complex fp32)."""
+        return 2 * 8 * self.n
+
+
+def filter_workload(name: str) -> FilterWorkload:
+    if name == "fl0":
+        return FilterWorkload("fl0", FILTER_N, 16, 64, 5, "16 signals of 2048 64-QAM samples, seed 5")
+    if name == "fl1":
+        return FilterWorkload("fl1", FILTER_N, 1 << 18, 64, 6,
+                              "2^18 signals of 2048 64-QAM samples (4.3 GB in + out), seed 6")
+    raise ValueError(name)

@@ -6,9 +6,10 @@ package.  The product package ``paper_1810_11451_b200`` never imports it and
 shares no code with it; the only shared module is the input generator
 ``bf_synth`` (no arithmetic of the method).
 
-The arithmetic lives in ``bf_oracle.c`` (plain C, fp64 accumulation, one
-rounding to fp32; see its header for the passage-by-passage reading).  This
-file only builds the C library with gcc if needed and marshals numpy arrays.
+The arithmetic lives in ``bf_oracle.c`` (beamforming) and
+``filter_oracle.c`` (the filter stage IFFT(MULT(FFT(s)))): plain
+C, fp64, one rounding to fp32; see their headers for the passage-by-passage
+reading.  This file only builds the C library with gcc and marshals numpy arrays.
 
 Pins (tests/test_oracle_pins.py, ``-m "not gpu"``): hand-expanded golden
 fixture (tests/golden/), f = 0 closed form, identity / selection / permutation
@@ -27,7 +28,7 @@ import tempfile
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRC = os.path.join(_HERE, "bf_oracle.c")
+_SRCS = [os.path.join(_HERE, "bf_oracle.c"), os.path.join(_HERE, "filter_oracle.c")]
 _LIB = os.path.join(_HERE, "libbforacle.so")
 _CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math",
            "-pthread"]
@@ -37,12 +38,12 @@ _lib = None
 def build(force: bool = False) -> str:
     """Compile bf_oracle.c with gcc into oracle/libbforacle.so (atomic rename)."""
     if (not force and os.path.exists(_LIB)
-            and os.path.getmtime(_LIB) >= os.path.getmtime(_SRC)):
+            and all(os.path.getmtime(_LIB) >= os.path.getmtime(src) for src in _SRCS)):
         return _LIB
     fd, tmp = tempfile.mkstemp(suffix=".so", dir=_HERE)
     os.close(fd)
     try:
-        subprocess.run(["gcc", *_CFLAGS, "-o", tmp, _SRC, "-lm"], check=True)
+        subprocess.run(["gcc", *_CFLAGS, "-o", tmp, *_SRCS, "-lm"], check=True)
         os.replace(tmp, _LIB)
     finally:
         if os.path.exists(tmp):
@@ -59,6 +60,13 @@ def _load():
             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
             ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int64)]
+        lib.fo_dft.restype = ctypes.c_int
+        lib.fo_dft.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
+                               ctypes.c_int]
+        lib.fo_filter.restype = ctypes.c_int
+        lib.fo_filter.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                  ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
+                                  ctypes.c_int]
         _lib = lib
     return _lib
 
@@ -105,3 +113,39 @@ def max_threads() -> int:
         return len(os.sched_getaffinity(0))
     except AttributeError:  # pragma: no cover
         return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# Filter stage: IFFT(MULT(FFT(s))), n = 2048
+# ---------------------------------------------------------------------------
+def dft(x: np.ndarray, inverse: bool = False) -> np.ndarray:
+    """Direct O(n^2) DFT of the last axis in fp64 (unnormalised forward, 1/n inverse)."""
+    x = np.ascontiguousarray(x, dtype=np.complex64)
+    flat = x.reshape(-1, x.shape[-1])
+    out = np.empty_like(flat)
+    rc = _load().fo_dft(_ptr(flat), _ptr(out), flat.shape[-1], flat.shape[0], int(inverse))
+    if rc != 0:
+        raise ValueError("oracle rejected the arguments")
+    return out.reshape(x.shape)
+
+
+def filter_apply(s: np.ndarray, h: np.ndarray, n_threads: int = 1, direct: bool = False):
+    """y = IDFT(DFT(h) . DFT(s)) per signal (direct=True: circular convolution s (*) h).
+
+    s: complex64 [n_sig][n]; h: complex64 [n] (the filter sequence).
+    Returns (y complex64 [n_sig][n], bound float64 [n_sig] = ||s||_2 max|DFT(h)|).
+    """
+    s = np.ascontiguousarray(s, dtype=np.complex64)
+    if s.ndim == 1:
+        s = s[None]
+    h = np.ascontiguousarray(h, dtype=np.complex64).reshape(-1)
+    n_sig, n = s.shape
+    if h.shape[0] != n:
+        raise ValueError("h must have the signal length")
+    y = np.empty_like(s)
+    bound = np.empty(n_sig, dtype=np.float64)
+    rc = _load().fo_filter(_ptr(s), _ptr(h), _ptr(y), _ptr(bound), n, n_sig, 1 if direct else 0,
+                           int(n_threads))
+    if rc != 0:
+        raise ValueError("oracle rejected the arguments")
+    return y, bound

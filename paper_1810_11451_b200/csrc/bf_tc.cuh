@@ -22,16 +22,16 @@
 // over 3 x KP/8 MMAs stays near 2e-6 T at f = 36, inside the
 // 1e-5 T contract.
 //
-// One CTA (10 warps) per SM, persistent over a contiguous range of the
+// One CTA (14 warps) per SM, persistent over a contiguous range of the
 // group-sorted block list; tiles are 2 consecutive blocks of the same group.
-//   warp 9     S producer: cp.async.bulk (TMA bulk engine) of each block's
+//   warp 13    S producer: cp.async.bulk (TMA bulk engine) of each block's
 //              480 F contiguous bytes into a 4-stage shared-memory ring,
 //              completing on mbarriers, up to 4 tiles ahead of the split;
 //   warps 0-3  split: LDS S (conflict-free, one RE column per lane), split into
 //              3 tf32 terms, tcgen05.st into the A region (one TMEM lane per RE);
 //   warp 4     MMA issuer (one thread) and W loader (cp.async.bulk of the
 //              group's pre-split B image into SMEM on a group change);
-//   warps 5-8  epilogue: tcgen05.ld of a whole D row (128 columns), release of
+//   warps 5-12 epilogue (two per lane quarter, half the D columns each): tcgen05.ld of a whole D row (128 columns), release of
 //              the TMEM buffer, then stores of two adjacent REs per lane (lane
 //              pairs trade one shuffle) — 256 contiguous bytes per antenna row.
 // TMEM: A terms at columns [0, 3 KP), D double buffer at [256, 384), [384, 512).
@@ -44,11 +44,12 @@
 
 namespace bftc {
 
-constexpr int kThreads = 320;
+constexpr int kThreads = 448;
 constexpr int kSplitWarps = 4;
 constexpr int kMmaWarp = 4;
 constexpr int kEpiWarp0 = 5;
-constexpr int kProdWarp = 9;
+constexpr int kEpiWarps = 8;          // two per TMEM lane quarter, 64 D columns each
+constexpr int kProdWarp = 13;
 constexpr int kMaxStages = 4;          // S ring depth (tiles), shared memory permitting
 constexpr int kSmemLimit = 232448;     // 227 KB per CTA
 constexpr int kDCol0 = 256;
@@ -170,8 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
         }
         bfk::mbar_init(bar_d_full + 0, 1);
         bfk::mbar_init(bar_d_full + 1, 1);
-        bfk::mbar_init(bar_d_free + 0, 128);
-        bfk::mbar_init(bar_d_free + 1, 128);
+        bfk::mbar_init(bar_d_free + 0, 32 * kEpiWarps);
+        bfk::mbar_init(bar_d_free + 1, 32 * kEpiWarps);
         bfk::mbar_init(bar_w, 1);
         for (int i = 0; i < L::kStages; ++i) {
             bfk::mbar_init(bar_s_full + i, 1);
@@ -352,11 +353,14 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
         }
     } else {
         // ------------------------------------------------------------ epilogue warps
-        // All 128 D columns of the thread's row are read from TMEM first, so the
-        // buffer is released (D_free) before the 64 global stores are issued; the
-        // stores then overlap the next tile's MMAs.  A warp's store covers 32
-        // consecutive REs of one antenna row: 256 contiguous bytes.
+        // Two warps per TMEM lane quarter; each reads its 64 D columns (32 antennas)
+        // of the thread's row from TMEM first, so the buffer is released (D_free)
+        // before the global stores are issued; the stores then overlap the next
+        // tile's MMAs.  A warp's store covers 32 consecutive REs of one antenna row:
+        // 256 contiguous bytes.  Eight storing warps keep more writes in flight
+        // than four (tools/write_bw).
         const int q = warp & 3;                          // TMEM lane quarter of this warp
+        const int h = (warp - kEpiWarp0) >> 2;           // D columns [64 h, 64 h + 64)
         const int m = q * 32 + lane;
         const int bsel = m >= 60 ? 1 : 0, j = m - 60 * bsel;
         for (int64_t t = 0; it.next(tl); ++t) {
@@ -367,10 +371,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
             float *Rb = p.R + blk * (int64_t)bfk::kRBlockFloats;
             bfk::mbar_wait(bar_d_full + b, u & 1);
             tc::fence_after_sync();
-            const uint32_t d = tmem + ((uint32_t)(q * 32) << 16) + kDCol0 + 128 * b;
-            uint32_t v[128];
+            const uint32_t d = tmem + ((uint32_t)(q * 32) << 16) + kDCol0 + 128 * b + 64 * h;
+            uint32_t v[64];
 #pragma unroll
-            for (int c0 = 0; c0 < 128; c0 += 16)
+            for (int c0 = 0; c0 < 64; c0 += 16)
                 tc::tmem_ld16(d + c0, *reinterpret_cast<uint32_t(*)[16]>(v + c0));
             tc::tmem_ld_wait();
             tc::fence_before_sync();
@@ -383,9 +387,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
             if constexpr (!(DBG & 2)) {
                 if (LAYOUT == 0) {
 #pragma unroll
-                    for (int a = 0; a < 64; a += 2) {
-                        const float re0 = __uint_as_float(v[2 * a]), im0 = __uint_as_float(v[2 * a + 1]);
-                        const float re1 = __uint_as_float(v[2 * a + 2]), im1 = __uint_as_float(v[2 * a + 3]);
+                    for (int aa = 0; aa < 32; aa += 2) {
+                        const int a = 32 * h + aa;
+                        const float re0 = __uint_as_float(v[2 * aa]), im0 = __uint_as_float(v[2 * aa + 1]);
+                        const float re1 = __uint_as_float(v[2 * aa + 2]), im1 = __uint_as_float(v[2 * aa + 3]);
                         const float gr = __shfl_xor_sync(0xffffffffu, odd ? re0 : re1, 1);
                         const float gi = __shfl_xor_sync(0xffffffffu, odd ? im0 : im1, 1);
                         // even lane: antenna a, REs j, j+1; odd lane: antenna a+1, REs j-1, j
@@ -396,8 +401,9 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
                     }
                 } else {
 #pragma unroll
-                    for (int a = 0; a < 64; ++a) {
-                        const float re = __uint_as_float(v[2 * a]), im = __uint_as_float(v[2 * a + 1]);
+                    for (int aa = 0; aa < 32; ++aa) {
+                        const int a = 32 * h + aa;
+                        const float re = __uint_as_float(v[2 * aa]), im = __uint_as_float(v[2 * aa + 1]);
                         const float g = __shfl_xor_sync(0xffffffffu, odd ? re : im, 1);
                         // even lane: re plane, REs j, j+1; odd lane: im plane, REs j-1, j
                         const float2 w2 = odd ? make_float2(g, im) : make_float2(re, g);

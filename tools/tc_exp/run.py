@@ -11,6 +11,9 @@ secs = float(sys.argv[2]) if len(sys.argv) > 2 else 0.0
 S = torch.randn(n * 36 * 60 * 2, device="cuda")
 R = torch.empty(n * 7680, device="cuda")
 W = torch.zeros(2 * 72 * 128, device="cuda")
+if os.environ.get("TCX_W", "zero") == "random":
+    W = torch.randn(2 * 72 * 128, device="cuda") * 0.1
+    W[72 * 128:] *= 2.0 ** -12          # second term ~ the W2 residual of a real split
 names = {0: "full", 1: "no-mma", 2: "no-store", 3: "no-mma,no-store", 4: "no-split", 5: "no-mma,no-split",
          6: "no-store,no-split", 7: "only-loads", 8: "no-loads", 10: "no-loads,no-store", 12: "no-loads,no-split",
          14: "only-mma", 15: "nothing"}
