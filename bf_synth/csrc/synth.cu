@@ -72,6 +72,17 @@ __global__ void gen_mods(int32_t *__restrict__ out, const int64_t *__restrict__ 
     }
 }
 
+__global__ void gen_signal(float2 *__restrict__ out, int64_t first, int64_t n_sig, int n,
+                           uint64_t key, Levels L, int mod_idx) {
+    const int64_t total = n_sig * n;
+    const uint64_t mask = (mod_idx == 0) ? 1u : (mod_idx == 1 ? 3u : 7u);
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t h = hash_at(key, (uint64_t)(first * n + e));
+        out[e] = make_float2(L.lv[mod_idx][h & mask], L.lv[mod_idx][(h >> 8) & mask]);
+    }
+}
+
 __global__ void fill_u32(uint32_t *__restrict__ p, int64_t n, uint32_t v) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -113,6 +124,19 @@ int bfs_gen_mods(int32_t *out, const int64_t *ids, int64_t first, int64_t n, uin
                  void *stream) {
     if (n <= 0) return 0;
     gen_mods<<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(out, ids, first, n, key);
+    return (int)cudaGetLastError();
+}
+
+// Filter-stage signals: n_sig x n complex samples of square M-QAM, element
+// index e = sig * n + k (bf_synth.filter_signals).
+int bfs_gen_signals(float *out, int64_t first, int64_t n_sig, int n, uint64_t key,
+                    const float *levels24, int mod_idx, void *stream) {
+    if (n_sig <= 0) return 0;
+    Levels L;
+    for (int m = 0; m < 3; ++m)
+        for (int i = 0; i < 8; ++i) L.lv[m][i] = levels24[m * 8 + i];
+    gen_signal<<<grid_for(n_sig * n), 256, 0, (cudaStream_t)stream>>>((float2 *)out, first, n_sig, n,
+                                                                      key, L, mod_idx);
     return (int)cudaGetLastError();
 }
 

@@ -12,7 +12,8 @@ import os
 import numpy as np
 import torch
 
-from . import (KIND_MOD, KIND_S, KIND_TAG, MODULATIONS, Workload, qam_levels, stream_key)
+from . import (KIND_FSIG, KIND_MOD, KIND_S, KIND_TAG, MODULATIONS, Workload, qam_levels,
+               stream_key)
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbfsynth.so")
 _lib = None
@@ -29,7 +30,8 @@ def _load():
         L.bfs_gen_tags.argtypes = [vp, vp, i64, i64, u64, i32, vp]
         L.bfs_gen_mods.argtypes = [vp, vp, i64, i64, u64, vp]
         L.bfs_fill_u32.argtypes = [vp, i64, ctypes.c_uint32, vp]
-        for f in (L.bfs_gen_qam, L.bfs_gen_tags, L.bfs_gen_mods, L.bfs_fill_u32):
+        L.bfs_gen_signals.argtypes = [vp, i64, i64, i32, u64, vp, i32, vp]
+        for f in (L.bfs_gen_qam, L.bfs_gen_tags, L.bfs_gen_mods, L.bfs_fill_u32, L.bfs_gen_signals):
             f.restype = i32
         _lib = L
     return _lib
@@ -112,3 +114,16 @@ def workload_device(wl: Workload, device, first: int = 0, n: int | None = None,
         if n > 0:
             gen_tags(tags, wl.seed, wl.n_groups, first=first, ids=ids)
     return S, tags
+
+
+def gen_filter_signals(out: torch.Tensor, seed: int, sub: int = 0, first: int = 0,
+                       M: int = 64) -> torch.Tensor:
+    """Fill out (cuda complex64 [n_sig][n]) with bf_synth.filter_signals(seed, sub, first + i)."""
+    n_sig, n = out.shape
+    lv = np.ascontiguousarray(_LEVELS)
+    rc = _load().bfs_gen_signals(ctypes.c_void_p(out.data_ptr()), int(first), int(n_sig), int(n),
+                                 stream_key(seed, KIND_FSIG, sub), lv.ctypes.data_as(ctypes.c_void_p),
+                                 MODULATIONS.index(M), _stream())
+    if rc:
+        raise RuntimeError(f"bfs_gen_signals failed: cudaError {rc}")
+    return out

@@ -16,6 +16,8 @@ EXPORTS = ("bf_plan_create", "bf_set_precoders", "bf_apply", "bf_apply_host", "b
            "bf_destroy", "bf_plan_set_profiling", "bf_plan_kernel_time",
            "bf_plan_launch_count", "bf_plan_set_host_chunk", "bf_plan_kernel_config",
            "bf_plan_set_variant", "bf_plan_get_variant",
+           "bff_plan_create", "bff_set_taps", "bff_apply", "bff_fft", "bff_destroy",
+           "bff_plan_set_profiling", "bff_plan_kernel_time", "bff_plan_launch_count",
            "bf_status_string", "bf_last_error", "bf_version")
 
 

@@ -18,32 +18,19 @@
 
 #include "bf.h"
 #include "bf_dispatch.h"
+#include "bf_host.h"
 #include "bf_ffma.cuh"
 #include "bf_tc.cuh"
 
+namespace bfh {
+thread_local std::string g_last_error;
+}
+
 namespace {
 
-thread_local std::string g_last_error;
-
-bf_status fail(bf_status s, const char *fmt, ...) {
-    char buf[512];
-    va_list ap;
-    va_start(ap, fmt);
-    vsnprintf(buf, sizeof(buf), fmt, ap);
-    va_end(ap);
-    g_last_error = buf;
-    return s;
-}
-
-bf_status cuda_fail(cudaError_t e, const char *what) {
-    return fail(BF_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
-}
-
-#define BF_CUDA(call)                                  \
-    do {                                               \
-        cudaError_t e_ = (call);                       \
-        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
-    } while (0)
+using bfh::fail;
+using bfh::cuda_fail;
+using bfh::DeviceGuard;
 
 constexpr int kMaxGroups = 1024;
 constexpr int kRouteThreads = 256;         // 8 warps
@@ -264,19 +251,6 @@ __global__ void bf_route_scatter(const int32_t *__restrict__ gidx, int64_t n, in
         __syncwarp();
     }
 }
-
-struct DeviceGuard {
-    int prev = -1;
-    bool changed = false;
-    explicit DeviceGuard(int dev) {
-        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) {
-            changed = cudaSetDevice(dev) == cudaSuccess;
-        }
-    }
-    ~DeviceGuard() {
-        if (changed) cudaSetDevice(prev);
-    }
-};
 
 template <typename T>
 bf_status grow(T **ptr, int64_t *cap, int64_t need, const char *what) {
@@ -509,7 +483,7 @@ const char *bf_status_string(bf_status s) {
     return "BF_ERR_UNKNOWN";
 }
 
-const char *bf_last_error(void) { return g_last_error.c_str(); }
+const char *bf_last_error(void) { return bfh::g_last_error.c_str(); }
 
 bf_status bf_plan_create(int n_ant, int f, int b, int layout, bf_plan_t *out) {
     if (!out) return fail(BF_ERR_INVALID_VALUE, "out is NULL");

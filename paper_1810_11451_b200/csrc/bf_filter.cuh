@@ -1,0 +1,245 @@
+// bf_filter.cuh — fused filter stage y = IFFT(H . FFT(s)) for n = 2048
+// (§III: "The filter algorithm computes IFFT(MULT(FFT(s))) where
+// MULT is the pointwise multiplication by the FFT of the filter sequence and
+// FFT sizes are all 2048").
+//
+// One CTA of 128 threads per signal (grid-stride over signals).  The forward
+// FFT, the pointwise product with H and the inverse FFT run in one kernel, so
+// each signal is read from HBM once and written once (32 KB per signal) — the
+// paper replaced its hand FFT by a vendor library; here the three steps are
+// fused, which a library call sequence cannot do.
+//
+// FFT: Stockham autosort, passes radix 16, 16, 8 (2048 = 16 * 16 * 8).  A pass with
+// stride Ns and radix R: butterfly j loads x[j + r N/R] (r < R), multiplies by
+// w^(r k N/(Ns R)) with k = j mod Ns and w = e^{-2 pi i / N} (fp32 table built in
+// fp64), does a DFT_R, and writes y[(j / Ns) Ns R + k + r Ns].  Thread t owns
+// butterfly t (and t + 128 in the radix-8 pass), so the first pass reads
+// x[t + 128 r] straight from HBM (coalesced) and the last pass leaves
+// X[t + 128 q] (natural order) in registers: MULT by H, and the inverse
+// transform (conj(FFT(conj(.))) / N) starts from registers again.  Between
+// passes values go through shared memory (two exchanges per transform) with
+// the padded index i + i/16 (conflict-free for the stride-16 writes of pass 1).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "bf_ffma.cuh"   // mbarrier / bulk-copy helpers
+
+namespace bff {
+
+constexpr int kN = 2048;
+constexpr int kThreads = 128;
+constexpr int kPad = kN + kN / 16;           // padded shared-memory slots (float2)
+// Twiddle table tw[m] = w^m = e^{-2 pi i m / N} (fp64-evaluated, rounded once), read
+// through L1.  A pass needs w^(c r k) for r < R: the kernel loads the binary powers
+// w^(c k 2^e) from the table and forms the others with at most 3 complex products
+// (relative error <= 4 * 2^-24), which keeps 4 instead of R - 1 twiddles live.
+constexpr int kTwN = kN;
+// Per-pass tables in shared memory, [r][k] (lanes read consecutive words): pass 2
+// w^(8 r k) (r 1..15, k < 16), pass 3 w^(r k) (r 1..7, k < 256).
+constexpr int kTw2 = 0, kTw3 = kTw2 + 15 * 16, kTwS = kTw3 + 7 * 256;
+
+
+
+__device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }   // a * (-i)
+__device__ __forceinline__ float2 conj2(float2 a) { return make_float2(a.x, -a.y); }
+
+// w^(m r) for r in [1, 16) from b[e] = w^(m 2^e), e < 4 (r is a compile-time constant).
+__device__ __forceinline__ float2 tw_pow(const float2 (&b)[4], int r) {
+    float2 acc = make_float2(1.0f, 0.0f);
+    bool first = true;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if (r & (1 << e)) {
+            acc = first ? b[e] : cmul(acc, b[e]);
+            first = false;
+        }
+    }
+    return acc;
+}
+
+// forward DFT4 (w = -i) in place
+__device__ __forceinline__ void dft4(float2 &x0, float2 &x1, float2 &x2, float2 &x3) {
+    const float2 t0 = cadd(x0, x2), t1 = csub(x0, x2), t2 = cadd(x1, x3), t3 = mul_mi(csub(x1, x3));
+    x0 = cadd(t0, t2);
+    x2 = csub(t0, t2);
+    x1 = cadd(t1, t3);
+    x3 = csub(t1, t3);
+}
+
+// forward DFT8 in place (v[k] <- sum_r v[r] e^{-2 pi i r k / 8})
+template <int S>
+__device__ __forceinline__ void dft8(float2 *v) {   // elements v[0], v[S], ..., v[7 S]
+    float2 e0 = v[0], e1 = v[2 * S], e2 = v[4 * S], e3 = v[6 * S];
+    float2 o0 = v[S], o1 = v[3 * S], o2 = v[5 * S], o3 = v[7 * S];
+    dft4(e0, e1, e2, e3);
+    dft4(o0, o1, o2, o3);
+    const float h = 0.70710678118654752440f;
+    // o_k *= W8^k: W8 = (1 - i)/sqrt2, W8^2 = -i, W8^3 = (-1 - i)/sqrt2
+    o1 = make_float2((o1.x + o1.y) * h, (o1.y - o1.x) * h);
+    o2 = mul_mi(o2);
+    o3 = make_float2((o3.y - o3.x) * h, -(o3.x + o3.y) * h);
+    v[0] = cadd(e0, o0); v[4 * S] = csub(e0, o0);
+    v[S] = cadd(e1, o1); v[5 * S] = csub(e1, o1);
+    v[2 * S] = cadd(e2, o2); v[6 * S] = csub(e2, o2);
+    v[3 * S] = cadd(e3, o3); v[7 * S] = csub(e3, o3);
+}
+
+// forward DFT16, 4 x 4: n = n2 + 4 n1, k = k1 + 4 k2,
+// X[k1 + 4 k2] = sum_n2 W4^(n2 k2) W16^(n2 k1) sum_n1 v[n2 + 4 n1] W4^(n1 k1).
+// The result is left TRANSPOSED in place: X[k1 + 4 k2] is in v[4 k1 + k2]
+// (tr16(k) below), which saves a 16-value copy; callers index with tr16.
+__host__ __device__ constexpr int tr16(int k) { return ((k & 3) << 2) | (k >> 2); }
+__device__ __forceinline__ void dft16(float2 (&v)[16]) {
+    const float c1 = 0.92387953251128675613f, s1 = 0.38268343236508977173f;   // cos, sin(pi/8)
+    const float h = 0.70710678118654752440f;
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4(v[n2], v[n2 + 4], v[n2 + 8], v[n2 + 12]);
+    // u[n2][k1] = v[n2 + 4 k1] after the inner DFT4s; twiddle by W16^(n2 k1)
+    // W16^1 = c1 - i s1, W16^2 = h - i h, W16^3 = s1 - i c1, W16^4 = -i, W16^6 = -h - i h,
+    // W16^9 = -c1 + i s1... only n2 k1 in {1, 2, 3, 2, 4, 6, 3, 6, 9} occur.
+    v[5] = make_float2(v[5].x * c1 + v[5].y * s1, v[5].y * c1 - v[5].x * s1);        // W^1
+    v[9] = make_float2((v[9].x + v[9].y) * h, (v[9].y - v[9].x) * h);               // W^2
+    v[13] = make_float2(v[13].x * s1 + v[13].y * c1, v[13].y * s1 - v[13].x * c1);  // W^3
+    v[6] = make_float2((v[6].x + v[6].y) * h, (v[6].y - v[6].x) * h);               // W^2
+    v[10] = mul_mi(v[10]);                                                         // W^4
+    v[14] = make_float2((v[14].y - v[14].x) * h, -(v[14].x + v[14].y) * h);         // W^6
+    v[7] = make_float2(v[7].x * s1 + v[7].y * c1, v[7].y * s1 - v[7].x * c1);       // W^3
+    v[11] = make_float2((v[11].y - v[11].x) * h, -(v[11].x + v[11].y) * h);        // W^6
+    v[15] = make_float2(-v[15].x * c1 - v[15].y * s1, v[15].x * s1 - v[15].y * c1); // W^9
+    // outer DFT4 over n2 for each k1: inputs v[4 k1 + n2] -> X[k1 + 4 k2] in v[4 k1 + k2]
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+}
+
+// One forward FFT of the CTA's signal (radix 16, 16, 8 Stockham).
+// In: v[q] = x[t + 128 q].  Out: v[q] = X[t + 128 q].
+__device__ __forceinline__ void fft2048(float2 (&v)[16], float2 *sm, const float2 *tw, int t) {
+    // pass 1: Ns = 1, R = 16 (no twiddles); y[16 j + r]
+    dft16(v);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) sm[pad(16 * t + r)] = v[tr16(r)];
+    __syncthreads();
+    // pass 2: Ns = 16, R = 16; twiddles w^(8 r k), k = j mod 16; y[(j/16) 256 + k + 16 r]
+    {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = sm[pad(t + 128 * r)];
+        const int k = t & 15;
+#pragma unroll
+        for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], tw[kTw2 + (r - 1) * 16 + k]);
+        dft16(v);
+        __syncthreads();
+        const int base = (t >> 4) * 256 + k;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) sm[pad(base + 16 * r)] = v[tr16(r)];
+        __syncthreads();
+    }
+    // pass 3: Ns = 256, R = 8, butterflies j = t and t + 128; twiddles w^(r j); y[j + 256 r]
+    {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            v[2 * r] = sm[pad(t + 256 * r)];
+            v[2 * r + 1] = sm[pad(t + 128 + 256 * r)];
+        }
+#pragma unroll
+        for (int r = 1; r < 8; ++r) {
+            v[2 * r] = cmul(v[2 * r], tw[kTw3 + (r - 1) * 256 + t]);
+            v[2 * r + 1] = cmul(v[2 * r + 1], tw[kTw3 + (r - 1) * 256 + t + 128]);
+        }
+        dft8<2>(v);        // butterfly t:       v[0], v[2], ..., v[14]
+        dft8<2>(v + 1);    // butterfly t + 128: v[1], v[3], ..., v[15]
+        __syncthreads();   // shared memory free for the next transform
+        // X[t + 256 r] = v[2 r], X[t + 128 + 256 r] = v[2 r + 1]  ->  v[q] = X[t + 128 q]
+    }
+}
+
+constexpr int kSmemBytes = (kN + kPad + kTwS) * 8 + 8;   // dynamic shared memory
+
+struct FParams {
+    const float2 *s;     // [n_sig][2048]
+    float2 *y;           // [n_sig][2048] (may alias s exactly: a signal is read, into
+                         // the prefetch stage, before the CTA writes it)
+    const float2 *H;     // [2048] FFT of the filter sequence (plan-owned)
+    const float2 *tw;    // [2048] twiddle table (plan-owned)
+    int64_t n_sig;
+    int mode;            // 0: filter; 1: forward FFT only (builds H from h)
+};
+
+__global__ void __launch_bounds__(kThreads, 4) filter_kernel(const FParams p) {
+    // sm: exchange buffer; stage: the next signal, prefetched with one TMA bulk copy
+    // (16 KB) while the current one is transformed.  Twiddles and H are read
+    // through L1 (__ldg): every CTA on the SM shares the same 32 KB.
+    extern __shared__ __align__(128) unsigned char fsm[];
+    float2 *stage = reinterpret_cast<float2 *>(fsm);                 // kN
+    float2 *sm = stage + kN;                                           // kPad
+    float2 *tws = sm + kPad;                                           // kTwS
+    uint64_t *barp = reinterpret_cast<uint64_t *>(tws + kTwS);
+    uint64_t &bar = *barp;
+    const int t = threadIdx.x;
+    for (int i = t; i < kTwS; i += kThreads) {
+        const int m = i < kTw3 ? 8 * (i / 16 + 1) * (i % 16) : ((i - kTw3) / 256 + 1) * ((i - kTw3) % 256);
+        tws[i] = p.tw[m & (kN - 1)];
+    }
+    if (t == 0) {
+        bfk::mbar_init(&bar, 1);
+        bfk::mbar_fence_init();
+    }
+    __syncthreads();
+    const uint64_t pol = bfk::policy_evict_first();
+    int64_t sig = blockIdx.x;
+    if (t == 0 && sig < p.n_sig) {
+        bfk::mbar_arrive_expect_tx(&bar, kN * 8);
+        bfk::bulk_g2s(stage, p.s + sig * kN, kN * 8, &bar, pol);
+    }
+    constexpr float inv_n = 1.0f / kN;
+    uint32_t phase = 0;
+    for (; sig < p.n_sig; sig += gridDim.x) {
+        float2 *dst = p.y + sig * kN;
+        float2 v[16];
+        bfk::mbar_wait(&bar, phase);
+        phase ^= 1u;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = stage[t + 128 * q];
+        __syncthreads();                                  // stage consumed by every thread
+        const int64_t nxt = sig + gridDim.x;
+        if (t == 0 && nxt < p.n_sig) {
+            bfk::mbar_arrive_expect_tx(&bar, kN * 8);
+            bfk::bulk_g2s(stage, p.s + nxt * kN, kN * 8, &bar, pol);
+        }
+        // forward FFT, MULT by H, inverse FFT as conj(FFT(conj(.))) / N — one copy of
+        // the transform code in a two-trip loop keeps register pressure at one FFT's
+        const int trips = p.mode == 0 ? 2 : 1;
+#pragma unroll 1
+        for (int trip = 0; trip < trips; ++trip) {
+            fft2048(v, sm, tws, t);
+            if (trip == 0 && trips == 2) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[q] = conj2(cmul(v[q], __ldg(p.H + t + 128 * q)));
+            }
+        }
+        if (p.mode == 0) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = make_float2(v[q].x * inv_n, -v[q].y * inv_n);
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) __stcs(dst + t + 128 * q, v[q]);
+    }
+}
+
+// tw[m] = e^{-2 pi i m / N}, evaluated in fp64 and rounded once.
+__global__ void twiddle_kernel(float2 *tw) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= kTwN) return;
+    double s, c;
+    sincospi(-2.0 * (double)m / kN, &s, &c);
+    tw[m] = make_float2((float)c, (float)s);
+}
+
+}  // namespace bff

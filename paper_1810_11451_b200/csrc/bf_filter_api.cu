@@ -1,0 +1,195 @@
+// bf_filter_api.cu — host side of the filter stage (include/bf_filter.h):
+// plan, twiddle table, H = DFT(h), launches of the fused filter kernel.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <new>
+#include <utility>
+#include <vector>
+
+#include "bf_filter.cuh"
+#include "bf_filter.h"
+#include "bf_host.h"
+
+using bfh::cuda_fail;
+using bfh::DeviceGuard;
+using bfh::fail;
+
+struct bff_plan_s {
+    int n = bff::kN, device = 0, num_sms = 0, ctas_per_sm = 0;
+    float2 *tw = nullptr, *H = nullptr;
+    bool have_taps = false;
+    bool profiling = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+    size_t prof_used = 0;
+    int64_t launches = 0;
+};
+
+namespace {
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bf_status launch(bff_plan_t p, const float2 *s, float2 *y, int64_t n, int mode, cudaStream_t st) {
+    bff::FParams fp{s, y, p->H, p->tw, n, mode};
+    const int64_t cap = (int64_t)p->num_sms * std::max(1, p->ctas_per_sm);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(n, cap));
+    cudaEvent_t e1 = nullptr;
+    if (p->profiling && mode == 0) {
+        if (p->prof_used == p->prof_events.size()) {
+            cudaEvent_t a, b;
+            BF_CUDA(cudaEventCreate(&a));
+            BF_CUDA(cudaEventCreate(&b));
+            p->prof_events.emplace_back(a, b);
+        }
+        BF_CUDA(cudaEventRecord(p->prof_events[p->prof_used].first, st));
+        e1 = p->prof_events[p->prof_used].second;
+        ++p->prof_used;
+    }
+    bff::filter_kernel<<<grid, bff::kThreads, bff::kSmemBytes, st>>>(fp);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "filter_kernel launch");
+    ++p->launches;
+    if (e1) BF_CUDA(cudaEventRecord(e1, st));
+    return BF_OK;
+}
+
+bf_status check_io(bff_plan_t p, const void *s, const void *y, int64_t n) {
+    if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
+    if (n < 0) return fail(BF_ERR_INVALID_VALUE, "n_signals must be >= 0");
+    if (n == 0) return BF_OK;
+    if (!s || !y) return fail(BF_ERR_INVALID_VALUE, "NULL signal buffer");
+    if (!aligned16(s) || !aligned16(y)) return fail(BF_ERR_MISALIGNED, "buffers must be 16-byte aligned");
+    const uintptr_t s0 = reinterpret_cast<uintptr_t>(s), y0 = reinterpret_cast<uintptr_t>(y);
+    const uintptr_t len = (uintptr_t)n * bff::kN * 8;
+    if (s0 != y0 && s0 < y0 + len && y0 < s0 + len)
+        return fail(BF_ERR_INVALID_VALUE, "y partially overlaps s (only exact aliasing is allowed)");
+    return BF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+bf_status bff_plan_create(int n, bff_plan_t *out) {
+    if (!out) return fail(BF_ERR_INVALID_VALUE, "out is NULL");
+    if (n < 1) return fail(BF_ERR_INVALID_VALUE, "n must be >= 1");
+    if (n != bff::kN) return fail(BF_ERR_UNSUPPORTED, "filter length %d unsupported (2048 only)", n);
+    int count = 0, dev = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(BF_ERR_NO_DEVICE, "no CUDA device: %s", cudaGetErrorString(e));
+    }
+    BF_CUDA(cudaGetDevice(&dev));
+    bff_plan_t p = new (std::nothrow) bff_plan_s();
+    if (!p) return fail(BF_ERR_OUT_OF_MEMORY, "host allocation of the plan failed");
+    p->device = dev;
+    cudaDeviceProp prop;
+    e = cudaGetDeviceProperties(&prop, dev);
+    if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaGetDeviceProperties"); }
+    if (prop.major != 10) {
+        delete p;
+        return fail(BF_ERR_UNSUPPORTED, "libbf.so is built for sm_100a; device is sm_%d%d", prop.major,
+                    prop.minor);
+    }
+    p->num_sms = prop.multiProcessorCount;
+    e = cudaFuncSetAttribute(bff::filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             bff::kSmemBytes);
+    if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaFuncSetAttribute (filter)"); }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->ctas_per_sm, bff::filter_kernel,
+                                                      bff::kThreads, bff::kSmemBytes);
+    if (e != cudaSuccess) { delete p; return cuda_fail(e, "occupancy query"); }
+    if (cudaMalloc(&p->tw, bff::kTwN * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc(&p->H, bff::kN * sizeof(float2)) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(p->tw);
+        cudaFree(p->H);
+        delete p;
+        return fail(BF_ERR_OUT_OF_MEMORY, "cudaMalloc of the filter plan tables failed");
+    }
+    bff::twiddle_kernel<<<(bff::kTwN + 255) / 256, 256>>>(p->tw);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        cudaFree(p->tw);
+        cudaFree(p->H);
+        delete p;
+        return cuda_fail(e, "twiddle table");
+    }
+    ++p->launches;
+    *out = p;
+    return BF_OK;
+}
+
+bf_status bff_set_taps(bff_plan_t p, const void *h_dev, void *stream) {
+    if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
+    if (!h_dev) return fail(BF_ERR_INVALID_VALUE, "h_dev is NULL");
+    if (!aligned16(h_dev)) return fail(BF_ERR_MISALIGNED, "h_dev must be 16-byte aligned");
+    DeviceGuard g(p->device);
+    bf_status s = launch(p, static_cast<const float2 *>(h_dev), p->H, 1, 1,
+                         static_cast<cudaStream_t>(stream));
+    if (s == BF_OK) p->have_taps = true;
+    return s;
+}
+
+bf_status bff_apply(bff_plan_t p, const void *s_dev, void *y_dev, int64_t n_signals, void *stream) {
+    bf_status s = check_io(p, s_dev, y_dev, n_signals);
+    if (s != BF_OK || n_signals == 0) return s;
+    if (!p->have_taps) return fail(BF_ERR_NO_PRECODERS, "bff_set_taps was not called");
+    DeviceGuard g(p->device);
+    return launch(p, static_cast<const float2 *>(s_dev), static_cast<float2 *>(y_dev), n_signals, 0,
+                  static_cast<cudaStream_t>(stream));
+}
+
+bf_status bff_fft(bff_plan_t p, const void *x_dev, void *X_dev, int64_t n_signals, void *stream) {
+    bf_status s = check_io(p, x_dev, X_dev, n_signals);
+    if (s != BF_OK || n_signals == 0) return s;
+    DeviceGuard g(p->device);
+    return launch(p, static_cast<const float2 *>(x_dev), static_cast<float2 *>(X_dev), n_signals, 1,
+                  static_cast<cudaStream_t>(stream));
+}
+
+bf_status bff_destroy(bff_plan_t p) {
+    if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
+    {
+        DeviceGuard g(p->device);
+        cudaFree(p->tw);
+        cudaFree(p->H);
+        for (auto &ev : p->prof_events) {
+            cudaEventDestroy(ev.first);
+            cudaEventDestroy(ev.second);
+        }
+    }
+    delete p;
+    return BF_OK;
+}
+
+bf_status bff_plan_set_profiling(bff_plan_t p, int enable) {
+    if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
+    p->profiling = enable != 0;
+    return BF_OK;
+}
+
+bf_status bff_plan_kernel_time(bff_plan_t p, double *total_ms, int64_t *n_launches) {
+    if (!p || !total_ms || !n_launches) return fail(BF_ERR_INVALID_VALUE, "NULL argument");
+    DeviceGuard g(p->device);
+    double sum = 0.0;
+    for (size_t i = 0; i < p->prof_used; ++i) {
+        BF_CUDA(cudaEventSynchronize(p->prof_events[i].second));
+        float ms = 0.f;
+        BF_CUDA(cudaEventElapsedTime(&ms, p->prof_events[i].first, p->prof_events[i].second));
+        sum += ms;
+    }
+    *total_ms = sum;
+    *n_launches = (int64_t)p->prof_used;
+    p->prof_used = 0;
+    return BF_OK;
+}
+
+bf_status bff_plan_launch_count(bff_plan_t p, int64_t *count) {
+    if (!p || !count) return fail(BF_ERR_INVALID_VALUE, "NULL argument");
+    *count = p->launches;
+    return BF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,48 @@
+// bf_host.h — host-side helpers shared by the C-ABI translation units of libbf.so:
+// thread-local error detail (bf_last_error), status helpers, device guard.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "bf.h"
+
+namespace bfh {
+
+extern thread_local std::string g_last_error;
+
+inline bf_status fail(bf_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return s;
+}
+
+inline bf_status cuda_fail(cudaError_t e, const char *what) {
+    return fail(BF_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+// Makes `dev` current for the scope of a call and restores the caller's device.
+struct DeviceGuard {
+    int prev = -1;
+    bool changed = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) changed = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (changed) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace bfh
+
+#define BF_CUDA(call)                                                \
+    do {                                                             \
+        cudaError_t e_ = (call);                                     \
+        if (e_ != cudaSuccess) return bfh::cuda_fail(e_, #call);     \
+    } while (0)

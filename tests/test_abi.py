@@ -20,9 +20,12 @@ def bf():
 
 
 def _declared_functions():
-    src = open(os.path.join(ROOT, "include", "bf.h")).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(bf_[a-z_]+)\s*\(", src)))
+    names = set()
+    for hdr in ("bf.h", "bf_filter.h"):
+        src = open(os.path.join(ROOT, "include", hdr)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names |= set(re.findall(r"\b(bff?_[a-z_]+)\s*\(", src))
+    return sorted(names)
 
 
 def test_header_declares_the_boundary_calls():
@@ -87,3 +90,10 @@ def test_null_plan_calls_are_rejected(bf):
     assert L.bf_apply(None, None, None, None, 0, None) == bf.Status.INVALID_VALUE
     assert L.bf_set_precoders(None, None, 1, None) == bf.Status.INVALID_VALUE
     assert L.bf_destroy(None) == bf.Status.INVALID_VALUE
+
+
+def test_filter_plan_validates_before_touching_gpu(bf):
+    assert bf.filter_plan_create_status(1024) == bf.Status.UNSUPPORTED
+    assert bf.filter_plan_create_status(0) == bf.Status.INVALID_VALUE
+    if not gpu_available():
+        assert bf.filter_plan_create_status(2048) == bf.Status.NO_DEVICE
