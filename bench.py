@@ -37,7 +37,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c4", help="c2 | c3 | c4 (default) | c5")
     ap.add_argument("--f", type=int, default=36, help="flow count for --config c3")
-    ap.add_argument("--layout", default="interleaved", choices=["interleaved", "planar"])
+    ap.add_argument("--layout", default="interleaved",
+                    choices=["interleaved", "planar", "interleaved_f16out"])
     ap.add_argument("--variant", default="auto", choices=["auto", "ffma", "tensor"],
                     help="kernel variant (auto = libbf's measured per-f table)")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -203,7 +204,7 @@ def run_ours(args):
 
     plan = bf.Plan(f=wl.f, layout=args.layout, variant=args.variant)
     plan.set_precoders(W)
-    R = torch.empty(plan.r_shape(n_local), dtype=plan.dtype, device=dev)
+    R = torch.empty(plan.r_shape(n_local), dtype=plan.r_dtype, device=dev)
     stream = torch.cuda.current_stream()
 
     # ---- warm-up, then K timed steps ---------------------------------------------
@@ -243,11 +244,13 @@ def run_ours(args):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_max = benchkit.fp32_peak_tflops(sms, peaks.get("sm_max_mhz", 1965.0))
     flops_launch = wl.block_flops * n_local
-    bytes_launch = wl.block_bytes * n_local
+    r_blk = 15360 if args.layout == "interleaved_f16out" else 30720
+    blk_bytes = 480 * wl.f + r_blk
+    bytes_launch = blk_bytes * n_local
     achieved_tf = flops_launch / (kern_avg_ms * 1e-3) / 1e12
     achieved_gbs = bytes_launch / (kern_avg_ms * 1e-3) / 1e9
     hbm = peaks["hbm_gbs"]
-    ai = wl.block_flops / wl.block_bytes
+    ai = wl.block_flops / blk_bytes
     variant = plan.variant.name.lower()
     # FFMA kernel: bound by the FP32 pipe when AI x HBM exceeds the FFMA peak.
     # Tensor kernel: 4 split-TF32 MMAs per K step at ~1.1 PFLOP/s nominal leave
@@ -297,11 +300,11 @@ def run_ours(args):
         del R
         torch.cuda.empty_cache()
         s_blk = 480 * wl.f
-        need = n_local * (s_blk + 30720 + 4)
+        need = n_local * (s_blk + r_blk + 4)
         budget = int(host_ram_available() * 0.6) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", world)))
         n_e2e = n_local if args.e2e_blocks <= 0 else min(args.e2e_blocks, n_local)
-        if n_e2e * (s_blk + 30720 + 4) > budget:
-            n_e2e = max(1, budget // (s_blk + 30720 + 4))
+        if n_e2e * (s_blk + r_blk + 4) > budget:
+            n_e2e = max(1, budget // (s_blk + r_blk + 4))
         Sh = torch.empty(plan.s_shape(n_e2e), dtype=plan.dtype).pin_memory()
         Sh.copy_(S[:n_e2e])
         th = None
@@ -310,7 +313,7 @@ def run_ours(args):
             th.copy_(tags[:n_e2e])
         del S
         torch.cuda.empty_cache()
-        Rh = torch.empty(plan.r_shape(n_e2e), dtype=plan.dtype).pin_memory()
+        Rh = torch.empty(plan.r_shape(n_e2e), dtype=plan.r_dtype).pin_memory()
         plan.apply_host(Sh, th, Rh)
         torch.cuda.synchronize()
         if world > 1:
@@ -324,7 +327,7 @@ def run_ours(args):
         n_e2e_total = int(shard.sum_over_ranks(n_e2e, dev))
         e2e = {"value": n_e2e_total * wl.b * args.e2e_steps / (e2e_ms * 1e-3), "unit": "REs/s",
                "h2d_bytes_per_step": int(n_e2e_total * (s_blk + (4 if tags is not None else 0))),
-               "d2h_bytes_per_step": int(n_e2e_total * 30720),
+               "d2h_bytes_per_step": int(n_e2e_total * r_blk),
                "steps": args.e2e_steps, "blocks_per_step": n_e2e_total,
                "ms_per_step": e2e_ms / args.e2e_steps,
                "path": "bf_apply_host: pinned host S/tags -> H2D -> route+kernel -> D2H pinned R, "

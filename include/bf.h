@@ -28,6 +28,7 @@
  *                          S [n_blocks][2][f][b]
  *                          R [n_blocks][2][n_ant][b]
  *   Both layouts move the same bytes per block: S 8*f*b, R 8*n_ant*b.
+ *   BF_LAYOUT_INTERLEAVED_F16OUT: as interleaved, R in fp16 pairs (4*n_ant*b).
  *
  * Supported domain: n_ant == 64, b == 60, 0 <= f <= 36, 1 <= n_groups <= 1024,
  * 0 <= n_blocks < 2^31.  Other shapes return BF_ERR_UNSUPPORTED (there is no
@@ -72,7 +73,13 @@ typedef struct bf_plan_s *bf_plan_t;
 
 typedef enum {
     BF_LAYOUT_INTERLEAVED = 0,
-    BF_LAYOUT_PLANAR = 1
+    BF_LAYOUT_PLANAR = 1,
+    /* W and S interleaved complex fp32 as BF_LAYOUT_INTERLEAVED, R written as
+     * interleaved IEEE binary16 (re, im) pairs [n_blocks][n_ant][b], each rounded
+     * once (round-to-nearest-even) from the fp32 result: 15,360 bytes per block
+     * instead of 30,720 (reduced-precision fronthaul
+     * output).  Accuracy: |R16 - R_exact| <= sqrt(2) 2^-11 |R_exact| + 1e-5 T. */
+    BF_LAYOUT_INTERLEAVED_F16OUT = 2
 } bf_layout;
 
 /* Kernel variant.  Both compute the same product within the same contract.

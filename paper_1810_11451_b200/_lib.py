@@ -35,6 +35,7 @@ class Status(enum.IntEnum):
 class Layout(enum.IntEnum):
     INTERLEAVED = 0
     PLANAR = 1
+    INTERLEAVED_F16OUT = 2    # R as fp16 (re, im) pairs
 
 
 class Variant(enum.IntEnum):

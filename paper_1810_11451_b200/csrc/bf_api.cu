@@ -75,7 +75,7 @@ __global__ void bf_relayout_w(const float *__restrict__ W, int n_groups, int F, 
         const int k = rem / 32, j = (rem % 32) / 8, ag = rem % 8;
         const int i0 = ag * 8 + 2 * j, i1 = i0 + 1;
         float4 v;
-        if (layout == BF_LAYOUT_INTERLEAVED) {
+        if (layout != BF_LAYOUT_PLANAR) {
             const float *Wg = W + g * 64 * F * 2;
             v = make_float4(Wg[(i0 * F + k) * 2], Wg[(i1 * F + k) * 2],
                             Wg[(i0 * F + k) * 2 + 1], Wg[(i1 * F + k) * 2 + 1]);
@@ -108,7 +108,7 @@ __global__ void bf_tc_build_wimg(const float *__restrict__ W, int n_groups, int 
         float val = 0.0f;
         if (k < F) {
             float wr, wi;
-            if (layout == 0) {
+            if (layout != BF_LAYOUT_PLANAR) {
                 wr = W[((g * 64 + i) * F + k) * 2];
                 wi = W[((g * 64 + i) * F + k) * 2 + 1];
             } else {
@@ -365,7 +365,7 @@ int grid_for(bf_plan_t p, int64_t n_items) {
 bf_status apply_device(bf_plan_t p, const void *S, const int32_t *gidx, void *R, int64_t n,
                        cudaStream_t st) {
     if (n == 0) return BF_OK;
-    const size_t r_bytes = (size_t)n * bfk::kRBlockFloats * sizeof(float);
+    const size_t r_bytes = (size_t)n * bfk::r_block_bytes(p->layout);
     if (p->f == 0) {   // a8: the empty sum, +0.0f everywhere
         BF_CUDA(cudaMemsetAsync(R, 0, r_bytes, st));
         return BF_OK;
@@ -431,7 +431,8 @@ bf_status ensure_host_pipeline(bf_plan_t p, bool tagged) {
         if (p->f > 0 &&
             (s = grow(&p->hS[i], &p->hS_cap[i], C * 120 * p->f, "host-pipeline S slot")) != BF_OK)
             return s;
-        if ((s = grow(&p->hR[i], &p->hR_cap[i], C * bfk::kRBlockFloats, "host-pipeline R slot")) !=
+        if ((s = grow(&p->hR[i], &p->hR_cap[i], C * (bfk::r_block_bytes(p->layout) / 4),
+                      "host-pipeline R slot")) !=
             BF_OK)
             return s;
         if (tagged && (s = grow(&p->hG[i], &p->hG_cap[i], C, "host-pipeline tag slot")) != BF_OK)
@@ -455,7 +456,8 @@ bf_status validate_layout_and_dims(int n_ant, int f, int b, int layout) {
     if (n_ant < 1 || f < 0 || b < 1)
         return fail(BF_ERR_INVALID_VALUE, "dimensions must satisfy n_ant >= 1, f >= 0, b >= 1 "
                                           "(got n_ant=%d f=%d b=%d)", n_ant, f, b);
-    if (layout != BF_LAYOUT_INTERLEAVED && layout != BF_LAYOUT_PLANAR)
+    if (layout != BF_LAYOUT_INTERLEAVED && layout != BF_LAYOUT_PLANAR &&
+        layout != BF_LAYOUT_INTERLEAVED_F16OUT)
         return fail(BF_ERR_INVALID_VALUE, "unknown layout %d", layout);
     if (n_ant != bfk::kAnt || b != bfk::kB || f > bfk::kMaxF)
         return fail(BF_ERR_UNSUPPORTED, "compiled domain is n_ant=64, b=60, 0<=f<=36 "
@@ -582,7 +584,8 @@ static bf_status validate_apply(bf_plan_t p, const void *S, const int32_t *gidx,
     }
     if (p->f > 0) {
         const uintptr_t s0 = reinterpret_cast<uintptr_t>(S), s1 = s0 + (uintptr_t)n * 480 * p->f;
-        const uintptr_t r0 = reinterpret_cast<uintptr_t>(R), r1 = r0 + (uintptr_t)n * 30720;
+        const uintptr_t r0 = reinterpret_cast<uintptr_t>(R),
+                        r1 = r0 + (uintptr_t)n * bfk::r_block_bytes(p->layout);
         if (s0 < r1 && r0 < s1) return fail(BF_ERR_INVALID_VALUE, "R overlaps S");
     }
     return BF_OK;
@@ -625,7 +628,7 @@ bf_status bf_apply_host(bf_plan_t p, const void *S_host, const int32_t *group_id
     const bool tagged = group_idx_host != nullptr && p->n_groups > 1;
     if ((s = ensure_host_pipeline(p, tagged)) != BF_OK) return s;
     const int64_t C = p->host_chunk;
-    const size_t s_blk = (size_t)480 * p->f, r_blk = (size_t)bfk::kRBlockFloats * sizeof(float);
+    const size_t s_blk = (size_t)480 * p->f, r_blk = (size_t)bfk::r_block_bytes(p->layout);
     BF_CUDA(cudaEventRecord(p->ev_start, st));
     BF_CUDA(cudaStreamWaitEvent(p->s_h2d, p->ev_start, 0));
     BF_CUDA(cudaStreamWaitEvent(p->s_d2h, p->ev_start, 0));

@@ -8,7 +8,7 @@ struct BfKernelEntry {
     int smem_bytes;      // dynamic shared memory of that instantiation
 };
 
-using BfKernelTable = BfKernelEntry[37][2];
+using BfKernelTable = BfKernelEntry[37][3];   // [f][layout: interleaved, planar, f16 out]
 
 void bf_register_f01_06(BfKernelTable &t, BfKernelTable &tc);
 void bf_register_f07_12(BfKernelTable &t, BfKernelTable &tc);

@@ -29,6 +29,7 @@
 //    a warp's two stores of a row cover whole 32-byte sectors.
 #pragma once
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace bfk {
@@ -42,6 +43,16 @@ constexpr int kTR = 5;            // REs per thread
 constexpr int kRG = 12;           // RE groups
 constexpr int kAG = 8;            // antenna groups
 constexpr int kRBlockFloats = 2 * kAnt * kB;   // 7680 floats = 30,720 B per block
+
+// I/O formats (the kernels' LAYOUT parameter; include/bf.h bf_layout):
+//   0 interleaved complex fp32 S/W/R;  1 planar complex fp32 S/W/R;
+//   2 interleaved fp32 S/W, R as interleaved fp16 (re, im) pairs (SURVEY.md §8(f)
+//     row 4: halves the dominant R stream; R rounded once, RN, from fp32).
+__host__ __device__ constexpr int r_block_bytes(int layout) { return layout == 2 ? 15360 : 30720; }
+__device__ __forceinline__ uint32_t pack_half2(float re, float im) {
+    const __half2 h = __floats2half2_rn(re, im);
+    return *reinterpret_cast<const uint32_t *>(&h);
+}
 
 struct KParams {
     const float4 *Wp;         // [n_groups][F][32] float4 (plan-owned relayout)
@@ -188,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 4) bf_ffma_kernel(const KParams p) {
                 float sr[kTR], si[kTR];
 #pragma unroll
                 for (int r = 0; r < kTR; ++r) {
-                    if (LAYOUT == 0) {
+                    if (LAYOUT != 1) {
                         const float2 v =
                             reinterpret_cast<const float2 *>(S)[k * kB + rg + kRG * r];
                         sr[r] = v.x;
@@ -228,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 4) bf_ffma_kernel(const KParams p) {
         if (t == 0 && item + 2 < end) issue(stage, item + 2);
 
         if (valid) {
-            float *Rb = p.R + blk * kRBlockFloats;
+            float *Rb = p.R + blk * (r_block_bytes(LAYOUT) / 4);
 #pragma unroll
             for (int a = 0; a < kTA; ++a) {
                 const int i = ag * kTA + a;
@@ -241,6 +252,9 @@ __global__ void __launch_bounds__(kThreads, 4) bf_ffma_kernel(const KParams p) {
                         // which forces register-bank conflicts in half of the FFMAs.
                         __stcs(Rb + 2 * (i * kB + j), are[a][r]);
                         __stcs(Rb + 2 * (i * kB + j) + 1, aim[a][r]);
+                    } else if (LAYOUT == 2) {
+                        __stcs(reinterpret_cast<unsigned int *>(Rb) + i * kB + j,
+                               pack_half2(are[a][r], aim[a][r]));
                     } else {
                         __stcs(Rb + i * kB + j, are[a][r]);
                         __stcs(Rb + kAnt * kB + i * kB + j, aim[a][r]);

@@ -10,6 +10,8 @@ static void reg(BfKernelTable &t, BfKernelTable &tc) {
     t[F][1] = {reinterpret_cast<const void *>(&bfk::bf_ffma_kernel<F, 1>), bfk::Smem<F>::kBytes};
     tc[F][0] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 0>), bftc::TcSmem<F>::kBytes};
     tc[F][1] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 1>), bftc::TcSmem<F>::kBytes};
+    t[F][2] = {reinterpret_cast<const void *>(&bfk::bf_ffma_kernel<F, 2>), bfk::Smem<F>::kBytes};
+    tc[F][2] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 2>), bftc::TcSmem<F>::kBytes};
 }
 
 void bf_register_f07_12(BfKernelTable &t, BfKernelTable &tc) {

@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
                         const int k = c0 / 2 + q;
                         float re = 0.0f, im = 0.0f;
                         if (k < F && valid) {
-                            if (LAYOUT == 0) {
+                            if (LAYOUT != 1) {
                                 const float2 v = reinterpret_cast<const float2 *>(Sb)[k * 60 + j];
                                 re = v.x;
                                 im = v.y;
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
             const uint32_t u = (uint32_t)(t >> 1);
             const bool valid = m < 120 && bsel < tl.cnt;
             const int64_t blk = valid ? block_of(p, tl.item + bsel) : 0;
-            float *Rb = p.R + blk * (int64_t)bfk::kRBlockFloats;
+            float *Rb = p.R + blk * (int64_t)(bfk::r_block_bytes(LAYOUT) / 4);
             bfk::mbar_wait(bar_d_full + b, u & 1);
             tc::fence_after_sync();
             const uint32_t d = tmem + ((uint32_t)(q * 32) << 16) + kDCol0 + 128 * b + 64 * h;
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
             // raises the write bandwidth of 4 storing warps (tools/write_bw).
             const bool odd = (j & 1) != 0;
             if constexpr (!(DBG & 2)) {
-                if (LAYOUT == 0) {
+                if (LAYOUT == 0 || LAYOUT == 2) {
 #pragma unroll
                     for (int aa = 0; aa < 32; aa += 2) {
                         const int a = 32 * h + aa;
@@ -395,9 +395,16 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
                         const float gi = __shfl_xor_sync(0xffffffffu, odd ? im0 : im1, 1);
                         // even lane: antenna a, REs j, j+1; odd lane: antenna a+1, REs j-1, j
                         const float4 w4 = odd ? make_float4(gr, gi, re1, im1) : make_float4(re0, im0, gr, gi);
-                        if (valid)
-                            __stcs(reinterpret_cast<float4 *>(Rb + 2 * ((a + (odd ? 1 : 0)) * 60 + j - (odd ? 1 : 0))),
-                                   w4);
+                        const int e = (a + (odd ? 1 : 0)) * 60 + j - (odd ? 1 : 0);   // element index
+                        if (valid) {
+                            if (LAYOUT == 0) {
+                                __stcs(reinterpret_cast<float4 *>(Rb + 2 * e), w4);
+                            } else {      // fp16 output: two (re, im) half pairs, 8 bytes
+                                __stcs(reinterpret_cast<uint2 *>(Rb) + e / 2,
+                                       make_uint2(bfk::pack_half2(w4.x, w4.y),
+                                                  bfk::pack_half2(w4.z, w4.w)));
+                            }
+                        }
                     }
                 } else {
 #pragma unroll

@@ -52,23 +52,32 @@ class Plan:
 
     # -- shapes ---------------------------------------------------------------
     def s_shape(self, n: int):
-        return (n, self.f, self.b) if self.layout == Layout.INTERLEAVED else (n, 2, self.f, self.b)
+        return (n, 2, self.f, self.b) if self.layout == Layout.PLANAR else (n, self.f, self.b)
 
     def r_shape(self, n: int):
-        return ((n, self.n_ant, self.b) if self.layout == Layout.INTERLEAVED
-                else (n, 2, self.n_ant, self.b))
+        if self.layout == Layout.PLANAR:
+            return (n, 2, self.n_ant, self.b)
+        if self.layout == Layout.INTERLEAVED_F16OUT:
+            return (n, self.n_ant, self.b, 2)
+        return (n, self.n_ant, self.b)
 
     def w_shape(self, g: int):
-        return ((g, self.n_ant, self.f) if self.layout == Layout.INTERLEAVED
-                else (g, 2, self.n_ant, self.f))
+        return (g, 2, self.n_ant, self.f) if self.layout == Layout.PLANAR else (g, self.n_ant, self.f)
 
     @property
     def dtype(self):
-        return torch.complex64 if self.layout == Layout.INTERLEAVED else torch.float32
+        """dtype of W and S."""
+        return torch.float32 if self.layout == Layout.PLANAR else torch.complex64
 
-    def _check(self, t: torch.Tensor, name: str, shape, device=True):
-        if t.dtype != self.dtype:
-            raise TypeError(f"{name} must be {self.dtype}, got {t.dtype}")
+    @property
+    def r_dtype(self):
+        """dtype of R (fp16 (re, im) pairs for INTERLEAVED_F16OUT)."""
+        return torch.float16 if self.layout == Layout.INTERLEAVED_F16OUT else self.dtype
+
+    def _check(self, t: torch.Tensor, name: str, shape, device=True, dtype=None):
+        dtype = self.dtype if dtype is None else dtype
+        if t.dtype != dtype:
+            raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
         if tuple(t.shape) != tuple(shape):
             raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
         if not t.is_contiguous():
@@ -81,7 +90,7 @@ class Plan:
     # -- the calls of include/bf.h ------------------------------------------------
     def set_precoders(self, W: torch.Tensor, stream=None) -> "Plan":
         """bf_set_precoders: W [G][64][f] complex64 (interleaved) or [G][2][64][f] float32."""
-        if W.dim() == (2 if self.layout == Layout.INTERLEAVED else 3):
+        if W.dim() == (3 if self.layout == Layout.PLANAR else 2):
             W = W.unsqueeze(0)
         G = W.shape[0]
         self._check(W, "W", self.w_shape(G))
@@ -96,8 +105,8 @@ class Plan:
         n = S.shape[0]
         self._check(S, "S", self.s_shape(n))
         if out is None:
-            out = torch.empty(self.r_shape(n), dtype=self.dtype, device=self.device)
-        self._check(out, "out", self.r_shape(n))
+            out = torch.empty(self.r_shape(n), dtype=self.r_dtype, device=self.device)
+        self._check(out, "out", self.r_shape(n), dtype=self.r_dtype)
         if group_idx is not None:
             if group_idx.dtype != torch.int32 or tuple(group_idx.shape) != (n,) \
                     or group_idx.device != self.device or not group_idx.is_contiguous():
@@ -111,7 +120,7 @@ class Plan:
         """bf_apply_host on host tensors (pinned for full speed)."""
         n = S.shape[0]
         self._check(S, "S", self.s_shape(n), device=False)
-        self._check(out, "out", self.r_shape(n), device=False)
+        self._check(out, "out", self.r_shape(n), device=False, dtype=self.r_dtype)
         if group_idx is not None and (group_idx.dtype != torch.int32 or
                                       tuple(group_idx.shape) != (n,) or group_idx.is_cuda):
             raise ValueError("group_idx must be a host int32 [n] tensor")

@@ -410,3 +410,43 @@ def test_variants_agree_within_contract():
     p.set_variant("tensor")
     assert p.variant == Variant.TENSOR
     p.close()
+
+
+# ---------------------------------------------------------------------------
+# fp16 output (BF_LAYOUT_INTERLEAVED_F16OUT)
+# ---------------------------------------------------------------------------
+def run_f16(W, S, tags, variant):
+    plan = Plan(f=W.shape[-1], layout=Layout.INTERLEAVED_F16OUT, variant=variant)
+    plan.set_precoders(torch.from_numpy(np.ascontiguousarray(W)).to(DEV))
+    R = plan.apply(torch.from_numpy(np.ascontiguousarray(S)).to(DEV),
+                   None if tags is None else torch.from_numpy(tags).to(DEV))
+    torch.cuda.synchronize()
+    plan.close()
+    h = R.cpu().numpy().astype(np.float64)
+    return h[..., 0] + 1j * h[..., 1]
+
+
+def test_f16_output_within_contract(variant):
+    """|R16 - R_exact| <= sqrt(2) 2^-11 |R_exact| + 1e-5 T (+ fp16 subnormal spacing)."""
+    wl = syn.workload("c4")
+    W, S, tags = syn.workload_inputs(wl, np.arange(701))
+    R_ref, T, _ = oracle.beamform(W, S, tags, n_threads=NT)
+    R16 = run_f16(W, S, tags, variant)
+    lim = np.sqrt(2) * 2.0 ** -11 * np.abs(R_ref.astype(np.complex128)) + TOL * T + 2.0 ** -24
+    err = np.abs(R16 - R_ref.astype(np.complex128))
+    assert (err <= lim).all(), (err / lim).max()
+    # and it is the fp32 result rounded once: compare with the fp32 path rounded on the host
+    R32 = run_plan(W, S, tags, variant=variant)
+    expect = R32.real.astype(np.float16).astype(np.float64) + 1j * R32.imag.astype(np.float16).astype(np.float64)
+    assert np.array_equal(R16, expect)
+
+
+@pytest.mark.parametrize("f", [1, 17, 36])
+def test_f16_output_identity_is_rounded_copy(f, variant):
+    S = syn.qam_symbols(5, 0, np.arange(30), f, 60, 64)
+    W = np.zeros((1, 64, f), np.complex64)
+    W[0, np.arange(f), np.arange(f)] = 1
+    R16 = run_f16(W, S, None, variant)
+    exp = S.real.astype(np.float16).astype(np.float64) + 1j * S.imag.astype(np.float16).astype(np.float64)
+    assert np.array_equal(R16[:, :f], exp)
+    assert not np.any(R16[:, f:])
