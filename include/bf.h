@@ -145,6 +145,15 @@ bf_status bf_apply_host(bf_plan_t p, const void *S_host, const int32_t *group_id
 bf_status bf_route(bf_plan_t p, const int32_t *group_idx_dev, int64_t n_blocks,
                    int32_t *perm_dev, int32_t *offsets_dev, void *stream);
 
+/* Apply to blocks already routed by bf_route (same tags, same plan precoder
+ * count): perm_dev / offsets_dev as bf_route wrote them, or both NULL (every
+ * block uses group 0).  Lets a streaming caller route the next batch on another
+ * stream while this one is beamformed; the result equals bf_apply bitwise.
+ * perm / offsets that did not come from bf_route are a precondition violation. */
+bf_status bf_apply_routed(bf_plan_t p, const void *S_dev, const int32_t *perm_dev,
+                          const int32_t *offsets_dev, void *R_dev, int64_t n_blocks,
+                          void *stream);
+
 /* Free the plan and everything it owns.  Call after its work has drained. */
 bf_status bf_destroy(bf_plan_t p);
 

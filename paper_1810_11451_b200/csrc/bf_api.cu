@@ -207,8 +207,7 @@ __global__ void bf_route_scan(int32_t *__restrict__ table, int P, int G, int64_t
 // Pass 3: stable scatter.  Each warp owns a contiguous sub-tile; ranks come
 // from __match_any_sync so the output order is (bin, block id) exactly.
 __global__ void bf_route_scatter(const int32_t *__restrict__ gidx, int64_t n, int G, int tile,
-                                 const int32_t *__restrict__ table, int32_t *__restrict__ perm,
-                                 int32_t *__restrict__ gsorted) {
+                                 const int32_t *__restrict__ table, int32_t *__restrict__ perm) {
     extern __shared__ int32_t cnt[];   // [8][G + 1]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nb = G + 1;
@@ -244,8 +243,79 @@ __global__ void bf_route_scatter(const int32_t *__restrict__ gidx, int64_t n, in
         if (b >= 0) {
             const int32_t pos = mycnt[b] + __popc(m & lt);
             perm[pos] = (int32_t)i;
-            gsorted[pos] = b;
         }
+        __syncwarp();
+        if (b >= 0 && (m & lt) == 0) mycnt[b] += __popc(m);
+        __syncwarp();
+    }
+}
+
+// Small batches (n <= kRouteSmallN, G <= kRouteSmallG): the whole stable counting
+// sort in ONE CTA of 32 warps — per-warp histograms (match_any), a bin-major
+// prefix, then the stable scatter — one launch instead of three (streaming
+// chunks of a few thousand blocks are latency-bound, bench --config c5).
+constexpr int kRouteSmallN = 16384;
+constexpr int kRouteSmallG = 256;
+
+__global__ void __launch_bounds__(1024) bf_route_small(const int32_t *__restrict__ gidx, int n, int G,
+                                                       int32_t *__restrict__ perm,
+                                                       int32_t *__restrict__ offsets,
+                                                       int32_t *__restrict__ err) {
+    extern __shared__ int32_t cnt[];   // [32][G + 1], then tot[G + 1]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nb = G + 1;
+    int32_t *tot = cnt + 32 * nb;
+    for (int e = threadIdx.x; e < 33 * nb; e += blockDim.x) cnt[e] = 0;
+    __syncthreads();
+    const int per = ((n + 31) / 32 + 31) / 32 * 32;    // items per warp, multiple of 32
+    const int ws = warp * per, we = min(n, ws + per);
+    int32_t *mycnt = cnt + warp * nb;
+    const unsigned lt = (1u << lane) - 1u;
+    int bad = 0;
+    for (int base = ws; base < we; base += 32) {
+        const int i = base + lane;
+        const int b = i < we ? route_bin(__ldg(gidx + i), G) : -1;
+        bad |= (b == G);
+        const unsigned m = __match_any_sync(0xffffffffu, b);
+        if (b >= 0 && (m & lt) == 0) mycnt[b] += __popc(m);
+        __syncwarp();
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) *err = 1;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {     // prefix over warps, per bin
+        int32_t run = 0;
+        for (int w = 0; w < 32; ++w) {
+            const int32_t c = cnt[w * nb + b];
+            cnt[w * nb + b] = run;
+            run += c;
+        }
+        tot[b] = run;
+    }
+    __syncthreads();
+    if (warp == 0) {                                          // exclusive scan over bins
+        int32_t carry = 0;
+        for (int b0 = 0; b0 < nb; b0 += 32) {
+            const int b = b0 + lane;
+            const int32_t v = b < nb ? tot[b] : 0;
+            int32_t inc = v;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += u;
+            }
+            if (b < nb) tot[b] = carry + inc - v;
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) offsets[b] = tot[b];
+    if (threadIdx.x == 0) offsets[nb] = n;
+    for (int e = threadIdx.x; e < 32 * nb; e += blockDim.x) cnt[e] += tot[e % nb];
+    __syncthreads();
+    for (int base = ws; base < we; base += 32) {
+        const int i = base + lane;
+        const int b = i < we ? route_bin(__ldg(gidx + i), G) : -1;
+        const unsigned m = __match_any_sync(0xffffffffu, b);
+        if (b >= 0) perm[mycnt[b] + __popc(m & lt)] = i;
         __syncwarp();
         if (b >= 0 && (m & lt) == 0) mycnt[b] += __popc(m);
         __syncwarp();
@@ -286,9 +356,8 @@ struct bf_plan_s {
     int32_t *wexact = nullptr;  // per group: W exactly tf32
     int64_t wexact_cap = 0;
     // routing workspace
-    int32_t *perm = nullptr, *gsorted = nullptr, *table = nullptr, *offsets = nullptr,
-            *err = nullptr;
-    int64_t perm_cap = 0, gs_cap = 0, table_cap = 0, offsets_cap = 0, err_cap = 0;
+    int32_t *perm = nullptr, *table = nullptr, *offsets = nullptr, *err = nullptr;
+    int64_t perm_cap = 0, table_cap = 0, offsets_cap = 0, err_cap = 0;
     // host pipeline
     int64_t host_chunk = kDefaultHostChunk, slot_cap = 0;
     float *hS[kHostSlots] = {}, *hR[kHostSlots] = {};
@@ -313,16 +382,23 @@ bf_status launched(bf_plan_t p, const char *what) {
     return BF_OK;
 }
 
-// Stable counting sort of blocks by tag into p->perm / p->gsorted (+offsets).
-bf_status route(bf_plan_t p, const int32_t *gidx, int64_t n, int32_t *perm, int32_t *gsorted,
-                int32_t *offsets, cudaStream_t st) {
+// Stable counting sort of blocks by tag into perm (+offsets).
+bf_status route(bf_plan_t p, const int32_t *gidx, int64_t n, int32_t *perm, int32_t *offsets,
+                cudaStream_t st) {
     const int G = p->n_groups;
+    bf_status s;
+    if (n <= kRouteSmallN && G <= kRouteSmallG) {
+        if ((s = grow(&p->err, &p->err_cap, 1, "routing flag")) != BF_OK) return s;
+        BF_CUDA(cudaMemsetAsync(p->err, 0, sizeof(int32_t), st));
+        const size_t smem = 33 * (G + 1) * sizeof(int32_t);
+        bf_route_small<<<1, 1024, smem, st>>>(gidx, (int)n, G, perm, offsets, p->err);
+        return launched(p, "bf_route_small launch");
+    }
     int64_t tile = kRouteMinTile;
     const int64_t max_tiles = std::max<int64_t>(1, kRouteMaxTable / (G + 1));
     if ((n + tile - 1) / tile > max_tiles) tile = (n + max_tiles - 1) / max_tiles;
     tile = (tile + kRouteThreads - 1) / kRouteThreads * kRouteThreads;
     const int64_t P = (n + tile - 1) / tile;
-    bf_status s;
     if ((s = grow(&p->table, &p->table_cap, P * (G + 1), "routing table")) != BF_OK) return s;
     if ((s = grow(&p->err, &p->err_cap, 1, "routing flag")) != BF_OK) return s;
     BF_CUDA(cudaMemsetAsync(p->err, 0, sizeof(int32_t), st));
@@ -334,7 +410,7 @@ bf_status route(bf_plan_t p, const int32_t *gidx, int64_t n, int32_t *perm, int3
     if ((s = launched(p, "bf_route_scan launch")) != BF_OK) return s;
     const size_t sc_smem = 8 * (G + 1) * sizeof(int32_t);
     bf_route_scatter<<<(unsigned)P, kRouteThreads, sc_smem, st>>>(gidx, n, G, (int)tile,
-                                                                    p->table, perm, gsorted);
+                                                                    p->table, perm);
     if ((s = launched(p, "bf_route_scatter launch")) != BF_OK) return s;
     return BF_OK;
 }
@@ -361,32 +437,25 @@ int grid_for(bf_plan_t p, int64_t n_items) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(n_items, cap));
 }
 
-// Device-resident apply (validated arguments).
-bf_status apply_device(bf_plan_t p, const void *S, const int32_t *gidx, void *R, int64_t n,
-                       cudaStream_t st) {
+// Device-resident apply of routed blocks (validated arguments): perm / offsets
+// from route(), or both NULL for untagged blocks (all group 0).
+bf_status apply_routed(bf_plan_t p, const void *S, const int32_t *perm, const int32_t *offsets,
+                       void *R, int64_t n, cudaStream_t st) {
     if (n == 0) return BF_OK;
     const size_t r_bytes = (size_t)n * bfk::r_block_bytes(p->layout);
     if (p->f == 0) {   // a8: the empty sum, +0.0f everywhere
         BF_CUDA(cudaMemsetAsync(R, 0, r_bytes, st));
         return BF_OK;
     }
+    bf_status s;
     bfk::KParams kp{};
     kp.Wp = p->Wp;
     kp.S = static_cast<const float *>(S);
     kp.R = static_cast<float *>(R);
     kp.n_items = n;
     kp.n_groups = p->n_groups;
-    bf_status s;
-    if (gidx && p->n_groups > 1) {
-        if ((s = grow(&p->perm, &p->perm_cap, n, "perm")) != BF_OK) return s;
-        if ((s = grow(&p->gsorted, &p->gs_cap, n, "gsorted")) != BF_OK) return s;
-        if ((s = grow(&p->offsets, &p->offsets_cap, p->n_groups + 2, "offsets")) != BF_OK)
-            return s;
-        if ((s = route(p, gidx, n, p->perm, p->gsorted, p->offsets, st)) != BF_OK) return s;
-        if ((s = check_tags_if_requested(p, st)) != BF_OK) return s;
-        kp.perm = p->perm;
-        kp.gsorted = p->gsorted;
-    }
+    kp.perm = perm;
+    kp.offsets = offsets;
     const bool tensor = use_tensor(p);
     const int grid = tensor ? (int)std::min<int64_t>(n, p->num_sms) : grid_for(p, n);
     const BfKernelEntry &kern = tensor ? p->kern_tc : p->kern;
@@ -394,8 +463,7 @@ bf_status apply_device(bf_plan_t p, const void *S, const int32_t *gidx, void *R,
     tp.Wimg = p->Wimg;
     tp.S = kp.S;
     tp.perm = kp.perm;
-    tp.gsorted = kp.gsorted;
-    tp.offsets = kp.gsorted ? p->offsets : nullptr;
+    tp.offsets = offsets;
     tp.wexact = p->wexact;
     tp.R = kp.R;
     tp.n_items = n;
@@ -422,6 +490,22 @@ bf_status apply_device(bf_plan_t p, const void *S, const int32_t *gidx, void *R,
     if ((s = launched(p, "beamforming kernel launch")) != BF_OK) return s;
     if (p->profiling) BF_CUDA(cudaEventRecord(e1, st));
     return BF_OK;
+}
+
+// Device-resident apply (validated arguments): routes tagged blocks into the
+// plan's workspace, then applies.
+bf_status apply_device(bf_plan_t p, const void *S, const int32_t *gidx, void *R, int64_t n,
+                       cudaStream_t st) {
+    if (n == 0) return BF_OK;
+    if (p->f > 0 && gidx && p->n_groups > 1) {
+        bf_status s;
+        if ((s = grow(&p->perm, &p->perm_cap, n, "perm")) != BF_OK) return s;
+        if ((s = grow(&p->offsets, &p->offsets_cap, p->n_groups + 2, "offsets")) != BF_OK) return s;
+        if ((s = route(p, gidx, n, p->perm, p->offsets, st)) != BF_OK) return s;
+        if ((s = check_tags_if_requested(p, st)) != BF_OK) return s;
+        return apply_routed(p, S, p->perm, p->offsets, R, n, st);
+    }
+    return apply_routed(p, S, nullptr, nullptr, R, n, st);
 }
 
 bf_status ensure_host_pipeline(bf_plan_t p, bool tagged) {
@@ -614,9 +698,19 @@ bf_status bf_route(bf_plan_t p, const int32_t *group_idx_dev, int64_t n_blocks, 
         BF_CUDA(cudaMemsetAsync(offsets_dev, 0, (p->n_groups + 2) * sizeof(int32_t), st));
         return BF_OK;
     }
-    bf_status s = grow(&p->gsorted, &p->gs_cap, n_blocks, "gsorted");
-    if (s != BF_OK) return s;
-    return route(p, group_idx_dev, n_blocks, perm_dev, p->gsorted, offsets_dev, st);
+    return route(p, group_idx_dev, n_blocks, perm_dev, offsets_dev, st);
+}
+
+bf_status bf_apply_routed(bf_plan_t p, const void *S_dev, const int32_t *perm_dev,
+                          const int32_t *offsets_dev, void *R_dev, int64_t n_blocks, void *stream) {
+    bf_status s = validate_apply(p, S_dev, perm_dev, R_dev, n_blocks, true);
+    if (s != BF_OK || n_blocks == 0) return s;
+    if ((perm_dev == nullptr) != (offsets_dev == nullptr))
+        return fail(BF_ERR_INVALID_VALUE, "perm and offsets must be given together");
+    if (offsets_dev && !aligned(offsets_dev, 4)) return fail(BF_ERR_MISALIGNED, "offsets misaligned");
+    DeviceGuard guard(p->device);
+    return apply_routed(p, S_dev, perm_dev, offsets_dev, R_dev, n_blocks,
+                        static_cast<cudaStream_t>(stream));
 }
 
 bf_status bf_apply_host(bf_plan_t p, const void *S_host, const int32_t *group_idx_host,
@@ -668,7 +762,6 @@ bf_status bf_destroy(bf_plan_t p) {
         cudaFree(p->Wimg);
         cudaFree(p->wexact);
         cudaFree(p->perm);
-        cudaFree(p->gsorted);
         cudaFree(p->table);
         cudaFree(p->offsets);
         cudaFree(p->err);

@@ -58,7 +58,7 @@ struct KParams {
     const float4 *Wp;         // [n_groups][F][32] float4 (plan-owned relayout)
     const float *S;           // [n_blocks] x 2*F*60 floats
     const int32_t *perm;      // [n_items] block ids (group-sorted) or NULL = identity
-    const int32_t *gsorted;   // [n_items] group of each item or NULL = group 0
+    const int32_t *offsets;   // [n_groups + 2] group starts of the sorted order, or NULL = group 0
     float *R;                 // [n_blocks] x 7680 floats
     int64_t n_items;
     int n_groups;
@@ -150,9 +150,17 @@ __global__ void __launch_bounds__(kThreads, 4) bf_ffma_kernel(const KParams p) {
     }
     __syncthreads();
 
+    // group of an item: walk the routing offsets (items are visited in increasing
+    // order, so the walk is amortised O(1)); items past offsets[G] are invalid.
+    int gi = 0;
+    auto group_of = [&](int64_t item) -> int32_t {
+        if (!p.offsets) return 0;
+        while (gi < p.n_groups && item >= __ldg(p.offsets + gi + 1)) ++gi;
+        return gi;   // == n_groups for invalid tags
+    };
     auto issue = [&](int stage, int64_t item) {   // thread 0 only
         const int64_t blk = p.perm ? (int64_t)__ldg(p.perm + item) : item;
-        const int32_t g = p.gsorted ? __ldg(p.gsorted + item) : 0;
+        const int32_t g = group_of(item);
         meta_blk[stage] = blk;
         meta_grp[stage] = g;
         mbar_arrive_expect_tx(&bars[stage], L::kSBytes);

@@ -61,7 +61,6 @@ struct TcParams {
     const float *Wimg;        // [n_groups][2][KP/4][16][8][4] floats (pre-split B image)
     const float *S;
     const int32_t *perm;      // NULL = identity order
-    const int32_t *gsorted;   // NULL = group 0 (unused: groups come from offsets)
     const int32_t *offsets;   // [n_groups + 2] group starts of the sorted order, or NULL
     const int32_t *wexact;    // [n_groups] 1 if the group's W is exactly tf32 (W2 == 0)
     float *R;

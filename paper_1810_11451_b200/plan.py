@@ -115,6 +115,26 @@ class Plan:
                              _stream_handle(stream)))
         return out
 
+    def apply_routed(self, S: torch.Tensor, perm: torch.Tensor | None,
+                     offsets: torch.Tensor | None, out: torch.Tensor | None = None,
+                     stream=None) -> torch.Tensor:
+        """bf_apply_routed: apply to blocks routed by route() (perm, offsets)."""
+        n = S.shape[0]
+        self._check(S, "S", self.s_shape(n))
+        if out is None:
+            out = torch.empty(self.r_shape(n), dtype=self.r_dtype, device=self.device)
+        self._check(out, "out", self.r_shape(n), dtype=self.r_dtype)
+        check(lib().bf_apply_routed(self._h, _ptr(S), _ptr(perm), _ptr(offsets), _ptr(out), n,
+                                    _stream_handle(stream)))
+        return out
+
+    def route_into(self, group_idx: torch.Tensor, perm: torch.Tensor, offsets: torch.Tensor,
+                   stream=None):
+        """bf_route into caller buffers (int32 [n] and int32 [n_groups + 2])."""
+        check(lib().bf_route(self._h, _ptr(group_idx), group_idx.shape[0], _ptr(perm),
+                             _ptr(offsets), _stream_handle(stream)))
+        return perm, offsets
+
     def apply_host(self, S: torch.Tensor, group_idx: torch.Tensor | None, out: torch.Tensor,
                    stream=None) -> torch.Tensor:
         """bf_apply_host on host tensors (pinned for full speed)."""

@@ -450,3 +450,27 @@ def test_f16_output_identity_is_rounded_copy(f, variant):
     exp = S.real.astype(np.float16).astype(np.float64) + 1j * S.imag.astype(np.float16).astype(np.float64)
     assert np.array_equal(R16[:, :f], exp)
     assert not np.any(R16[:, f:])
+
+
+def test_apply_routed_equals_apply(variant):
+    """bf_route on one stream + bf_apply_routed on another == bf_apply, bitwise."""
+    wl = syn.workload("c4")
+    W, S, tags = syn.workload_inputs(wl, np.arange(1500))
+    plan = Plan(f=36, variant=variant)
+    plan.set_precoders(torch.from_numpy(W).to(DEV))
+    Sd, td = torch.from_numpy(S).to(DEV), torch.from_numpy(tags).to(DEV)
+    ref = plan.apply(Sd, td)
+    side = torch.cuda.Stream()
+    perm = torch.empty(1500, dtype=torch.int32, device=DEV)
+    offs = torch.empty(57, dtype=torch.int32, device=DEV)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(side):
+        plan.route_into(td, perm, offs)
+    torch.cuda.current_stream().wait_stream(side)
+    got = plan.apply_routed(Sd, perm, offs)
+    untagged = plan.apply_routed(Sd[:10], None, None)
+    torch.cuda.synchronize()
+    assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), "routed")
+    R_ref, T, _ = oracle.beamform(W[0], S[:10], n_threads=NT)
+    assert_parity(untagged.cpu().numpy(), R_ref, T, what="untagged routed")
+    plan.close()
