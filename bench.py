@@ -108,9 +108,31 @@ def run_reference(args):
     if rank != 0:
         return 0
     import benchkit
+    import bf_synth as syn
     import oracle
     wl = workload_of(args)
     threads = oracle.max_threads()
+    if isinstance(wl, syn.FilterWorkload):
+        rates = []
+        for st in range(args.warmup + args.steps):
+            nb = max(threads, 32)
+            ss = syn.filter_signals(wl.seed, 0, np.arange(st * nb, (st + 1) * nb), wl.n, wl.M)
+            t0 = time.perf_counter()
+            oracle.filter_apply(ss, syn.filter_taps(wl.n), n_threads=threads)
+            if st >= args.warmup:
+                rates.append((nb * wl.n, time.perf_counter() - t0))
+        value = sum(r for r, _ in rates) / sum(t for _, t in rates)
+        print(json.dumps({
+            "impl": "reference", "metric": "filtered samples/s (IFFT(MULT(FFT(s))), n=2048)",
+            "value": value, "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * sum(t for _, t in rates) / len(rates),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": wl.name, "n": wl.n},
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{args.steps} steps of {max(threads, 32)} signals (fp64 O(n^2) DFTs)"},
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
+        return 0
     rates = []
     per_step_seconds = max(2.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
     for s in range(args.warmup + args.steps):
@@ -219,14 +241,29 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        plan.apply(S, tags, out=R)
-    e1.record(stream)
-    torch.cuda.synchronize()
+    small = (wl.block_bytes * n_local) < 4 * 126e6     # working set not >> the 126 MB L2
+    if not small:
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.apply(S, tags, out=R)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        elapsed_ms = e0.elapsed_time(e1)
+    else:
+        # Cold-L2 timing: overwrite a 512 MB buffer between steps (outside the events)
+        # and sum the per-step device times.
+        flush = torch.empty(128 << 20, dtype=torch.float32, device=dev)
+        elapsed_ms = 0.0
+        for _ in range(args.steps):
+            sync.fill_u32(flush, 0)
+            e0.record(stream)
+            plan.apply(S, tags, out=R)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            elapsed_ms += e0.elapsed_time(e1)
+        del flush
     if world > 1:
         dist.barrier()
-    elapsed_ms = e0.elapsed_time(e1)
     kern_ms, kern_n = plan.kernel_time()
     launches = plan.launch_count() - launches0
     plan.set_profiling(False)
@@ -355,8 +392,8 @@ def run_ours(args):
                        "b": wl.b, "blocks": wl.n_blocks, "groups": wl.n_groups,
                        "layout": args.layout, "parallelism": f"dp{world} (blocks sharded by subband)"
                        if wl.tagged else f"dp{world}",
-                       "l2": "inputs larger than L2 (S+R >> 126 MB)" if bytes_launch > 512e6
-                       else "inputs fit in L2 (warm; no flush)",
+                       "l2": "inputs larger than L2 (S+R >> 126 MB)" if not small
+                       else "L2 flushed between steps (512 MB write outside the timed events)",
                        "kernel": cfg, "gpu": gpu_name, "w_broadcast_ms": t_bc * 1e3},
             "flops_per_s": total_blocks * wl.block_flops * args.steps / (elapsed_ms * 1e-3),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
