@@ -4,6 +4,7 @@
 // group routing (a3, stable counting sort), dispatch to the per-f kernel
 // instantiation (a4+a5+a7), the f = 0 path (a8), and the host-buffer pipeline
 // used for end-to-end measurement.  PAPER.md:84-86 defines the operation.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -91,22 +92,22 @@ __global__ void bf_relayout_w(const float *__restrict__ W, int n_groups, int F, 
 // img[g][t][kc][ng][r][e] = term t of B'[n = 8 ng + r][kk = 4 kc + e].
 __global__ void bf_tc_build_wimg(const float *__restrict__ W, int n_groups, int F, int layout,
                                  float *__restrict__ img) {
+    // Per group: [W1 tf32 core matrices: KP/4 K-chunks x 16 row groups x 8 rows x 4]
+    //            [bf16 correction image: K'' = 2 KP as KP/4 chunks of 8 bf16, rows n;
+    //             K'' < KP -> bf16(W1[n][K'']), K'' >= KP -> bf16(W2[n][K'' - KP])]
+    // with B'[n][kk] the real embedding (n = 2i + c_out, kk = 2k + c_in) and
+    // W1 = tf32(B'), W2 = tf32(B' - W1).
     const int KP = bftc::kp_of(F);
-    const int64_t per_group = 2LL * KP * 128;
+    const int64_t half = (int64_t)KP * 128;            // 32-bit words per part
+    const int64_t per_group = 2 * half;
     const int64_t total = (int64_t)n_groups * per_group;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t g = idx / per_group;
-        int rem = (int)(idx - g * per_group);
-        const int term = rem / (KP * 128);
-        rem -= term * KP * 128;
-        const int kc = rem / 512;           // 16 groups x 8 rows x 4 elements per K chunk
-        rem -= kc * 512;
-        const int ng = rem / 32, r = (rem / 4) % 8, e = rem % 4;
-        const int n = ng * 8 + r, kk = kc * 4 + e;
-        const int i = n >> 1, cout = n & 1, k = kk >> 1, cin = kk & 1;
-        float val = 0.0f;
-        if (k < F) {
+        const int rem = (int)(idx - g * per_group);
+        auto bprime = [&](int n, int kk) -> float {
+            const int i = n >> 1, cout = n & 1, k = kk >> 1, cin = kk & 1;
+            if (k >= F) return 0.0f;
             float wr, wi;
             if (layout != BF_LAYOUT_PLANAR) {
                 wr = W[((g * 64 + i) * F + k) * 2];
@@ -116,21 +117,41 @@ __global__ void bf_tc_build_wimg(const float *__restrict__ W, int n_groups, int 
                 wi = W[(g * 2 + 1) * 64 * F + i * F + k];
             }
             // B'[2i][2k] = wr, B'[2i][2k+1] = -wi, B'[2i+1][2k] = wi, B'[2i+1][2k+1] = wr
-            val = cout == 0 ? (cin == 0 ? wr : -wi) : (cin == 0 ? wi : wr);
+            return cout == 0 ? (cin == 0 ? wr : -wi) : (cin == 0 ? wi : wr);
+        };
+        if (rem < half) {                               // W1, tf32
+            const int kc = rem / 512, r2 = rem % 512;
+            const int ng = r2 / 32, r = (r2 / 4) % 8, e = r2 % 4;
+            img[idx] = tc::to_tf32(bprime(ng * 8 + r, kc * 4 + e));
+        } else {                                        // bf16 pair (K'' = 2 e2, 2 e2 + 1)
+            const int w = rem - (int)half;
+            const int kc = w / 512, r2 = w % 512;
+            const int ng = r2 / 32, r = (r2 / 4) % 8, e2 = r2 % 4;
+            const int n = ng * 8 + r;
+            float pair[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int kk2 = kc * 8 + 2 * e2 + h;
+                const int kk = kk2 < KP ? kk2 : kk2 - KP;
+                const float v = bprime(n, kk);
+                const float w1 = tc::to_tf32(v);
+                pair[h] = kk2 < KP ? w1 : tc::to_tf32(v - w1);
+            }
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn(pair[0], pair[1]);   // .x low
+            img[idx] = __uint_as_float(*reinterpret_cast<const uint32_t *>(&b2));
         }
-        const float w1 = tc::to_tf32(val);
-        img[idx] = term == 0 ? w1 : tc::to_tf32(val - w1);
     }
 }
 
-
-// wexact[g] = 1 when group g's W is exactly representable in tf32 (its W2 half
-// of the image is all zero); the tensor kernel then multiplies S3 instead of W2.
+// wexact[g] = 1 when group g's W is exactly representable in tf32: the W2 part of
+// its bf16 correction image (the last quarter of the group image) is all zero.  The
+// tensor kernel then multiplies S3 in tf32 instead of running the bf16 corrections.
 __global__ void bf_tc_wexact(const float *__restrict__ img, int KP, int32_t *__restrict__ wexact) {
     const int64_t per_group = 2LL * KP * 128;
-    const float *w2 = img + blockIdx.x * per_group + per_group / 2;
+    const float *w2 = img + blockIdx.x * per_group + per_group / 2 + per_group / 4;
     int nz = 0;
-    for (int i = threadIdx.x; i < KP * 128; i += blockDim.x) nz |= (w2[i] != 0.0f);
+    for (int i = threadIdx.x; i < KP * 128 / 2; i += blockDim.x)
+        nz |= (__float_as_uint(w2[i]) & 0x7FFF7FFFu) != 0u;
     nz = __syncthreads_or(nz);
     if (threadIdx.x == 0) wexact[blockIdx.x] = nz ? 0 : 1;
 }

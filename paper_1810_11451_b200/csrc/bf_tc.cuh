@@ -63,6 +63,8 @@ struct TcParams {
     const int32_t *perm;      // NULL = identity order
     const int32_t *offsets;   // [n_groups + 2] group starts of the sorted order, or NULL
     const int32_t *wexact;    // [n_groups] 1 if the group's W is exactly tf32 (W2 == 0)
+    // Wimg per group: [W1 as tf32 core matrices (KP/4 K-chunks)] then
+    // [C = (W1 ; W2) as bf16 core matrices (2 KP bf16 of K = KP/4 chunks of 16 B)]
     float *R;
     int64_t n_items;
     int n_groups;
@@ -71,7 +73,7 @@ struct TcParams {
 template <int F>
 struct TcSmem {
     static constexpr int KP = kp_of(F);
-    static constexpr int kWBytes = 2 * KP * 128 * 4;   // two tf32 terms
+    static constexpr int kWBytes = 2 * KP * 128 * 4;   // W1 tf32 image + bf16 correction image
     static constexpr int kSBlock = 480 * F;            // one block of S
     static constexpr int kFixed = kWBytes + 24 * 8 + 16 + 1028 * 4;
     static constexpr int kStagesFit = (kSmemLimit - kFixed) / (2 * kSBlock);
@@ -252,7 +254,24 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
                         const float x3 = r1 - x2;            // exact, fits tf32
                         v[e] = __float_as_uint(term == 0 ? x1 : (term == 1 ? x2 : x3));
                     }
-                    if constexpr (!(DBG & 4)) tc::tmem_st8(a_lane + term * KP + c0, v);
+                    if (term == 1 && !cur_exact) {
+                        // general W: region 1 holds the bf16 correction operand, K'' = 2 KP
+                        // elements [S2 (kk < KP) | S1 (kk >= KP)], two per column: this
+                        // chunk's 8 values of S2 go to columns c0/2.., of S1 to KP/2 + c0/2..
+                        uint32_t w2[4], w1[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            w2[e] = tc::pack_bf16x2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+                            const float s1a = tc::tf32_round(x[2 * e]), s1b = tc::tf32_round(x[2 * e + 1]);
+                            w1[e] = tc::pack_bf16x2(s1a, s1b);
+                        }
+                        if constexpr (!(DBG & 4)) {
+                            tc::tmem_st4(a_lane + KP + c0 / 2, w2);
+                            tc::tmem_st4(a_lane + KP + KP / 2 + c0 / 2, w1);
+                        }
+                    } else {
+                        if constexpr (!(DBG & 4)) tc::tmem_st8(a_lane + term * KP + c0, v);
+                    }
                 }
                 tc::tmem_st_wait();
                 tc::fence_before_sync();
@@ -295,6 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
         int cur_g = -1;
         uint32_t wphase = 0;
         constexpr uint32_t idesc = tc::idesc_tf32(128, 128);
+        constexpr uint32_t idesc_c = tc::idesc_bf16(128, 128);
         const uint32_t w_base = tc::smem_u32(Wsm);
         bool exact = false;
         for (int64_t t = 0; it.next(tl); ++t) {
@@ -314,30 +334,35 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
             const uint32_t u = (uint32_t)(t >> 1);
             const uint32_t d = tmem + kDCol0 + 128 * b;
             bfk::mbar_wait(bar_d_free + b, (u & 1) ^ 1);
-            // Three MMA groups over K, small terms first:
+            // MMA groups over K, small terms first:
             //   tf32-exact W (W2 == 0, e.g. identity / selection): S2 W1, S3 W1, S1 W1
-            //   (= S W exactly up to accumulation rounding: copies are bit-exact);
-            //   general W: S2 W1, S1 W1, S1 W2 (dropped S3 W1, S2 W2 <= 2^-21 T).
+            //   in tf32 (= S W exactly up to accumulation rounding: copies are bit-exact);
+            //   general W: the two correction products S2 W1 + S1 W2 as ONE bf16 MMA
+            //   group over K'' = 2 KP ([S2 | S1] x [W1 ; W2], KP/8 instructions of K = 16),
+            //   then S1 W1 in tf32 — 2 KP/8 instead of 3 KP/8 MMAs.
             // Each split term's TMEM region is released by a commit once read.
 #pragma unroll
-            for (int grp = 0; grp < 4; ++grp) {
-                const int at = grp == 0 ? 1 : (grp == 1 ? 2 : 0);   // A term: S2, S3, S1, S1
-                const int wt = grp == 3 ? 1 : 0;                    // W term: W1, W1, W1, W2
-                if (grp < 3) {
-                    bfk::mbar_wait(bar_a_full + at, (uint32_t)(t & 1));
-                    tc::fence_after_sync();
-                }
-                const bool run = (grp == 1) ? exact : (grp == 3 ? !exact : true);
+            for (int grp = 0; grp < 3; ++grp) {
+                const int at = grp == 0 ? 1 : (grp == 1 ? 2 : 0);   // A region: S2/corr, S3, S1
+                bfk::mbar_wait(bar_a_full + at, (uint32_t)(t & 1));
+                tc::fence_after_sync();
+                const bool run = grp != 1 || exact;
+                const bool bf16 = grp == 0 && !exact;
                 if (lane == 0) {
                     if (run) {
 #pragma unroll
                         for (int kb = 0; kb < KP / 8; ++kb) {
                             const uint64_t desc = tc::smem_desc(
-                                w_base + (uint32_t)((wt * (KP / 4) + 2 * kb) * 16 * 128), 16 * 128,
-                                128);
-                            if constexpr (!(DBG & 1))
-                                tc::mma_tf32_ts(d, tmem + at * KP + kb * 8, desc, idesc,
-                                                (grp | kb) != 0);
+                                w_base + (uint32_t)(((bf16 ? KP / 4 : 0) + 2 * kb) * 16 * 128),
+                                16 * 128, 128);
+                            if constexpr (!(DBG & 1)) {
+                                if (bf16)
+                                    tc::mma_bf16_ts(d, tmem + at * KP + kb * 8, desc, idesc_c,
+                                                    kb != 0);
+                                else
+                                    tc::mma_tf32_ts(d, tmem + at * KP + kb * 8, desc, idesc,
+                                                    (grp | kb) != 0);
+                            }
                         }
                     }
                     if (grp < 2) tc::mma_commit(bar_a_free + at);
