@@ -52,7 +52,8 @@
  * so callers need no CUDA headers.  All enqueueing calls are asynchronous with
  * respect to the host unless stated otherwise.
  *
- * Concurrency: distinct plans are independent.  bf_set_precoders must not race
+ * Concurrency: distinct plans are independent.  A plan is not thread-safe: it
+ * must not be used from several host threads at the same time.  bf_set_precoders must not race
  * with in-flight applies of the same plan.  Untagged applies of one plan may
  * run on several streams concurrently (read-only W); tagged applies share the
  * plan's routing workspace and must be serialised by the caller (one stream).
@@ -159,9 +160,10 @@ bf_status bf_destroy(bf_plan_t p);
 
 /* Instrumentation (used by bench.py; never changes results).
  * set_profiling(1): every bf_apply also records CUDA events around the main
- * beamforming kernel on its launching stream.  kernel_time: synchronises those
- * events, returns the summed milliseconds and number of timed launches, and
- * clears the record.  launch_count: kernels this plan has launched so far
+ * beamforming kernel on its launching stream (at most 65,536 launches are kept
+ * between two kernel_time calls).  kernel_time: synchronises those events,
+ * returns the summed milliseconds and number of timed launches, and clears the
+ * record.  launch_count: kernels this plan has launched so far
  * (routing, relayout and beamforming kernels; memsets and copies excluded). */
 bf_status bf_plan_set_profiling(bf_plan_t p, int enable);
 bf_status bf_plan_kernel_time(bf_plan_t p, double *total_ms, int64_t *n_launches);

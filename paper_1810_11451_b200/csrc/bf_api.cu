@@ -39,6 +39,7 @@ constexpr int kRouteMinTile = 512;          // small batches still spread over s
 constexpr int kRouteMaxTable = 65536;      // tiles x (groups + 1) entries
 constexpr int64_t kDefaultHostChunk = 2048;
 constexpr int kHostSlots = 3;
+constexpr size_t kMaxProfEvents = 1 << 16;  // timed launches kept between kernel_time() calls
 // AUTO variant table (measured, profiles/r01_sweep_f_*.jsonl: c3, 100 000 blocks
 // per f, both layouts): the tensor-core kernel is at least as fast as the FFMA
 // kernel for every f >= 1 (equal at f = 4, 2.2x at f = 36), so AUTO picks it.
@@ -490,7 +491,8 @@ bf_status apply_routed(bf_plan_t p, const void *S, const int32_t *perm, const in
     tp.n_items = n;
     tp.n_groups = p->n_groups;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (p->profiling) {
+    const bool prof = p->profiling && p->prof_used < kMaxProfEvents;
+    if (prof) {
         if (p->prof_used == p->prof_events.size()) {
             cudaEvent_t a, b;
             BF_CUDA(cudaEventCreate(&a));
@@ -509,7 +511,7 @@ bf_status apply_routed(bf_plan_t p, const void *S, const int32_t *perm, const in
                                      tensor ? args_tc : args_ffma, (size_t)kern.smem_bytes, st);
     if (e != cudaSuccess) return cuda_fail(e, "beamforming kernel launch");
     if ((s = launched(p, "beamforming kernel launch")) != BF_OK) return s;
-    if (p->profiling) BF_CUDA(cudaEventRecord(e1, st));
+    if (prof) BF_CUDA(cudaEventRecord(e1, st));
     return BF_OK;
 }
 
