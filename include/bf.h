@@ -178,6 +178,16 @@ bf_status bf_plan_get_variant(bf_plan_t p, int *resolved);
 /* Chunk size (blocks) of bf_apply_host's pipeline; 0 selects the default. */
 bf_status bf_plan_set_host_chunk(bf_plan_t p, int64_t blocks);
 
+/* Number of SMs the beamforming kernel of later applies spreads over
+ * (grid = sms x resident CTAs per SM, capped by the block count); 0 = every SM
+ * of the device (the default), values above the SM count are clamped.  For
+ * several plans applied concurrently on their own streams (e.g. one plan per
+ * cell): giving each plan a share proportional to
+ * its work lets the kernels run side by side instead of each one filling and
+ * draining the whole GPU.  Never changes results (the block -> CTA split does
+ * not enter the arithmetic).  BF_ERR_INVALID_VALUE if sms < 0. */
+bf_status bf_plan_set_sm_share(bf_plan_t p, int sms);
+
 /* Static description of the kernel chosen for this plan: grid and block size
  * for n_blocks, dynamic shared memory bytes and resident CTAs per SM. */
 bf_status bf_plan_kernel_config(bf_plan_t p, int64_t n_blocks, int *grid, int *block,

@@ -370,6 +370,7 @@ struct bf_plan_s {
     BfKernelEntry kern{};       // FFMA kernel of this (f, layout)
     BfKernelEntry kern_tc{};    // tensor-core kernel of this (f, layout)
     int ctas_per_sm = 0;
+    int sm_share = 0;           // bf_plan_set_sm_share (0 = every SM)
     int variant = BF_VARIANT_AUTO;
     float4 *Wp = nullptr;       // FFMA precoder image
     int64_t Wp_cap = 0;
@@ -454,8 +455,14 @@ bool use_tensor(bf_plan_t p) {
     return p->f >= kAutoTensorMinF;
 }
 
-int grid_for(bf_plan_t p, int64_t n_items) {
-    const int64_t cap = (int64_t)p->num_sms * std::max(1, p->ctas_per_sm);
+int sms_used(bf_plan_t p) {
+    return p->sm_share > 0 ? std::min(p->sm_share, p->num_sms) : p->num_sms;
+}
+
+// Grid of the beamforming kernel for n_items blocks: persistent CTAs, one per SM
+// (tensor) or ctas_per_sm per SM (FFMA), over the plan's SM share.
+int grid_for(bf_plan_t p, int64_t n_items, bool tensor) {
+    const int64_t cap = (int64_t)sms_used(p) * (tensor ? 1 : std::max(1, p->ctas_per_sm));
     return (int)std::max<int64_t>(1, std::min<int64_t>(n_items, cap));
 }
 
@@ -479,7 +486,7 @@ bf_status apply_routed(bf_plan_t p, const void *S, const int32_t *perm, const in
     kp.perm = perm;
     kp.offsets = offsets;
     const bool tensor = use_tensor(p);
-    const int grid = tensor ? (int)std::min<int64_t>(n, p->num_sms) : grid_for(p, n);
+    const int grid = grid_for(p, n, tensor);
     const BfKernelEntry &kern = tensor ? p->kern_tc : p->kern;
     bftc::TcParams tp{};
     tp.Wimg = p->Wimg;
@@ -856,13 +863,20 @@ bf_status bf_plan_set_host_chunk(bf_plan_t p, int64_t blocks) {
     return BF_OK;
 }
 
+bf_status bf_plan_set_sm_share(bf_plan_t p, int sms) {
+    if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
+    if (sms < 0) return fail(BF_ERR_INVALID_VALUE, "sms must be >= 0 (got %d)", sms);
+    p->sm_share = sms;
+    return BF_OK;
+}
+
 bf_status bf_plan_kernel_config(bf_plan_t p, int64_t n_blocks, int *grid, int *block,
                                 int *smem_bytes, int *ctas_per_sm) {
     if (!p || !grid || !block || !smem_bytes || !ctas_per_sm)
         return fail(BF_ERR_INVALID_VALUE, "NULL argument");
     const bool tensor = p->f > 0 && use_tensor(p);
     const int64_t nb = std::max<int64_t>(n_blocks, 1);
-    *grid = p->f == 0 ? 0 : (tensor ? (int)std::min<int64_t>(nb, p->num_sms) : grid_for(p, nb));
+    *grid = p->f == 0 ? 0 : grid_for(p, nb, tensor);
     *block = p->f == 0 ? 0 : (tensor ? bftc::kThreads : bfk::kThreads);
     *smem_bytes = tensor ? p->kern_tc.smem_bytes : p->kern.smem_bytes;
     *ctas_per_sm = tensor ? 1 : p->ctas_per_sm;

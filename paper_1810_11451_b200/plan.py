@@ -185,6 +185,10 @@ class Plan:
         check(lib().bf_plan_get_variant(self._h, ctypes.byref(v)))
         return Variant(v.value)
 
+    def set_sm_share(self, sms: int) -> None:
+        """bf_plan_set_sm_share: spread later applies over `sms` SMs (0 = all)."""
+        check(lib().bf_plan_set_sm_share(self._h, int(sms)))
+
     def set_host_chunk(self, blocks: int) -> None:
         check(lib().bf_plan_set_host_chunk(self._h, int(blocks)))
 

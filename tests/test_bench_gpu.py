@@ -1,0 +1,88 @@
+"""bench.py's JSON contract on the GPU, including the N > 1 path.
+
+The N = 2 case runs two torchrun ranks on the box's one GPU with the gloo backend
+(bench.py's BF_BENCH_SHARE_GPU / BF_BENCH_DIST_BACKEND test hooks): the ranks never
+wait on one another on the device, so this exercises the sharding, W broadcast and
+max-over-ranks reduction of the real bench end to end.  Small configs keep it quick.
+"""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():   # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+        "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+        "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks")
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(args, world=1, timeout=600):
+    env = dict(os.environ)
+    if world == 1:
+        cmd = [sys.executable, "bench.py", *args]
+    else:
+        env.update(BF_BENCH_SHARE_GPU="1", BF_BENCH_DIST_BACKEND="gloo")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
+               "--master-port", str(_port()), "bench.py", "--gpus", str(world), *args]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, r.stderr[-4000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_bench_c2_single_gpu_contract():
+    d = _run(["--config", "c2", "--steps", "5", "--warmup", "3", "--cpu-seconds", "1",
+              "--e2e-steps", "2"])
+    for k in KEYS:
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["unit"] == "REs/s" and d["value"] > 0
+    assert d["config"]["workload"] == "c2"
+    assert d["roofline"]["bound"] in ("hbm", "alu") and 0 < d["roofline"]["frac"] < 1.5
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 770 * 480 * 36
+    assert d["e2e"]["d2h_bytes_per_step"] == 770 * 30720
+    assert d["gpu_launches"] >= 5
+
+
+def test_bench_c4_two_ranks_share_gpu():
+    """torchrun N = 2: subband sharding, W broadcast, max over ranks, whole-job value."""
+    d = _run(["--config", "c4", "--steps", "3", "--warmup", "3", "--no-e2e"], world=2)
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["config"]["parallelism"].startswith("dp2")
+    assert d["cpu_baseline"] is None          # rank 0 at N = 1 only
+    assert d["gpu_launches"] >= 2 * 3
+
+
+def test_bench_c5_short_stream():
+    d = _run(["--config", "c5", "--steps", "3", "--warmup", "3", "--c5-chunks", "64"])
+    assert d["config"]["workload"] == "c5" and d["config"]["chunks_per_step"] == 64
+    assert d["config"]["launch_mode"] == "cuda_graph"
+    assert sum(d["config"]["sm_shares"]) + d["config"]["route_sms"] \
+        == torch.cuda.get_device_properties(0).multi_processor_count
+    assert d["value"] > 0 and 0 < d["roofline"]["frac"] < 1.5
+
+
+def test_bench_reference_arm():
+    d = _run(["--impl", "reference", "--config", "c2", "--steps", "2", "--warmup", "3",
+              "--cpu-seconds", "1"])
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0

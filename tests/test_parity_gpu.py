@@ -474,3 +474,41 @@ def test_apply_routed_equals_apply(variant):
     R_ref, T, _ = oracle.beamform(W[0], S[:10], n_threads=NT)
     assert_parity(untagged.cpu().numpy(), R_ref, T, what="untagged routed")
     plan.close()
+
+
+def test_sm_share_concurrent_plans_bitwise(variant):
+    """bf_plan_set_sm_share: plans of different f on their own streams, each on a share of
+    the SMs, running side by side; results equal the default full-grid applies bitwise."""
+    shares, fs = [5, 37, 1, 200], [3, 36, 17, 8]
+    plans, ins, refs = [], [], []
+    for i, (sh, f) in enumerate(zip(shares, fs)):
+        W = syn.precoders(41, i, 4, 64, f, "unit_columns")
+        S = syn.qam_symbols(41, i, np.arange(2003), f, 60, 16)
+        tags = syn.subband_tags(41, np.arange(2003) + i, 4)
+        p = Plan(f=f, variant=variant)
+        p.set_precoders(torch.from_numpy(W).to(DEV))
+        Sd, td = torch.from_numpy(S).to(DEV), torch.from_numpy(tags).to(DEV)
+        refs.append(p.apply(Sd, td))
+        p.set_sm_share(sh)
+        cfg = p.kernel_config(2003)
+        sms = torch.cuda.get_device_properties(DEV).multi_processor_count
+        assert cfg["grid"] == min(sh, sms) * cfg["ctas_per_sm"]
+        plans.append(p)
+        ins.append((Sd, td))
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in plans]
+    outs = []
+    for p, (Sd, td), st in zip(plans, ins, streams):
+        with torch.cuda.stream(st):
+            outs.append(p.apply(Sd, td))
+    torch.cuda.synchronize()
+    for i, (got, ref) in enumerate(zip(outs, refs)):
+        assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), f"share {shares[i]}")
+    W = syn.precoders(41, 0, 4, 64, fs[0], "unit_columns")
+    S = syn.qam_symbols(41, 0, np.arange(2003), fs[0], 60, 16)
+    R_ref, T, _ = oracle.beamform(W, S, syn.subband_tags(41, np.arange(2003), 4), n_threads=NT)
+    assert_parity(outs[0].cpu().numpy(), R_ref, T, what="sm share 5")
+    with pytest.raises(bf.BfError):
+        plans[0].set_sm_share(-1)
+    for p in plans:
+        p.close()
