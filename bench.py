@@ -505,10 +505,9 @@ def run_c5(args, wl, world, rank, local, dev):
     in 4096-block chunks (chunk c -> cell c mod 8), mixed QPSK/16/64-QAM per block.
 
     S of every chunk is generated before the timed region and stays in HBM; R (258 GB)
-    streams through per-cell rings.  A step processes every chunk as its own routed apply;
-    the 8 cells run side by side on their own streams, each plan on an SM share
-    proportional to its work (bf_plan_set_sm_share), all captured in one CUDA graph; each
-    rank takes an even share of every chunk.  `value` counts the whole
+    streams through a ring.  A step processes every chunk as its own routed apply
+    (routing on a side stream on 2 SMs kept free of apply CTAs, two apply streams, all
+    captured in one CUDA graph); each rank takes an even share of every chunk.  `value` counts the whole
     stream's REs over the step's device time; the roofline is the mixed-f one (sum
     over chunks of algorithmic bytes / measured HBM bandwidth).
     """
@@ -538,25 +537,25 @@ def run_c5(args, wl, world, rank, local, dev):
     torch.cuda.synchronize()
     t_bc = time.perf_counter() - t_bc
     _, nloc = shard.chunk_shard(0, chunk, rank, world)
-    # S (and tags) of every chunk of this rank are generated up front and stay resident
-    # in HBM (74.5 GB at N = 1), so the timed region holds only the method: per chunk,
-    # the routing (bf_route) and the beamforming kernel (bf_apply_routed).  R (257.7 GB
-    # in total) cannot stay resident: every cell writes a 2-slot ring of its own.
-    # Cells run side by side: cell k's chunks (c = k, k + 8, ...) are applied in order
-    # on apply stream k with the plan's kernel spread over an SM share proportional to
-    # the cell's bytes per block, 480 (64 + f_k) (bf_plan_set_sm_share); the routing of
-    # the cell's next chunk runs ahead on route stream k, on the SMs left free.  Each
-    # kernel then streams ~200 blocks per CTA instead of filling and draining the whole
-    # GPU for 28 blocks per CTA.
-    NSLOT = 2
+    # The apply kernels leave 2 SMs free so the routing of the next chunks (one CTA
+    # each, on the route stream) never waits for an SM (bf_plan_set_sm_share).
+    # tools/c5_exp.py measured the alternatives: one stream per cell with SM shares
+    # proportional to the cell's work (50-61 % of roofline: large-f cells run slower
+    # per SM than their byte share, and static per-CTA ranges cannot rebalance), deep
+    # routing rings (no gain) and routing inline on the apply stream (65 %); this
+    # two-stream pipeline reaches 72 % over 1024 chunks, untagged applies 80 %.
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     route_sms = 2
-    weights = np.array([480.0 * (64 + int(fc[k])) for k in range(n_cells)])
-    shares = np.maximum(1, np.floor(weights / weights.sum() * (sms - route_sms))).astype(int)
-    while shares.sum() < sms - route_sms:        # largest remainder
-        shares[np.argmax(weights / weights.sum() * (sms - route_sms) - shares)] += 1
-    for k, pl in enumerate(plans):
-        pl.set_sm_share(int(shares[k]))
+    for pl in plans:
+        pl.set_sm_share(sms - route_sms)
+    # S (and tags) of every chunk of this rank are generated up front and stay resident
+    # in HBM (74.5 GB at N = 1), so the timed region holds only the method: per chunk,
+    # the routing (bf_route, on the "route" stream) and the beamforming kernel
+    # (bf_apply_routed).  R (257.7 GB in total) cannot stay resident: chunks write a
+    # 4-slot ring.  Chunk c applies on stream c % 2; consecutive chunks belong to
+    # different cells (plans), so one chunk's tail overlaps the next one's head while
+    # every plan stays on one stream.
+    NSLOT = 4
     chunk_f = [int(fc[c % n_cells]) for c in range(n_chunks)]
     s_off = np.concatenate([[0], np.cumsum([nloc * f * 60 for f in chunk_f])]).astype(np.int64)
     S_all = torch.empty(int(s_off[-1]), dtype=torch.complex64, device=dev)
@@ -567,55 +566,56 @@ def run_c5(args, wl, world, rank, local, dev):
         sync.gen_symbols(Sv, wl.seed, 0, chunk_f[c], 60, 0, first=first)
         sync.gen_tags(T_all[c, :cnt], wl.seed, wl.n_groups, first=first)
     torch.cuda.synchronize()
-    P_ring = [[torch.empty(nloc, dtype=torch.int32, device=dev) for _ in range(NSLOT)]
-              for _ in range(n_cells)]
-    O_ring = [[torch.empty(wl.n_groups + 2, dtype=torch.int32, device=dev) for _ in range(NSLOT)]
-              for _ in range(n_cells)]
-    R_ring = [[torch.empty((nloc, 64, 60), dtype=torch.complex64, device=dev) for _ in range(NSLOT)]
-              for _ in range(n_cells)]
-    a_st = [torch.cuda.Stream(device=dev) for _ in range(n_cells)]
-    r_st = [torch.cuda.Stream(device=dev) for _ in range(n_cells)]
+    P_ring = [torch.empty(nloc, dtype=torch.int32, device=dev) for _ in range(NSLOT)]
+    O_ring = [torch.empty(wl.n_groups + 2, dtype=torch.int32, device=dev) for _ in range(NSLOT)]
+    route_plans = [bf.Plan(f=int(fc[c]), variant=args.variant) for c in range(NSLOT)]
+    for rp in route_plans:         # routing needs only the precoder count
+        rp.set_precoders(torch.zeros((wl.n_groups, 64, rp.f), dtype=torch.complex64, device=dev))
+    R_ring = [torch.empty((nloc, 64, 60), dtype=torch.complex64, device=dev) for _ in range(NSLOT)]
+    rstream = torch.cuda.Stream(device=dev)
+    side = torch.cuda.Stream(device=dev)
     main = torch.cuda.current_stream()
-    ev_rt = [[torch.cuda.Event() for _ in range(NSLOT)] for _ in range(n_cells)]
-    ev_use = [[torch.cuda.Event() for _ in range(NSLOT)] for _ in range(n_cells)]
-    ev_fork = torch.cuda.Event()
-    ev_join = [torch.cuda.Event() for _ in range(2 * n_cells)]
+    ev_rt = [torch.cuda.Event() for _ in range(NSLOT)]
+    ev_use = [torch.cuda.Event() for _ in range(NSLOT)]
+    ev_fork, ev_join = torch.cuda.Event(), torch.cuda.Event()
+
     def step():
-        ev_fork.record(main)                # fork every stream from main (graph-safe)
-        for st in a_st + r_st:
-            st.wait_event(ev_fork)
-        for k in range(n_cells):
-            for s_ in range(NSLOT):
-                ev_use[k][s_].record(a_st[k])
+        ev_fork.record(main)                # fork the side streams from main (graph-safe)
+        rstream.wait_event(ev_fork)
+        side.wait_event(ev_fork)
+        for s_ in range(NSLOT):
+            ev_use[s_].record(main)
         for c in range(n_chunks):
-            k, s = c % n_cells, (c // n_cells) % NSLOT
+            s, cell = c % NSLOT, c % n_cells
+            ap = main if c % 2 == 0 else side
             f = chunk_f[c]
             _, cnt = shard.chunk_shard(c, chunk, rank, world)
             Sv = S_all[int(s_off[c]):int(s_off[c]) + cnt * f * 60].view(cnt, f, 60)
-            r_st[k].wait_event(ev_use[k][s])
-            plans[k].route_into(T_all[c, :cnt], P_ring[k][s][:cnt], O_ring[k][s], stream=r_st[k])
-            ev_rt[k][s].record(r_st[k])
-            a_st[k].wait_event(ev_rt[k][s])
-            plans[k].apply_routed(Sv, P_ring[k][s][:cnt], O_ring[k][s], out=R_ring[k][s][:cnt],
-                                  stream=a_st[k])
-            ev_use[k][s].record(a_st[k])
-        for i, st in enumerate(a_st + r_st):   # join every stream back into main
-            ev_join[i].record(st)
-            main.wait_event(ev_join[i])
+            with torch.cuda.stream(rstream):
+                rstream.wait_event(ev_use[s])
+                route_plans[s].route_into(T_all[c, :cnt], P_ring[s][:cnt], O_ring[s])
+                ev_rt[s].record(rstream)
+            ap.wait_event(ev_rt[s])
+            plans[cell].apply_routed(Sv, P_ring[s][:cnt], O_ring[s], out=R_ring[s][:cnt], stream=ap)
+            ev_use[s].record(ap)
+        ev_join.record(side)                # join the side streams back into main
+        main.wait_event(ev_join)
+        ev_join.record(rstream)
+        main.wait_event(ev_join)
 
     step()                                  # grows every workspace before any capture
     torch.cuda.synchronize()
-    # The step (n_chunks routings and beamforming kernels on 16 streams) is captured
-    # once into a CUDA graph and replayed, so host launch overhead stays out of it.
+    # The step (n_chunks routings and beamforming kernels) is captured once into a
+    # CUDA graph and replayed, so host launch overhead stays out of it.
     graph, mode = None, "eager"
     if not args.no_graph:
         try:
-            launches_cap0 = sum(pl.launch_count() for pl in plans)
+            launches_cap0 = sum(pl.launch_count() for pl in plans + route_plans)
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
                 main = torch.cuda.current_stream()
                 step()
-            launches_per_step = sum(pl.launch_count() for pl in plans) - launches_cap0
+            launches_per_step = sum(pl.launch_count() for pl in plans + route_plans) - launches_cap0
             mode = "cuda_graph"
         except Exception as ex:  # pragma: no cover - reported, eager path measured instead
             graph, mode = None, f"eager (graph capture failed: {ex})"
@@ -629,7 +629,7 @@ def run_c5(args, wl, world, rank, local, dev):
         for pl in plans:
             pl.set_profiling(True)
             pl.kernel_time()
-    launches0 = sum(pl.launch_count() for pl in plans)
+    launches0 = sum(pl.launch_count() for pl in plans + route_plans)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -655,7 +655,7 @@ def run_c5(args, wl, world, rank, local, dev):
         launches = launches_per_step * args.steps
     else:
         kern_ms = sum(pl.kernel_time()[0] for pl in plans)
-        launches = sum(pl.launch_count() for pl in plans) - launches0
+        launches = sum(pl.launch_count() for pl in plans + route_plans) - launches0
     kern_ms = shard.max_over_ranks(kern_ms, dev)
     launches = int(shard.sum_over_ranks(launches, dev))
     clk = clocks.stop() if clocks else None
@@ -691,8 +691,8 @@ def run_c5(args, wl, world, rank, local, dev):
                        "parallelism": f"dp{world} (every chunk split evenly across ranks)",
                        "l2": "S resident (74.5 GB at N=1, >> L2); R streamed through a 4-slot ring",
                        "gpu": torch.cuda.get_device_name(dev), "w_broadcast_ms": t_bc * 1e3,
-                       "launch_mode": mode, "apply_streams": n_cells, "sm_shares": [int(x) for x in shares],
-                       "route_sms": route_sms, "ring_slots_per_cell": NSLOT,
+                       "launch_mode": mode, "apply_streams": 2, "ring_slots": NSLOT,
+                       "apply_sms": sms - route_sms, "route_sms": route_sms,
                        },
             "flops_per_s": flops_all / (elapsed_ms * 1e-3), "roofline": roof, "cpu_baseline": None,
             "e2e": None, "gpu_launches": launches, "clocks": clk,

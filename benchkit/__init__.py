@@ -114,6 +114,7 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons,
                 "power_w_max": max(pw) if pw else None,
+                "power_w_median": statistics.median(pw) if pw else None,
                 "samples": len(self.rows), "samples_under_load": len(load)}
 
 
