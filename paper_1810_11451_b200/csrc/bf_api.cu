@@ -284,33 +284,45 @@ __global__ void __launch_bounds__(1024) bf_route_small(const int32_t *__restrict
                                                        int32_t *__restrict__ offsets,
                                                        int32_t *__restrict__ err) {
     extern __shared__ int32_t cnt[];   // [32][G + 1], then tot[G + 1]
+    constexpr int kPer = kRouteSmallN / 1024;          // tags per lane, kept in registers
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nb = G + 1;
     int32_t *tot = cnt + 32 * nb;
-    for (int e = threadIdx.x; e < 33 * nb; e += blockDim.x) cnt[e] = 0;
-    __syncthreads();
+    // every tag is loaded once, all loads in flight together (no dependent chain)
     const int per = ((n + 31) / 32 + 31) / 32 * 32;    // items per warp, multiple of 32
     const int ws = warp * per, we = min(n, ws + per);
+    int bins[kPer];
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+        const int i = ws + 32 * r + lane;
+        bins[r] = (32 * r < per && i < we) ? route_bin(__ldg(gidx + i), G) : -1;
+    }
+    for (int e = threadIdx.x; e < 33 * nb; e += blockDim.x) cnt[e] = 0;
+    __syncthreads();
     int32_t *mycnt = cnt + warp * nb;
     const unsigned lt = (1u << lane) - 1u;
     int bad = 0;
-    for (int base = ws; base < we; base += 32) {
-        const int i = base + lane;
-        const int b = i < we ? route_bin(__ldg(gidx + i), G) : -1;
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+        if (32 * r >= per) break;
+        const int b = bins[r];
         bad |= (b == G);
         const unsigned m = __match_any_sync(0xffffffffu, b);
         if (b >= 0 && (m & lt) == 0) mycnt[b] += __popc(m);
         __syncwarp();
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) *err = 1;
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) {     // prefix over warps, per bin
-        int32_t run = 0;
-        for (int w = 0; w < 32; ++w) {
-            const int32_t c = cnt[w * nb + b];
-            cnt[w * nb + b] = run;
-            run += c;
+    // per bin, exclusive prefix over the 32 warps: one warp per bin, lane = warp index
+    for (int b = warp; b < nb; b += 32) {
+        const int32_t c = cnt[lane * nb + b];
+        int32_t inc = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += u;
         }
-        tot[b] = run;
+        cnt[lane * nb + b] = inc - c;
+        if (lane == 31) tot[b] = inc;
     }
     __syncthreads();
     if (warp == 0) {                                          // exclusive scan over bins
@@ -333,11 +345,12 @@ __global__ void __launch_bounds__(1024) bf_route_small(const int32_t *__restrict
     if (threadIdx.x == 0) offsets[nb] = n;
     for (int e = threadIdx.x; e < 32 * nb; e += blockDim.x) cnt[e] += tot[e % nb];
     __syncthreads();
-    for (int base = ws; base < we; base += 32) {
-        const int i = base + lane;
-        const int b = i < we ? route_bin(__ldg(gidx + i), G) : -1;
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+        if (32 * r >= per) break;
+        const int b = bins[r];
         const unsigned m = __match_any_sync(0xffffffffu, b);
-        if (b >= 0) perm[mycnt[b] + __popc(m & lt)] = i;
+        if (b >= 0) perm[mycnt[b] + __popc(m & lt)] = ws + 32 * r + lane;
         __syncwarp();
         if (b >= 0 && (m & lt) == 0) mycnt[b] += __popc(m);
         __syncwarp();

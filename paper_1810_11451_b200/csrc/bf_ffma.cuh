@@ -152,7 +152,18 @@ __global__ void __launch_bounds__(kThreads, 4) bf_ffma_kernel(const KParams p) {
 
     // group of an item: walk the routing offsets (items are visited in increasing
     // order, so the walk is amortised O(1)); items past offsets[G] are invalid.
+    // The walk starts at begin's group, found by binary search (first g with
+    // offsets[g + 1] > begin), so a CTA late in the list does not chase G
+    // dependent global loads before its first block.
     int gi = 0;
+    if (p.offsets && t == 0) {
+        int lo = 0, hi = p.n_groups;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(p.offsets + mid + 1) > begin) hi = mid; else lo = mid + 1;
+        }
+        gi = lo;
+    }
     auto group_of = [&](int64_t item) -> int32_t {
         if (!p.offsets) return 0;
         while (gi < p.n_groups && item >= __ldg(p.offsets + gi + 1)) ++gi;

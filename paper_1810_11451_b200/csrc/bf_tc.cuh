@@ -22,15 +22,16 @@
 // over 3 x KP/8 MMAs stays near 2e-6 T at f = 36, inside the
 // 1e-5 T contract.
 //
-// One CTA (14 warps) per SM, persistent over a contiguous range of the
-// group-sorted block list; tiles are 2 consecutive blocks of the same group.
-//   warp 13    S producer: cp.async.bulk (TMA bulk engine) of each block's
-//              480 F contiguous bytes into a 4-stage shared-memory ring,
-//              completing on mbarriers, up to 4 tiles ahead of the split;
+// One CTA (14 warps) per SM, persistent over a cost-balanced range of the
+// group-sorted block list (cta_range); tiles are 2 consecutive blocks of one group.
+//   warp 13    producer: cp.async.bulk (TMA bulk engine) of each block's 480 F
+//              contiguous bytes into a 2-4-stage shared-memory ring, completing on
+//              mbarriers, up to kStages tiles ahead of the split; and the pre-split
+//              B image (W) of each group segment into one of two W buffers, so a
+//              group change does not stall the tensor pipe;
 //   warps 0-3  split: LDS S (conflict-free, one RE column per lane), split into
 //              3 tf32 terms, tcgen05.st into the A region (one TMEM lane per RE);
-//   warp 4     MMA issuer (one thread) and W loader (cp.async.bulk of the
-//              group's pre-split B image into SMEM on a group change);
+//   warp 4     MMA issuer (one thread);
 //   warps 5-12 epilogue (two per lane quarter, half the D columns each): tcgen05.ld of a whole D row (128 columns), release of
 //              the TMEM buffer, then stores of two adjacent REs per lane (lane
 //              pairs trade one shuffle) — 256 contiguous bytes per antenna row.
@@ -50,7 +51,10 @@ constexpr int kMmaWarp = 4;
 constexpr int kEpiWarp0 = 5;
 constexpr int kEpiWarps = 8;          // two per TMEM lane quarter, 64 D columns each
 constexpr int kProdWarp = 13;
-constexpr int kMaxStages = 4;          // S ring depth (tiles), shared memory permitting
+#ifndef BFTC_MAX_STAGES
+#define BFTC_MAX_STAGES 4
+#endif
+constexpr int kMaxStages = BFTC_MAX_STAGES;   // S ring depth (tiles), shared memory permitting
 constexpr int kSmemLimit = 232448;     // 227 KB per CTA
 constexpr int kDCol0 = 256;
 constexpr int kMinSmem = 120 * 1024;   // forces one CTA (and one TMEM owner) per SM
@@ -75,15 +79,18 @@ struct TcSmem {
     static constexpr int KP = kp_of(F);
     static constexpr int kWBytes = 2 * KP * 128 * 4;   // W1 tf32 image + bf16 correction image
     static constexpr int kSBlock = 480 * F;            // one block of S
-    static constexpr int kFixed = kWBytes + 24 * 8 + 16 + 1028 * 4;
+    // two W buffers: the producer prefetches the next group's image while the
+    // current group's MMAs run (a reload no longer drains the tensor pipe)
+    static constexpr int kFixed = 2 * kWBytes + 24 * 8 + 16 + 1028 * 4 + 24;
     static constexpr int kStagesFit = (kSmemLimit - kFixed) / (2 * kSBlock);
     static constexpr int kStages = kStagesFit < kMaxStages ? kStagesFit : kMaxStages;
     static_assert(kStages >= 2, "S ring needs two stages");
-    static constexpr int kOffS = kWBytes;              // kStages x 2 blocks
+    static constexpr int kOffS = 2 * kWBytes;          // kStages x 2 blocks
     static constexpr int kOffBar = kOffS + kStages * 2 * kSBlock;   // 24 mbarrier slots
     static constexpr int kOffTmem = kOffBar + 24 * 8;
     static constexpr int kOffOffs = kOffTmem + 16;     // group offsets (<= 1026 ints)
-    static constexpr int kBytesUsed = kOffOffs + 1028 * 4;
+    static constexpr int kOffRange = kOffOffs + 1028 * 4;   // this CTA's [begin, end)
+    static constexpr int kBytesUsed = kOffRange + 24;
     static constexpr int kBytes = kBytesUsed > kMinSmem ? kBytesUsed : kMinSmem;
 };
 
@@ -122,6 +129,79 @@ struct TileIter {
     }
 };
 
+// Cost-balanced split of the group-sorted item list over the CTAs.  Work is
+// counted in tiles (2 blocks of one group; a group of m blocks is ceil(m / 2)
+// tiles) plus a W reload per group segment (kWCost quarter-tiles, ~half a tile:
+// the MMA issuer drains and reloads the group's B image), so a CTA whose range
+// crosses group boundaries gets fewer tiles; an item-count split would make those
+// CTAs, and with them the launch, slower (short launches: c5's 4096-block chunks).
+// Boundaries fall on tile starts (group start + even offset); position x of the
+// cost axis maps to an item monotonically, so adjacent CTAs share their boundary.
+// Pure integer function of the offsets: results do not depend on it (a D row only
+// depends on its own A row), only the timing does.
+constexpr int64_t kTileCost = 4, kWCost = 2;
+
+// item where cost position x falls inside group g (x_in = x - cost before g)
+__device__ __forceinline__ int64_t item_at(const int32_t *offs, int g, int64_t x_in) {
+    const int64_t m = offs[g + 1] - offs[g], r = x_in - kWCost;
+    if (r <= 0) return offs[g];
+    return offs[g] + min(m, 2 * ((r + kTileCost - 1) / kTileCost));
+}
+
+// One warp computes this CTA's [begin, end) (lanes scan 32 groups at a time).
+__device__ __forceinline__ void cta_range(const int32_t *offs, int G, int64_t n, int lane,
+                                          int64_t &begin, int64_t &end, int &g_begin) {
+    g_begin = 0;
+    const int64_t bid = blockIdx.x, grid = gridDim.x;
+    if (!offs) {
+        const int64_t tot = kTileCost * ((n + 1) / 2);
+        begin = min(n, 2 * ((tot * bid / grid + kTileCost - 1) / kTileCost));
+        end = bid + 1 == grid ? n : min(n, 2 * ((tot * (bid + 1) / grid + kTileCost - 1) / kTileCost));
+        return;
+    }
+    auto cost = [&](int g) -> int64_t {
+        if (g >= G) return 0;
+        const int64_t m = offs[g + 1] - offs[g];
+        return m > 0 ? kWCost + kTileCost * ((m + 1) / 2) : 0;
+    };
+    int64_t tot = 0;
+    for (int base = 0; base < G; base += 32) {
+        int64_t c = cost(base + lane);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        tot += c;
+    }
+    const int64_t xb = tot * bid / grid, xe = tot * (bid + 1) / grid;
+    begin = n;
+    end = n;
+    bool fb = false, fe = bid + 1 == grid;
+    int64_t carry = 0;
+    for (int base = 0; base < G && !(fb && fe); base += 32) {
+        const int g = base + lane;
+        const int64_t c = cost(g);
+        int64_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        incl += carry;
+        const int64_t excl = incl - c;
+        const bool hb = !fb && c > 0 && xb >= excl && xb < incl;
+        const bool he = !fe && c > 0 && xe >= excl && xe < incl;
+        const int64_t ib = hb ? item_at(offs, g, xb - excl) : 0;
+        const int64_t ie = he ? item_at(offs, g, xe - excl) : 0;
+        const unsigned mb = __ballot_sync(0xffffffffu, hb), me = __ballot_sync(0xffffffffu, he);
+        if (mb) {
+            begin = __shfl_sync(0xffffffffu, ib, __ffs(mb) - 1);
+            g_begin = base + __ffs(mb) - 1;
+            fb = true;
+        }
+        if (me) { end = __shfl_sync(0xffffffffu, ie, __ffs(me) - 1); fe = true; }
+        carry = __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
 // Named barrier 1 over the 4 epilogue warps (128 threads).
 __device__ __forceinline__ void epi_bar_sync() {
     asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -152,16 +232,28 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::kOffBar);
     // a_full[t] / a_free[t]: TMEM A region of split term t (0: S1, 1: S2, 2: S3)
     uint64_t *bar_a_full = bars + 0, *bar_a_free = bars + 3, *bar_d_full = bars + 6,
-             *bar_d_free = bars + 8, *bar_w = bars + 10, *bar_s_full = bars + 11,
-             *bar_s_empty = bars + 11 + L::kStages;
+             *bar_d_free = bars + 8, *bar_wfull = bars + 10, *bar_wfree = bars + 12,
+             *bar_s_full = bars + 14, *bar_s_empty = bars + 14 + L::kStages;
     float *Ss = reinterpret_cast<float *>(smem + L::kOffS);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L::kOffTmem);
     int32_t *soffs = reinterpret_cast<int32_t *>(smem + L::kOffOffs);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t n = p.n_items;
-    const int64_t begin = n * blockIdx.x / gridDim.x;
-    const int64_t end = n * (blockIdx.x + 1) / gridDim.x;
+    if (p.offsets)
+        for (int i = threadIdx.x; i < p.n_groups + 2; i += blockDim.x) soffs[i] = p.offsets[i];
+    __syncthreads();
+    const int32_t *offs = p.offsets ? soffs : nullptr;
+    int64_t *srange = reinterpret_cast<int64_t *>(smem + L::kOffRange);
+    if (warp == 0) {
+        int64_t b0, e0;
+        int g0;
+        cta_range(offs, p.n_groups, n, lane, b0, e0, g0);
+        if (lane == 0) { srange[0] = b0; srange[1] = e0; srange[2] = g0; }
+    }
+    __syncthreads();
+    const int64_t begin = srange[0], end = srange[1];
+    const int g_begin = (int)srange[2];   // every role's walk starts in begin's group
     if (begin >= end) return;   // CTA-uniform, before any TMEM allocation
 
     if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
@@ -174,20 +266,21 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
         bfk::mbar_init(bar_d_full + 1, 1);
         bfk::mbar_init(bar_d_free + 0, 32 * kEpiWarps);
         bfk::mbar_init(bar_d_free + 1, 32 * kEpiWarps);
-        bfk::mbar_init(bar_w, 1);
+        for (int i = 0; i < 2; ++i) {
+            bfk::mbar_init(bar_wfull + i, 1);
+            bfk::mbar_init(bar_wfree + i, 1);
+        }
         for (int i = 0; i < L::kStages; ++i) {
             bfk::mbar_init(bar_s_full + i, 1);
             bfk::mbar_init(bar_s_empty + i, 128);
         }
         bfk::mbar_fence_init();
     }
-    if (p.offsets)
-        for (int i = threadIdx.x; i < p.n_groups + 2; i += blockDim.x) soffs[i] = p.offsets[i];
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = *tmem_slot;
-    TileIter it{p.offsets ? soffs : nullptr, p.n_groups, 0, begin, end};
+    TileIter it{offs, p.n_groups, g_begin, begin, end};
     Tile tl;
 
     if (warp < kSplitWarps) {
@@ -281,7 +374,12 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
         }
     } else if (warp == kProdWarp) {
         // ------------------------------------------------------------ S producer (TMA bulk)
+        // It also loads each group segment's B image (W) into W buffer (segment & 1)
+        // as it reaches the segment's first tile — up to kStages tiles ahead of the
+        // MMAs — once the segment two back has released that buffer (wfree).
         const uint64_t pol = bfk::policy_evict_first();
+        int cur_g = -1;
+        int64_t seg = -1;
         bool have = it.next(tl);
         int64_t blk0 = have ? block_of(p, tl.item) : 0;
         int64_t blk1 = have && tl.cnt > 1 ? block_of(p, tl.item + 1) : 0;
@@ -291,6 +389,18 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
             const int64_t nb0 = have_nx ? block_of(p, nx.item) : 0;
             const int64_t nb1 = have_nx && nx.cnt > 1 ? block_of(p, nx.item + 1) : 0;
             const int stage = (int)(t % L::kStages);
+            if (tl.g != cur_g) {
+                cur_g = tl.g;
+                ++seg;
+                const int wb = (int)(seg & 1);
+                if (seg >= 2) bfk::mbar_wait(bar_wfree + wb, (uint32_t)(((seg >> 1) - 1) & 1));
+                if (lane == 0) {
+                    bfk::mbar_arrive_expect_tx(bar_wfull + wb, L::kWBytes);
+                    bfk::bulk_g2s(Wsm + wb * (L::kWBytes / 4), p.Wimg + (int64_t)tl.g * (L::kWBytes / 4),
+                                  L::kWBytes, bar_wfull + wb, bfk::policy_evict_last());
+                }
+                __syncwarp();
+            }
             bfk::mbar_wait(bar_s_empty + stage, (uint32_t)(((t / L::kStages) & 1) ^ 1));
             if (DBG & 8) {
                 if (lane == 0) mbar_arrive(bar_s_full + stage);
@@ -312,22 +422,21 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------------------ MMA issuer
         int cur_g = -1;
-        uint32_t wphase = 0;
+        int64_t seg = -1;
         constexpr uint32_t idesc = tc::idesc_tf32(128, 128);
         constexpr uint32_t idesc_c = tc::idesc_bf16(128, 128);
-        const uint32_t w_base = tc::smem_u32(Wsm);
+        uint32_t w_base = tc::smem_u32(Wsm);
         bool exact = false;
         for (int64_t t = 0; it.next(tl); ++t) {
-            if (tl.g != cur_g) {   // old W is no longer read once tile t-1's last MMAs completed
+            if (tl.g != cur_g) {   // new group segment: its W was prefetched by the producer
                 exact = __ldg(p.wexact + tl.g) != 0;
-                if (t > 0) bfk::mbar_wait(bar_a_free + 0, (uint32_t)((t - 1) & 1));
-                if (lane == 0) {
-                    bfk::mbar_arrive_expect_tx(bar_w, L::kWBytes);
-                    bfk::bulk_g2s(Wsm, p.Wimg + (int64_t)tl.g * (L::kWBytes / 4), L::kWBytes, bar_w,
-                                  bfk::policy_evict_last());
-                }
-                bfk::mbar_wait(bar_w, wphase);
-                wphase ^= 1u;
+                // the previous segment's buffer is free once every MMA issued so far completed
+                if (seg >= 0 && lane == 0) tc::mma_commit(bar_wfree + (int)(seg & 1));
+                __syncwarp();
+                ++seg;
+                const int wb = (int)(seg & 1);
+                bfk::mbar_wait(bar_wfull + wb, (uint32_t)((seg >> 1) & 1));
+                w_base = tc::smem_u32(Wsm + wb * (L::kWBytes / 4));
                 cur_g = tl.g;
             }
             const int b = (int)(t & 1);

@@ -512,3 +512,33 @@ def test_sm_share_concurrent_plans_bitwise(variant):
         plans[0].set_sm_share(-1)
     for p in plans:
         p.close()
+
+
+@pytest.mark.parametrize("n,G,share", [(1, 1, 0), (3, 55, 0), (7, 5, 3), (150, 55, 0), (301, 1024, 0),
+                                       (4096, 55, 146), (4097, 2, 7), (5000, 300, 148)])
+def test_cost_balanced_partition_covers_every_block(n, G, share):
+    """The tensor kernel splits the group-sorted list over CTAs by tiles + W reloads: every
+    valid block is written exactly as by a single-CTA launch (empty groups, one-block groups,
+    more CTAs than tiles, many groups)."""
+    f = 12
+    ids = np.arange(n)
+    W = syn.precoders(7, G, G, 64, f, "unit_columns")
+    S = syn.qam_symbols(7, G, ids, f, 60, 16)
+    tags = syn.subband_tags(7, ids, G)
+    if G > 3:
+        tags[tags % 3 == 1] = 0          # leave some groups empty, make group 0 large
+    Sd, td = torch.from_numpy(S).to(DEV), torch.from_numpy(tags).to(DEV)
+    outs = []
+    for sh in (share, 1):
+        plan = Plan(f=f, variant=Variant.TENSOR)
+        plan.set_precoders(torch.from_numpy(W).to(DEV))
+        plan.set_sm_share(sh)
+        R = torch.full((n, 64, 60), float("nan"), dtype=torch.complex64, device=DEV)
+        plan.apply(Sd, td, out=R)
+        torch.cuda.synchronize()
+        outs.append(R.cpu().numpy())
+        plan.close()
+    assert np.isfinite(outs[0].view(np.float32)).all()
+    assert_bitwise(outs[0], outs[1], f"n={n} G={G} share={share}")
+    R_ref, T, _ = oracle.beamform(W, S, tags, n_threads=NT)
+    assert_parity(outs[0], R_ref, T, what=f"partition n={n} G={G}")

@@ -3,7 +3,7 @@ sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."
 import torch
 import benchkit
 HERE = os.path.dirname(os.path.abspath(__file__))
-L = ctypes.CDLL(os.path.join(HERE, "libtcexp.so"))
+L = ctypes.CDLL(os.path.join(HERE, os.environ.get("TCX_LIB", "libtcexp.so")))
 L.tcx_run.restype = ctypes.c_float
 L.tcx_run.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 100000
