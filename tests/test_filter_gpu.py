@@ -134,3 +134,22 @@ def test_filter_error_paths():
     assert st == bf.Status.MISALIGNED
     assert L.bff_apply(plan._h, None, None, 0, None) == bf.Status.OK
     plan.close()
+
+
+@pytest.mark.parametrize("n_sig", [1, 149, 600])
+def test_filter_no_write_outside_y(n_sig):
+    """Out-of-bounds write check (compute-sanitizer is closed on this pool): y sits between
+    guard bands of a sentinel pattern that must survive; every word of y is written."""
+    guard = 2048
+    plan = FilterPlan()
+    plan.set_taps(torch.from_numpy(syn.filter_taps()).to(DEV))
+    s = torch.from_numpy(syn.filter_signals(8, 0, np.arange(n_sig))).to(DEV)
+    words = n_sig * 2048 * 2
+    buf = torch.full((guard + words + guard,), 0x7FC0DEAD, dtype=torch.int32, device=DEV)
+    y = buf[guard:guard + words].view(torch.complex64).view(n_sig, 2048)
+    plan.apply(s, out=y)
+    torch.cuda.synchronize()
+    h = buf.cpu().numpy()
+    assert (h[:guard] == 0x7FC0DEAD).all() and (h[guard + words:] == 0x7FC0DEAD).all()
+    assert not (h[guard:guard + words] == 0x7FC0DEAD).any()
+    plan.close()

@@ -542,3 +542,29 @@ def test_cost_balanced_partition_covers_every_block(n, G, share):
     assert_bitwise(outs[0], outs[1], f"n={n} G={G} share={share}")
     R_ref, T, _ = oracle.beamform(W, S, tags, n_threads=NT)
     assert_parity(outs[0], R_ref, T, what=f"partition n={n} G={G}")
+
+
+@pytest.mark.parametrize("layout", [Layout.INTERLEAVED, Layout.PLANAR, Layout.INTERLEAVED_F16OUT])
+@pytest.mark.parametrize("f", [1, 7, 36])
+def test_no_write_outside_R(f, layout, variant):
+    """Out-of-bounds write check (compute-sanitizer is closed on this pool): R is a slice of
+    a larger buffer whose guard bands hold a sentinel pattern; after tagged and untagged
+    applies at ragged sizes the guards are untouched, and every byte of R was written."""
+    n, guard = 333, 4096
+    W = syn.precoders(11, f, 5, 64, f, "unit_columns")
+    S = syn.qam_symbols(11, f, np.arange(n), f, 60, 16)
+    tags = syn.subband_tags(11, np.arange(n), 5)
+    plan = Plan(f=f, layout=layout, variant=variant)
+    Wd = torch.from_numpy(syn.to_planar(W) if layout == Layout.PLANAR else W).to(DEV)
+    Sd = torch.from_numpy(syn.to_planar(S) if layout == Layout.PLANAR else S).to(DEV)
+    plan.set_precoders(Wd)
+    r_words = int(np.prod(plan.r_shape(n))) * torch.empty((), dtype=plan.r_dtype).element_size() // 4
+    for td in (None, torch.from_numpy(tags).to(DEV)):
+        buf = torch.full((guard + r_words + guard,), 0x7FC0DEAD, dtype=torch.int32, device=DEV)
+        R = buf[guard:guard + r_words].view(plan.r_dtype).view(plan.r_shape(n))
+        plan.apply(Sd, td, out=R)
+        torch.cuda.synchronize()
+        h = buf.cpu().numpy()
+        assert (h[:guard] == 0x7FC0DEAD).all() and (h[guard + r_words:] == 0x7FC0DEAD).all()
+        assert not (h[guard:guard + r_words] == 0x7FC0DEAD).any(), "R not fully written"
+    plan.close()

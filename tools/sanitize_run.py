@@ -51,6 +51,24 @@ def main():
         plan.apply_host(torch.from_numpy(S).pin_memory(), torch.from_numpy(tags).pin_memory(), Rh)
         torch.cuda.synchronize()
         plan.close()
+    # many groups, a share of the SMs (cost-balanced ranges, W double buffer, group walk)
+    ids = np.arange(700)
+    W = syn.precoders(3, 0, 300, 64, 12, "unit_columns")
+    S = syn.qam_symbols(3, 0, ids, 12, 60, 16)
+    tags = syn.subband_tags(3, ids, 300)
+    for variant in ("ffma", "tensor"):
+        plan = bf.Plan(f=12, variant=variant)
+        plan.set_sm_share(7)
+        plan.set_precoders(torch.from_numpy(W).cuda())
+        plan.apply(torch.from_numpy(S).cuda(), torch.from_numpy(tags).cuda())
+        torch.cuda.synchronize()
+        plan.close()
+    # the filter stage
+    fp = bf.FilterPlan()
+    fp.set_taps(torch.from_numpy(syn.filter_taps()).cuda())
+    fp.apply(torch.from_numpy(syn.filter_signals(5, 0, np.arange(3))).cuda())
+    torch.cuda.synchronize()
+    fp.close()
     p0 = bf.Plan(f=0)
     p0.set_precoders(torch.zeros((1, 64, 0), dtype=torch.complex64, device="cuda"))
     p0.apply(torch.zeros((5, 0, 60), dtype=torch.complex64, device="cuda"))
