@@ -50,6 +50,8 @@ def parse():
                     help="target CPU work of the oracle baseline sample")
     ap.add_argument("--c5-chunks", type=int, default=0, help="c5: chunks per step (0 = all 2048)")
     ap.add_argument("--no-graph", action="store_true", help="c5: launch eagerly, no CUDA graph")
+    ap.add_argument("--c5-batch", type=int, default=8,
+                    help="c5: consecutive chunks per bf_apply_batch launch (1 = one bf_apply_routed per chunk)")
     return ap.parse_args()
 
 
@@ -550,11 +552,12 @@ def run_c5(args, wl, world, rank, local, dev):
         pl.set_sm_share(sms - route_sms)
     # S (and tags) of every chunk of this rank are generated up front and stay resident
     # in HBM (74.5 GB at N = 1), so the timed region holds only the method: per chunk,
-    # the routing (bf_route, on the "route" stream) and the beamforming kernel
-    # (bf_apply_routed).  R (257.7 GB in total) cannot stay resident: chunks write a
-    # 4-slot ring.  Chunk c applies on stream c % 2; consecutive chunks belong to
-    # different cells (plans), so one chunk's tail overlaps the next one's head while
-    # every plan stays on one stream.
+    # the routing (bf_route, on the "route" stream) and the beamforming.  Chunks are
+    # beamformed in windows of B consecutive chunks (--c5-batch, default 8: one chunk of
+    # each cell), one bf_apply_batch launch per window, so the tensor kernel's fill and
+    # drain is paid once per window; B = 1 is one bf_apply_routed per chunk.  R (257.7 GB
+    # in total) cannot stay resident: windows write a 4-slot ring.  Window w applies on
+    # stream w % 2, so one window's tail overlaps the next one's head.
     NSLOT = 4
     chunk_f = [int(fc[c % n_cells]) for c in range(n_chunks)]
     s_off = np.concatenate([[0], np.cumsum([nloc * f * 60 for f in chunk_f])]).astype(np.int64)
@@ -566,12 +569,16 @@ def run_c5(args, wl, world, rank, local, dev):
         sync.gen_symbols(Sv, wl.seed, 0, chunk_f[c], 60, 0, first=first)
         sync.gen_tags(T_all[c, :cnt], wl.seed, wl.n_groups, first=first)
     torch.cuda.synchronize()
-    P_ring = [torch.empty(nloc, dtype=torch.int32, device=dev) for _ in range(NSLOT)]
-    O_ring = [torch.empty(wl.n_groups + 2, dtype=torch.int32, device=dev) for _ in range(NSLOT)]
-    route_plans = [bf.Plan(f=int(fc[c]), variant=args.variant) for c in range(NSLOT)]
-    for rp in route_plans:         # routing needs only the precoder count
-        rp.set_precoders(torch.zeros((wl.n_groups, 64, rp.f), dtype=torch.complex64, device=dev))
-    R_ring = [torch.empty((nloc, 64, 60), dtype=torch.complex64, device=dev) for _ in range(NSLOT)]
+    B = max(1, args.c5_batch)                # chunks per bf_apply_batch launch (window)
+    n_win = (n_chunks + B - 1) // B
+    P_ring = [[torch.empty(nloc, dtype=torch.int32, device=dev) for _ in range(B)] for _ in range(NSLOT)]
+    O_ring = [[torch.empty(wl.n_groups + 2, dtype=torch.int32, device=dev) for _ in range(B)]
+              for _ in range(NSLOT)]
+    route_plan = bf.Plan(f=1, variant=args.variant)   # routing needs only the precoder count
+    route_plan.set_precoders(torch.zeros((wl.n_groups, 64, 1), dtype=torch.complex64, device=dev))
+    route_plans = [route_plan]
+    R_ring = [[torch.empty((nloc, 64, 60), dtype=torch.complex64, device=dev) for _ in range(B)]
+              for _ in range(NSLOT)]
     rstream = torch.cuda.Stream(device=dev)
     side = torch.cuda.Stream(device=dev)
     main = torch.cuda.current_stream()
@@ -585,18 +592,26 @@ def run_c5(args, wl, world, rank, local, dev):
         side.wait_event(ev_fork)
         for s_ in range(NSLOT):
             ev_use[s_].record(main)
-        for c in range(n_chunks):
-            s, cell = c % NSLOT, c % n_cells
-            ap = main if c % 2 == 0 else side
-            f = chunk_f[c]
-            _, cnt = shard.chunk_shard(c, chunk, rank, world)
-            Sv = S_all[int(s_off[c]):int(s_off[c]) + cnt * f * 60].view(cnt, f, 60)
+        for w in range(n_win):
+            s = w % NSLOT
+            ap = main if w % 2 == 0 else side
+            jobs = []
             with torch.cuda.stream(rstream):
                 rstream.wait_event(ev_use[s])
-                route_plans[s].route_into(T_all[c, :cnt], P_ring[s][:cnt], O_ring[s])
+                for i, c in enumerate(range(w * B, min((w + 1) * B, n_chunks))):
+                    f = chunk_f[c]
+                    _, cnt = shard.chunk_shard(c, chunk, rank, world)
+                    Sv = S_all[int(s_off[c]):int(s_off[c]) + cnt * f * 60].view(cnt, f, 60)
+                    route_plan.route_into(T_all[c, :cnt], P_ring[s][i][:cnt], O_ring[s][i])
+                    jobs.append((plans[c % n_cells], Sv, P_ring[s][i][:cnt], O_ring[s][i],
+                                 R_ring[s][i][:cnt]))
                 ev_rt[s].record(rstream)
             ap.wait_event(ev_rt[s])
-            plans[cell].apply_routed(Sv, P_ring[s][:cnt], O_ring[s], out=R_ring[s][:cnt], stream=ap)
+            if B == 1:
+                pl, Sv, pm, of, Rv = jobs[0]
+                pl.apply_routed(Sv, pm, of, out=Rv, stream=ap)
+            else:
+                bf.apply_batch(jobs, stream=ap)
             ev_use[s].record(ap)
         ev_join.record(side)                # join the side streams back into main
         main.wait_event(ev_join)
@@ -692,6 +707,7 @@ def run_c5(args, wl, world, rank, local, dev):
                        "l2": "S resident (74.5 GB at N=1, >> L2); R streamed through a 4-slot ring",
                        "gpu": torch.cuda.get_device_name(dev), "w_broadcast_ms": t_bc * 1e3,
                        "launch_mode": mode, "apply_streams": 2, "ring_slots": NSLOT,
+                       "chunks_per_launch": B, "launches_per_step": n_win,
                        "apply_sms": sms - route_sms, "route_sms": route_sms,
                        },
             "flops_per_s": flops_all / (elapsed_ms * 1e-3), "roofline": roof, "cpu_baseline": None,

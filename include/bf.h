@@ -155,6 +155,34 @@ bf_status bf_apply_routed(bf_plan_t p, const void *S_dev, const int32_t *perm_de
                           const int32_t *offsets_dev, void *R_dev, int64_t n_blocks,
                           void *stream);
 
+/* One job of bf_apply_batch: bf_apply_routed(plan, S_dev, perm_dev, offsets_dev,
+ * R_dev, n_blocks) — the same arguments with the same rules (alignment, R not
+ * overlapping S, perm / offsets from bf_route or both NULL). */
+typedef struct {
+    bf_plan_t plan;
+    const void *S_dev;
+    const int32_t *perm_dev;
+    const int32_t *offsets_dev;
+    void *R_dev;
+    int64_t n_blocks;
+} bf_batch_job;
+
+/* Many routed applies in one kernel launch ("many products W x S", PAPER.md:84,
+ * over several precoder sets at once, e.g. consecutive streaming chunks of
+ * different cells).  Equivalent to calling
+ * bf_apply_routed for jobs[0..n_jobs) in order on `stream`, with bitwise equal
+ * results; the tensor-core jobs are packed into launches of up to 16 jobs (each
+ * job split over every CTA, so one kernel fill and drain is paid per pack instead
+ * of per job).  f = 0 jobs and plans forced to BF_VARIANT_FFMA run as their own
+ * applies.  Every plan must live on one device and share job 0's layout; the
+ * grid follows job 0's plan (bf_plan_set_sm_share), and its profiling record and
+ * launch count take the packed launches.  Every job is validated before anything
+ * is enqueued (BF_ERR_INVALID_VALUE / BF_ERR_MISALIGNED naming the job); a tagged
+ * job whose plan has more than 1026 groups is BF_ERR_UNSUPPORTED.  n_jobs == 0 is a
+ * no-op.  Jobs may share a plan (read-only), but a job's R must not overlap
+ * another job's S or R (precondition, not checked). */
+bf_status bf_apply_batch(const bf_batch_job *jobs, int n_jobs, void *stream);
+
 /* Free the plan and everything it owns.  Call after its work has drained. */
 bf_status bf_destroy(bf_plan_t p);
 

@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libbf.so")
 
 # every symbol include/bf.h declares (tests check the .so exports all of them)
 EXPORTS = ("bf_plan_create", "bf_set_precoders", "bf_apply", "bf_apply_host", "bf_route",
-           "bf_apply_routed",
+           "bf_apply_routed", "bf_apply_batch",
            "bf_destroy", "bf_plan_set_profiling", "bf_plan_kernel_time",
            "bf_plan_launch_count", "bf_plan_set_host_chunk", "bf_plan_kernel_config",
            "bf_plan_set_variant", "bf_plan_get_variant", "bf_plan_set_sm_share",
@@ -45,6 +45,13 @@ class Variant(enum.IntEnum):
     TENSOR = 2
 
 
+class BatchJob(ctypes.Structure):
+    """bf_batch_job (include/bf.h)."""
+    _fields_ = [("plan", ctypes.c_void_p), ("S_dev", ctypes.c_void_p),
+                ("perm_dev", ctypes.c_void_p), ("offsets_dev", ctypes.c_void_p),
+                ("R_dev", ctypes.c_void_p), ("n_blocks", ctypes.c_int64)]
+
+
 class BfError(RuntimeError):
     def __init__(self, status: int, detail: str):
         self.status = Status(status)
@@ -71,6 +78,7 @@ def lib() -> ctypes.CDLL:
         "bf_apply_host": (i32, [vp, vp, vp, vp, i64, vp]),
         "bf_route": (i32, [vp, vp, i64, vp, vp, vp]),
         "bf_apply_routed": (i32, [vp, vp, vp, vp, vp, i64, vp]),
+        "bf_apply_batch": (i32, [P(BatchJob), i32, vp]),
         "bf_destroy": (i32, [vp]),
         "bf_plan_set_profiling": (i32, [vp, i32]),
         "bf_plan_kernel_time": (i32, [vp, P(ctypes.c_double), P(i64)]),

@@ -58,6 +58,7 @@ void init_table() {
     bf_register_f19_24(g_table, g_table_tc);
     bf_register_f25_30(g_table, g_table_tc);
     bf_register_f31_36(g_table, g_table_tc);
+    bf_register_batch(g_table_tc);
 }
 
 // ---------------------------------------------------------------------------
@@ -479,6 +480,37 @@ int grid_for(bf_plan_t p, int64_t n_items, bool tensor) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(n_items, cap));
 }
 
+// CUDA events around a plan's beamforming kernel when profiling is on (bench.py).
+bf_status prof_begin(bf_plan_t p, cudaStream_t st, cudaEvent_t *e1) {
+    *e1 = nullptr;
+    if (!p->profiling || p->prof_used >= kMaxProfEvents) return BF_OK;
+    if (p->prof_used == p->prof_events.size()) {
+        cudaEvent_t a, b;
+        BF_CUDA(cudaEventCreate(&a));
+        BF_CUDA(cudaEventCreate(&b));
+        p->prof_events.emplace_back(a, b);
+    }
+    BF_CUDA(cudaEventRecord(p->prof_events[p->prof_used].first, st));
+    *e1 = p->prof_events[p->prof_used].second;
+    ++p->prof_used;
+    return BF_OK;
+}
+
+bftc::TcJob tc_job(bf_plan_t p, const void *S, const int32_t *perm, const int32_t *offsets,
+                   void *R, int64_t n) {
+    bftc::TcJob j{};
+    j.Wimg = p->Wimg;
+    j.S = static_cast<const float *>(S);
+    j.perm = perm;
+    j.offsets = offsets;
+    j.wexact = p->wexact;
+    j.R = static_cast<float *>(R);
+    j.n_items = n;
+    j.n_groups = p->n_groups;
+    j.f = p->f;
+    return j;
+}
+
 // Device-resident apply of routed blocks (validated arguments): perm / offsets
 // from route(), or both NULL for untagged blocks (all group 0).
 bf_status apply_routed(bf_plan_t p, const void *S, const int32_t *perm, const int32_t *offsets,
@@ -502,28 +534,10 @@ bf_status apply_routed(bf_plan_t p, const void *S, const int32_t *perm, const in
     const int grid = grid_for(p, n, tensor);
     const BfKernelEntry &kern = tensor ? p->kern_tc : p->kern;
     bftc::TcParams tp{};
-    tp.Wimg = p->Wimg;
-    tp.S = kp.S;
-    tp.perm = kp.perm;
-    tp.offsets = offsets;
-    tp.wexact = p->wexact;
-    tp.R = kp.R;
-    tp.n_items = n;
-    tp.n_groups = p->n_groups;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    const bool prof = p->profiling && p->prof_used < kMaxProfEvents;
-    if (prof) {
-        if (p->prof_used == p->prof_events.size()) {
-            cudaEvent_t a, b;
-            BF_CUDA(cudaEventCreate(&a));
-            BF_CUDA(cudaEventCreate(&b));
-            p->prof_events.emplace_back(a, b);
-        }
-        e0 = p->prof_events[p->prof_used].first;
-        e1 = p->prof_events[p->prof_used].second;
-        ++p->prof_used;
-        BF_CUDA(cudaEventRecord(e0, st));
-    }
+    tp.job[0] = tc_job(p, S, perm, offsets, R, n);
+    tp.n_jobs = 1;
+    cudaEvent_t e1;
+    if ((s = prof_begin(p, st, &e1)) != BF_OK) return s;
     void *args_ffma[] = {&kp};
     void *args_tc[] = {&tp};
     cudaError_t e = cudaLaunchKernel(kern.fn, dim3(grid),
@@ -531,7 +545,40 @@ bf_status apply_routed(bf_plan_t p, const void *S, const int32_t *perm, const in
                                      tensor ? args_tc : args_ffma, (size_t)kern.smem_bytes, st);
     if (e != cudaSuccess) return cuda_fail(e, "beamforming kernel launch");
     if ((s = launched(p, "beamforming kernel launch")) != BF_OK) return s;
-    if (prof) BF_CUDA(cudaEventRecord(e1, st));
+    if (e1) BF_CUDA(cudaEventRecord(e1, st));
+    return BF_OK;
+}
+
+// One launch of the runtime-f tensor kernel over up to kMaxJobs validated jobs of
+// tensor-variant plans (same device and layout); profiling / launch count on the
+// first job's plan.
+bf_status launch_batch(const bf_batch_job *jobs, int n, cudaStream_t st) {
+    bf_plan_t p0 = jobs[0].plan;
+    const BfKernelEntry &kern = g_table_tc[0][p0->layout];
+    static bool attr_set[64][3] = {};
+    if (!attr_set[p0->device & 63][p0->layout]) {
+        BF_CUDA(cudaFuncSetAttribute(kern.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kern.smem_bytes));
+        attr_set[p0->device & 63][p0->layout] = true;
+    }
+    bftc::TcParams tp{};
+    int64_t tiles = 0;
+    for (int i = 0; i < n; ++i) {
+        tp.job[i] = tc_job(jobs[i].plan, jobs[i].S_dev, jobs[i].perm_dev, jobs[i].offsets_dev,
+                           jobs[i].R_dev, jobs[i].n_blocks);
+        tiles += (jobs[i].n_blocks + 1) / 2;
+    }
+    tp.n_jobs = n;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, sms_used(p0)));
+    bf_status s;
+    cudaEvent_t e1;
+    if ((s = prof_begin(p0, st, &e1)) != BF_OK) return s;
+    void *args[] = {&tp};
+    cudaError_t e = cudaLaunchKernel(kern.fn, dim3(grid), dim3(bftc::kThreads), args,
+                                     (size_t)kern.smem_bytes, st);
+    if (e != cudaSuccess) return cuda_fail(e, "batched beamforming kernel launch");
+    if ((s = launched(p0, "batched beamforming kernel launch")) != BF_OK) return s;
+    if (e1) BF_CUDA(cudaEventRecord(e1, st));
     return BF_OK;
 }
 
@@ -754,6 +801,59 @@ bf_status bf_apply_routed(bf_plan_t p, const void *S_dev, const int32_t *perm_de
     DeviceGuard guard(p->device);
     return apply_routed(p, S_dev, perm_dev, offsets_dev, R_dev, n_blocks,
                         static_cast<cudaStream_t>(stream));
+}
+
+bf_status bf_apply_batch(const bf_batch_job *jobs, int n_jobs, void *stream) {
+    if (n_jobs < 0 || (n_jobs > 0 && !jobs)) return fail(BF_ERR_INVALID_VALUE, "bad job list");
+    if (n_jobs == 0) return BF_OK;
+    const bf_plan_t p0 = jobs[0].plan;
+    if (!p0) return fail(BF_ERR_INVALID_VALUE, "job 0: plan is NULL");
+    for (int i = 0; i < n_jobs; ++i) {   // every argument check before anything is enqueued
+        const bf_batch_job &jb = jobs[i];
+        bf_status s = validate_apply(jb.plan, jb.S_dev, jb.perm_dev, jb.R_dev, jb.n_blocks, true);
+        if (s != BF_OK) {
+            const std::string why = bfh::g_last_error;
+            return fail(s, "job %d: %s", i, why.c_str());
+        }
+        if (jb.plan->device != p0->device || jb.plan->layout != p0->layout)
+            return fail(BF_ERR_INVALID_VALUE, "job %d: every plan must share the device and layout "
+                                              "of job 0", i);
+        if ((jb.perm_dev == nullptr) != (jb.offsets_dev == nullptr))
+            return fail(BF_ERR_INVALID_VALUE, "job %d: perm and offsets must be given together", i);
+        if (jb.offsets_dev && !aligned(jb.offsets_dev, 4))
+            return fail(BF_ERR_MISALIGNED, "job %d: offsets misaligned", i);
+        if (jb.offsets_dev && jb.plan->n_groups + 2 > bftc::kOffsSlots)
+            return fail(BF_ERR_UNSUPPORTED, "job %d: n_groups=%d exceeds the batched kernel's %d",
+                        i, jb.plan->n_groups, bftc::kOffsSlots - 2);
+    }
+    DeviceGuard guard(p0->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // f == 0 and FFMA-variant jobs run as their own applies, in order; tensor jobs are
+    // packed into launches of at most kMaxJobs jobs and kOffsSlots group offsets.
+    bf_batch_job pack[bftc::kMaxJobs];
+    int np = 0, slots = 0;
+    bf_status s;
+    for (int i = 0; i <= n_jobs; ++i) {
+        const bool end = i == n_jobs;
+        const bf_batch_job *jb = end ? nullptr : &jobs[i];
+        const bool tc = !end && jb->n_blocks > 0 && jb->plan->f > 0 && use_tensor(jb->plan);
+        const int need = tc && jb->offsets_dev ? jb->plan->n_groups + 2 : 0;
+        if (np > 0 && (end || !tc || np == bftc::kMaxJobs || slots + need > bftc::kOffsSlots)) {
+            if ((s = launch_batch(pack, np, st)) != BF_OK) return s;
+            np = 0;
+            slots = 0;
+        }
+        if (end) break;
+        if (tc) {
+            pack[np++] = *jb;
+            slots += need;
+        } else if (jb->n_blocks > 0) {
+            if ((s = apply_routed(jb->plan, jb->S_dev, jb->perm_dev, jb->offsets_dev, jb->R_dev,
+                                  jb->n_blocks, st)) != BF_OK)
+                return s;
+        }
+    }
+    return BF_OK;
 }
 
 bf_status bf_apply_host(bf_plan_t p, const void *S_host, const int32_t *group_idx_host,

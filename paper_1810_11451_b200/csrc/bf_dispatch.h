@@ -9,6 +9,7 @@ struct BfKernelEntry {
 };
 
 using BfKernelTable = BfKernelEntry[37][3];   // [f][layout: interleaved, planar, f16 out]
+                                              // (tensor table f = 0: the batch kernel)
 
 void bf_register_f01_06(BfKernelTable &t, BfKernelTable &tc);
 void bf_register_f07_12(BfKernelTable &t, BfKernelTable &tc);
@@ -16,3 +17,4 @@ void bf_register_f13_18(BfKernelTable &t, BfKernelTable &tc);
 void bf_register_f19_24(BfKernelTable &t, BfKernelTable &tc);
 void bf_register_f25_30(BfKernelTable &t, BfKernelTable &tc);
 void bf_register_f31_36(BfKernelTable &t, BfKernelTable &tc);
+void bf_register_batch(BfKernelTable &tc);   // slot [0][layout]: runtime-f batch kernel

@@ -35,7 +35,8 @@
 //   warps 5-12 epilogue (two per lane quarter, half the D columns each): tcgen05.ld of a whole D row (128 columns), release of
 //              the TMEM buffer, then stores of two adjacent REs per lane (lane
 //              pairs trade one shuffle) — 256 contiguous bytes per antenna row.
-// TMEM: A terms at columns [0, 3 KP), D double buffer at [256, 384), [384, 512).
+// TMEM: A terms at columns [0, 3 KP) (KP of f = 36 for the batch kernel), D double buffer at
+// [256, 384), [384, 512).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -61,71 +62,124 @@ constexpr int kMinSmem = 120 * 1024;   // forces one CTA (and one TMEM owner) pe
 
 __host__ __device__ constexpr int kp_of(int F) { return (2 * F + 7) / 8 * 8; }
 
-struct TcParams {
+// One apply of a plan: blocks [0, n_items) of S -> R with the plan's precoders.
+// A launch processes a list of jobs (bf_apply: one; bf_apply_batch: up to
+// kMaxJobs, e.g. consecutive streaming chunks of different cells), each split
+// over all CTAs; the kernel template's F is the flow count of every job, or 0
+// for the batch kernel whose jobs carry their own f (1..36).
+constexpr int kMaxJobs = 16;
+constexpr int kOffsSlots = 1028;       // shared group-offset slots: sum over jobs of (n_groups + 2)
+
+struct TcJob {
     const float *Wimg;        // [n_groups][2][KP/4][16][8][4] floats (pre-split B image)
+    // Wimg per group: [W1 as tf32 core matrices (KP/4 K-chunks)] then
+    // [C = (W1 ; W2) as bf16 core matrices (2 KP bf16 of K = KP/4 chunks of 16 B)]
     const float *S;
     const int32_t *perm;      // NULL = identity order
     const int32_t *offsets;   // [n_groups + 2] group starts of the sorted order, or NULL
     const int32_t *wexact;    // [n_groups] 1 if the group's W is exactly tf32 (W2 == 0)
-    // Wimg per group: [W1 as tf32 core matrices (KP/4 K-chunks)] then
-    // [C = (W1 ; W2) as bf16 core matrices (2 KP bf16 of K = KP/4 chunks of 16 B)]
     float *R;
     int64_t n_items;
     int n_groups;
+    int f;
+};
+
+struct TcParams {
+    TcJob job[kMaxJobs];
+    int n_jobs;
 };
 
 template <int F>
 struct TcSmem {
-    static constexpr int KP = kp_of(F);
+    static constexpr int FS = F > 0 ? F : 36;          // sizing flow count (36 for runtime f)
+    static constexpr int KP = kp_of(FS);
     static constexpr int kWBytes = 2 * KP * 128 * 4;   // W1 tf32 image + bf16 correction image
-    static constexpr int kSBlock = 480 * F;            // one block of S
+    static constexpr int kSBlock = 480 * FS;           // one block of S (slot stride)
     // two W buffers: the producer prefetches the next group's image while the
     // current group's MMAs run (a reload no longer drains the tensor pipe)
-    static constexpr int kFixed = 2 * kWBytes + 24 * 8 + 16 + 1028 * 4 + 24;
+    static constexpr int kJobBytes = kMaxJobs * 96;    // per-job context (JobCtx)
+    static constexpr int kFixed = 2 * kWBytes + 24 * 8 + 16 + kOffsSlots * 4 + kJobBytes;
     static constexpr int kStagesFit = (kSmemLimit - kFixed) / (2 * kSBlock);
     static constexpr int kStages = kStagesFit < kMaxStages ? kStagesFit : kMaxStages;
     static_assert(kStages >= 2, "S ring needs two stages");
     static constexpr int kOffS = 2 * kWBytes;          // kStages x 2 blocks
     static constexpr int kOffBar = kOffS + kStages * 2 * kSBlock;   // 24 mbarrier slots
     static constexpr int kOffTmem = kOffBar + 24 * 8;
-    static constexpr int kOffOffs = kOffTmem + 16;     // group offsets (<= 1026 ints)
-    static constexpr int kOffRange = kOffOffs + 1028 * 4;   // this CTA's [begin, end)
-    static constexpr int kBytesUsed = kOffRange + 24;
+    static constexpr int kOffJobs = kOffTmem + 16;     // JobCtx[kMaxJobs]
+    static constexpr int kOffOffs = kOffJobs + kJobBytes;   // group offsets of every job
+    static constexpr int kBytesUsed = kOffOffs + kOffsSlots * 4;
     static constexpr int kBytes = kBytesUsed > kMinSmem ? kBytesUsed : kMinSmem;
 };
+
+// A job as the roles see it (shared memory), with this CTA's share of it.
+struct JobCtx {
+    const float *Wimg, *S;
+    const int32_t *perm, *wexact;
+    float *R;
+    const int32_t *offs;      // shared copy of the job's offsets, or nullptr (untagged)
+    int64_t begin, end;       // this CTA's item range
+    int g_begin;              // group of begin
+    int n_groups, f, kp;
+    int wbytes;               // bytes of one group's B image
+    int pad_;
+};
+static_assert(sizeof(JobCtx) <= 96, "JobCtx slot");
 
 struct Tile {
     int64_t item;
     int cnt;      // 1 or 2 blocks
     int g;
+    int job;
 };
 
-__device__ __forceinline__ int64_t block_of(const TcParams &p, int64_t item) {
-    return p.perm ? (int64_t)__ldg(p.perm + item) : item;
+__device__ __forceinline__ int64_t block_of(const JobCtx &J, int64_t item) {
+    return J.perm ? (int64_t)__ldg(J.perm + item) : item;
 }
 
-// Walks a CTA's item range in tiles of up to 2 consecutive blocks of one group.
-// Groups come from the routing offsets copied to shared memory (no global loads
-// on the critical path); every role runs the same walk, so tile t is the same
-// tile everywhere.  Items with invalid tags sort last and are skipped.
+// Walks a CTA's item ranges, job after job, in tiles of up to 2 consecutive blocks
+// of one group.  Groups come from the routing offsets copied to shared memory (no
+// global loads on the critical path); every role runs the same walk, so tile t is
+// the same tile everywhere.  Items with invalid tags sort last and are skipped.
 struct TileIter {
-    const int32_t *offs;   // shared copy of offsets [G + 2], or nullptr (untagged)
+    const JobCtx *jobs;
+    int n_jobs;
+    int j;
+    const int32_t *offs;
     int G;
     int gi;
     int64_t item, end;
-    __device__ bool next(Tile &t) {
-        if (item >= end) return false;
-        int64_t gend = end;
-        if (offs) {
-            while (gi < G && item >= offs[gi + 1]) ++gi;
-            if (gi >= G) { item = end; return false; }
-            gend = min(end, (int64_t)offs[gi + 1]);
+    __device__ void enter(int jj) {
+        j = jj;
+        if (jj < n_jobs) {
+            offs = jobs[jj].offs;
+            G = jobs[jj].n_groups;
+            gi = jobs[jj].g_begin;
+            item = jobs[jj].begin;
+            end = jobs[jj].end;
         }
-        t.item = item;
-        t.g = offs ? gi : 0;
-        t.cnt = (item + 1 < gend) ? 2 : 1;
-        item += t.cnt;
-        return true;
+    }
+    __device__ bool next(Tile &t) {
+        while (j < n_jobs) {
+            if (item < end) {
+                int64_t gend = end;
+                bool ok = true;
+                if (offs) {
+                    while (gi < G && item >= offs[gi + 1]) ++gi;
+                    if (gi >= G) ok = false;
+                    else gend = min(end, (int64_t)offs[gi + 1]);
+                }
+                if (ok) {
+                    t.item = item;
+                    t.g = offs ? gi : 0;
+                    t.job = j;
+                    t.cnt = (item + 1 < gend) ? 2 : 1;
+                    item += t.cnt;
+                    return true;
+                }
+            }
+            enter(j + 1);
+        }
+        return false;
     }
 };
 
@@ -226,7 +280,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 template <int F, int LAYOUT, int DBG = 0>
 __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
     using L = TcSmem<F>;
-    constexpr int KP = L::KP;
+    // TMEM column stride of the three A regions: fixed across the jobs of a launch
+    // (the split of a job's first tile must not overlap the previous job's regions
+    // that its last MMAs may still read).
+    constexpr int kARegion = L::KP;
     extern __shared__ __align__(1024) unsigned char smem[];
     float *Wsm = reinterpret_cast<float *>(smem);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::kOffBar);
@@ -236,25 +293,52 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
              *bar_s_full = bars + 14, *bar_s_empty = bars + 14 + L::kStages;
     float *Ss = reinterpret_cast<float *>(smem + L::kOffS);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L::kOffTmem);
+    JobCtx *jobs = reinterpret_cast<JobCtx *>(smem + L::kOffJobs);
     int32_t *soffs = reinterpret_cast<int32_t *>(smem + L::kOffOffs);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t n = p.n_items;
-    if (p.offsets)
-        for (int i = threadIdx.x; i < p.n_groups + 2; i += blockDim.x) soffs[i] = p.offsets[i];
-    __syncthreads();
-    const int32_t *offs = p.offsets ? soffs : nullptr;
-    int64_t *srange = reinterpret_cast<int64_t *>(smem + L::kOffRange);
-    if (warp == 0) {
-        int64_t b0, e0;
-        int g0;
-        cta_range(offs, p.n_groups, n, lane, b0, e0, g0);
-        if (lane == 0) { srange[0] = b0; srange[1] = e0; srange[2] = g0; }
+    const int n_jobs = p.n_jobs;
+    // ---- prologue: jobs and their group offsets into shared memory, then this CTA's
+    //      cost-balanced range of every job (one warp each, shuffle scans).
+    if (threadIdx.x < n_jobs) {
+        const TcJob &q = p.job[threadIdx.x];
+        int base = 0;
+        for (int i = 0; i < (int)threadIdx.x; ++i)
+            if (p.job[i].offsets) base += p.job[i].n_groups + 2;
+        JobCtx &J = jobs[threadIdx.x];
+        J.Wimg = q.Wimg;
+        J.S = q.S;
+        J.perm = q.perm;
+        J.wexact = q.wexact;
+        J.R = q.R;
+        J.offs = q.offsets ? soffs + base : nullptr;
+        J.n_groups = q.n_groups;
+        J.f = F > 0 ? F : q.f;
+        J.kp = kp_of(J.f);
+        J.wbytes = 2 * J.kp * 128 * 4;
+        J.begin = J.end = 0;
+        J.g_begin = 0;
     }
     __syncthreads();
-    const int64_t begin = srange[0], end = srange[1];
-    const int g_begin = (int)srange[2];   // every role's walk starts in begin's group
-    if (begin >= end) return;   // CTA-uniform, before any TMEM allocation
+    for (int jj = 0; jj < n_jobs; ++jj)
+        if (jobs[jj].offs)
+            for (int i = threadIdx.x; i < jobs[jj].n_groups + 2; i += blockDim.x)
+                const_cast<int32_t *>(jobs[jj].offs)[i] = p.job[jj].offsets[i];
+    __syncthreads();
+    for (int jj = warp; jj < n_jobs; jj += kThreads / 32) {
+        int64_t b0, e0;
+        int g0;
+        cta_range(jobs[jj].offs, jobs[jj].n_groups, p.job[jj].n_items, lane, b0, e0, g0);
+        if (lane == 0) {
+            jobs[jj].begin = b0;
+            jobs[jj].end = e0;
+            jobs[jj].g_begin = g0;
+        }
+    }
+    __syncthreads();
+    bool any = false;
+    for (int jj = 0; jj < n_jobs; ++jj) any |= jobs[jj].begin < jobs[jj].end;
+    if (!any) return;   // CTA-uniform, before any TMEM allocation
 
     if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
     if (threadIdx.x == 32) {
@@ -280,7 +364,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = *tmem_slot;
-    TileIter it{offs, p.n_groups, g_begin, begin, end};
+    TileIter it{jobs, n_jobs, 0, nullptr, 0, 0, 0, 0};
+    it.enter(0);
     Tile tl;
 
     if (warp < kSplitWarps) {
@@ -288,9 +373,12 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
         const int m = warp * 32 + lane;                  // TMEM lane == A row
         const int bsel = m >= 60 ? 1 : 0, j = m - 60 * bsel;
         const uint32_t a_lane = tmem + ((uint32_t)(warp * 32) << 16);
-        int cur_g = -1;
+        int cur_g = -1, cur_j = -1;
         bool cur_exact = false;
         for (int64_t t = 0; it.next(tl); ++t) {
+            const JobCtx &J = jobs[tl.job];
+            const int f = F > 0 ? F : J.f;
+            const int KP = F > 0 ? L::KP : J.kp;
             const bool valid = m < 120 && bsel < tl.cnt;
             const int stage = (int)(t % L::kStages);
             bfk::mbar_wait(bar_s_full + stage, (uint32_t)((t / L::kStages) & 1));
@@ -301,9 +389,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
             // ring for every term (cheap LDS) instead of being held in 2F registers.
             // tcgen05.st is warp-collective: every lane stores (invalid rows store 0).
             const uint32_t par = (uint32_t)((t & 1) ^ 1);
-            if (tl.g != cur_g) {
+            if (tl.g != cur_g || tl.job != cur_j) {
                 cur_g = tl.g;
-                cur_exact = __ldg(p.wexact + tl.g) != 0;
+                cur_j = tl.job;
+                cur_exact = __ldg(J.wexact + tl.g) != 0;
             }
 #pragma unroll
             for (int pass = 0; pass < 3; ++pass) {
@@ -322,14 +411,14 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
                     for (int q = 0; q < 4; ++q) {
                         const int k = c0 / 2 + q;
                         float re = 0.0f, im = 0.0f;
-                        if (k < F && valid) {
+                        if (k < f && valid) {
                             if (LAYOUT != 1) {
                                 const float2 v = reinterpret_cast<const float2 *>(Sb)[k * 60 + j];
                                 re = v.x;
                                 im = v.y;
                             } else {
                                 re = Sb[k * 60 + j];
-                                im = Sb[F * 60 + k * 60 + j];
+                                im = Sb[f * 60 + k * 60 + j];
                             }
                         }
                         x[2 * q] = re;
@@ -359,11 +448,11 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
                             w1[e] = tc::pack_bf16x2(s1a, s1b);
                         }
                         if constexpr (!(DBG & 4)) {
-                            tc::tmem_st4(a_lane + KP + c0 / 2, w2);
-                            tc::tmem_st4(a_lane + KP + KP / 2 + c0 / 2, w1);
+                            tc::tmem_st4(a_lane + kARegion + c0 / 2, w2);
+                            tc::tmem_st4(a_lane + kARegion + KP / 2 + c0 / 2, w1);
                         }
                     } else {
-                        if constexpr (!(DBG & 4)) tc::tmem_st8(a_lane + term * KP + c0, v);
+                        if constexpr (!(DBG & 4)) tc::tmem_st8(a_lane + term * kARegion + c0, v);
                     }
                 }
                 tc::tmem_st_wait();
@@ -378,26 +467,30 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
         // as it reaches the segment's first tile — up to kStages tiles ahead of the
         // MMAs — once the segment two back has released that buffer (wfree).
         const uint64_t pol = bfk::policy_evict_first();
-        int cur_g = -1;
+        int cur_g = -1, cur_j = -1;
         int64_t seg = -1;
         bool have = it.next(tl);
-        int64_t blk0 = have ? block_of(p, tl.item) : 0;
-        int64_t blk1 = have && tl.cnt > 1 ? block_of(p, tl.item + 1) : 0;
+        int64_t blk0 = have ? block_of(jobs[tl.job], tl.item) : 0;
+        int64_t blk1 = have && tl.cnt > 1 ? block_of(jobs[tl.job], tl.item + 1) : 0;
         for (int64_t t = 0; have; ++t) {
             Tile nx;                       // next tile's block ids load while we wait
             const bool have_nx = it.next(nx);
-            const int64_t nb0 = have_nx ? block_of(p, nx.item) : 0;
-            const int64_t nb1 = have_nx && nx.cnt > 1 ? block_of(p, nx.item + 1) : 0;
+            const int64_t nb0 = have_nx ? block_of(jobs[nx.job], nx.item) : 0;
+            const int64_t nb1 = have_nx && nx.cnt > 1 ? block_of(jobs[nx.job], nx.item + 1) : 0;
+            const JobCtx &J = jobs[tl.job];
+            const int f = F > 0 ? F : J.f;
             const int stage = (int)(t % L::kStages);
-            if (tl.g != cur_g) {
+            if (tl.g != cur_g || tl.job != cur_j) {
                 cur_g = tl.g;
+                cur_j = tl.job;
                 ++seg;
                 const int wb = (int)(seg & 1);
+                const int wbytes = F > 0 ? L::kWBytes : J.wbytes;
                 if (seg >= 2) bfk::mbar_wait(bar_wfree + wb, (uint32_t)(((seg >> 1) - 1) & 1));
                 if (lane == 0) {
-                    bfk::mbar_arrive_expect_tx(bar_wfull + wb, L::kWBytes);
-                    bfk::bulk_g2s(Wsm + wb * (L::kWBytes / 4), p.Wimg + (int64_t)tl.g * (L::kWBytes / 4),
-                                  L::kWBytes, bar_wfull + wb, bfk::policy_evict_last());
+                    bfk::mbar_arrive_expect_tx(bar_wfull + wb, (uint32_t)wbytes);
+                    bfk::bulk_g2s(Wsm + wb * (L::kWBytes / 4), J.Wimg + (int64_t)tl.g * (wbytes / 4),
+                                  (uint32_t)wbytes, bar_wfull + wb, bfk::policy_evict_last());
                 }
                 __syncwarp();
             }
@@ -405,13 +498,13 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
             if (DBG & 8) {
                 if (lane == 0) mbar_arrive(bar_s_full + stage);
             } else if (lane == 0) {
-                bfk::mbar_arrive_expect_tx(bar_s_full + stage, (uint32_t)(tl.cnt * L::kSBlock));
-                bfk::bulk_g2s(Ss + (stage * 2) * (L::kSBlock / 4), p.S + blk0 * (int64_t)(120 * F),
-                              L::kSBlock, bar_s_full + stage, pol);
+                const uint32_t sbytes = (uint32_t)(480 * f);
+                bfk::mbar_arrive_expect_tx(bar_s_full + stage, (uint32_t)tl.cnt * sbytes);
+                bfk::bulk_g2s(Ss + (stage * 2) * (L::kSBlock / 4), J.S + blk0 * (int64_t)(120 * f),
+                              sbytes, bar_s_full + stage, pol);
                 if (tl.cnt > 1)
                     bfk::bulk_g2s(Ss + (stage * 2 + 1) * (L::kSBlock / 4),
-                                  p.S + blk1 * (int64_t)(120 * F), L::kSBlock, bar_s_full + stage,
-                                  pol);
+                                  J.S + blk1 * (int64_t)(120 * f), sbytes, bar_s_full + stage, pol);
             }
             __syncwarp();
             tl = nx;
@@ -421,15 +514,17 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------------------ MMA issuer
-        int cur_g = -1;
+        int cur_g = -1, cur_j = -1;
         int64_t seg = -1;
         constexpr uint32_t idesc = tc::idesc_tf32(128, 128);
         constexpr uint32_t idesc_c = tc::idesc_bf16(128, 128);
         uint32_t w_base = tc::smem_u32(Wsm);
         bool exact = false;
         for (int64_t t = 0; it.next(tl); ++t) {
-            if (tl.g != cur_g) {   // new group segment: its W was prefetched by the producer
-                exact = __ldg(p.wexact + tl.g) != 0;
+            const JobCtx &J = jobs[tl.job];
+            const int KP = F > 0 ? L::KP : J.kp;
+            if (tl.g != cur_g || tl.job != cur_j) {   // new group segment: W prefetched by the producer
+                exact = __ldg(J.wexact + tl.g) != 0;
                 // the previous segment's buffer is free once every MMA issued so far completed
                 if (seg >= 0 && lane == 0) tc::mma_commit(bar_wfree + (int)(seg & 1));
                 __syncwarp();
@@ -438,6 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
                 bfk::mbar_wait(bar_wfull + wb, (uint32_t)((seg >> 1) & 1));
                 w_base = tc::smem_u32(Wsm + wb * (L::kWBytes / 4));
                 cur_g = tl.g;
+                cur_j = tl.job;
             }
             const int b = (int)(t & 1);
             const uint32_t u = (uint32_t)(t >> 1);
@@ -466,10 +562,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
                                 16 * 128, 128);
                             if constexpr (!(DBG & 1)) {
                                 if (bf16)
-                                    tc::mma_bf16_ts(d, tmem + at * KP + kb * 8, desc, idesc_c,
+                                    tc::mma_bf16_ts(d, tmem + at * kARegion + kb * 8, desc, idesc_c,
                                                     kb != 0);
                                 else
-                                    tc::mma_tf32_ts(d, tmem + at * KP + kb * 8, desc, idesc,
+                                    tc::mma_tf32_ts(d, tmem + at * kARegion + kb * 8, desc, idesc,
                                                     (grp | kb) != 0);
                             }
                         }
@@ -497,11 +593,12 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
         const int m = q * 32 + lane;
         const int bsel = m >= 60 ? 1 : 0, j = m - 60 * bsel;
         for (int64_t t = 0; it.next(tl); ++t) {
+            const JobCtx &J = jobs[tl.job];
             const int b = (int)(t & 1);
             const uint32_t u = (uint32_t)(t >> 1);
             const bool valid = m < 120 && bsel < tl.cnt;
-            const int64_t blk = valid ? block_of(p, tl.item + bsel) : 0;
-            float *Rb = p.R + blk * (int64_t)(bfk::r_block_bytes(LAYOUT) / 4);
+            const int64_t blk = valid ? block_of(J, tl.item + bsel) : 0;
+            float *Rb = J.R + blk * (int64_t)(bfk::r_block_bytes(LAYOUT) / 4);
             bfk::mbar_wait(bar_d_full + b, u & 1);
             tc::fence_after_sync();
             const uint32_t d = tmem + ((uint32_t)(q * 32) << 16) + kDCol0 + 128 * b + 64 * h;

@@ -14,7 +14,7 @@ import ctypes
 
 import torch
 
-from ._lib import BfError, Layout, Status, Variant, check, lib
+from ._lib import BatchJob, BfError, Layout, Status, Variant, check, lib
 
 N_ANT = 64
 N_RE = 60
@@ -226,3 +226,18 @@ def plan_create_status(n_ant: int, f: int, b: int, layout: int = 0) -> Status:
 
 
 __all__ = ["Plan", "Layout", "Status", "Variant", "BfError", "plan_create_status", "N_ANT", "N_RE", "MAX_F"]
+
+
+def apply_batch(jobs, stream=None) -> None:
+    """bf_apply_batch: jobs is a sequence of (plan, S, perm, offsets, out) with perm /
+    offsets from Plan.route / route_into or both None; same checks as apply_routed."""
+    arr = (BatchJob * max(1, len(jobs)))()
+    keep = []
+    for i, (plan, S, perm, offsets, out) in enumerate(jobs):
+        n = S.shape[0]
+        plan._check(S, "S", plan.s_shape(n))
+        plan._check(out, "out", plan.r_shape(n), dtype=plan.r_dtype)
+        arr[i] = BatchJob(plan._h.value, S.data_ptr(), None if perm is None else perm.data_ptr(),
+                          None if offsets is None else offsets.data_ptr(), out.data_ptr(), n)
+        keep.append((S, perm, offsets, out))
+    check(lib().bf_apply_batch(arr, len(jobs), _stream_handle(stream)))

@@ -76,6 +76,7 @@ def test_bench_c5_short_stream():
     d = _run(["--config", "c5", "--steps", "3", "--warmup", "3", "--c5-chunks", "64"])
     assert d["config"]["workload"] == "c5" and d["config"]["chunks_per_step"] == 64
     assert d["config"]["launch_mode"] == "cuda_graph"
+    assert d["config"]["chunks_per_launch"] == 8 and d["config"]["launches_per_step"] == 8
     assert d["config"]["apply_sms"] + d["config"]["route_sms"] \
         == torch.cuda.get_device_properties(0).multi_processor_count
     assert d["value"] > 0 and 0 < d["roofline"]["frac"] < 1.5

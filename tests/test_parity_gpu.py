@@ -568,3 +568,64 @@ def test_no_write_outside_R(f, layout, variant):
         assert (h[:guard] == 0x7FC0DEAD).all() and (h[guard + r_words:] == 0x7FC0DEAD).all()
         assert not (h[guard:guard + r_words] == 0x7FC0DEAD).any(), "R not fully written"
     plan.close()
+
+
+@pytest.mark.parametrize("layout", [Layout.INTERLEAVED, Layout.PLANAR, Layout.INTERLEAVED_F16OUT])
+def test_apply_batch_equals_routed_applies(layout):
+    """bf_apply_batch over 19 jobs (more than one pack of 16): plans of different f, tagged
+    and untagged, f = 0, an FFMA-forced plan, an empty job, a plan used twice — bitwise equal
+    to the jobs' own bf_apply_routed calls, and within the contract of the oracle."""
+    planar = layout == Layout.PLANAR
+    specs = [(36, 55, 700), (1, 1, 33), (7, 5, 129), (0, 1, 9), (17, 3, 1), (36, 55, 0),
+             (12, 300, 901), (3, 2, 64)] + [(f, 4, 40 + f) for f in (5, 9, 20, 24, 31, 33, 35, 2, 13, 30, 36)]
+    plans, jobs, refs, host = {}, [], [], []
+    for i, (f, G, n) in enumerate(specs):
+        key = (f, G)
+        if key not in plans:
+            pl = Plan(f=f, layout=layout, variant=Variant.FFMA if (f, G) == (17, 3) else Variant.AUTO)
+            W = syn.precoders(21, i, G, 64, f, "unit_columns")
+            pl.set_precoders(torch.from_numpy(syn.to_planar(W) if planar else W).to(DEV))
+            plans[key] = (pl, W)
+        pl, W = plans[key]
+        S = syn.qam_symbols(21, 100 + i, np.arange(n), f, 60, 64)
+        Sd = torch.from_numpy(syn.to_planar(S) if planar else S).to(DEV)
+        perm = offs = None
+        tags = None
+        if G > 1 and n > 0:
+            tags = syn.subband_tags(21, np.arange(n) + 7 * i, G)
+            perm, offs = pl.route(torch.from_numpy(tags).to(DEV))
+        out = torch.full(pl.r_shape(n), 7.0, dtype=pl.r_dtype, device=DEV)
+        ref = pl.apply_routed(Sd, perm, offs) if n > 0 else out.clone()
+        jobs.append((pl, Sd, perm, offs, out))
+        refs.append(ref)
+        host.append((W, S, tags))
+    torch.cuda.synchronize()
+    bf.apply_batch(jobs)
+    torch.cuda.synchronize()
+    for i, ((_, _, _, _, out), ref) in enumerate(zip(jobs, refs)):
+        assert_bitwise(out.cpu().numpy(), ref.cpu().numpy(), f"job {i} {specs[i]}")
+    if layout == Layout.INTERLEAVED:
+        for i in (0, 2, 6, 12):
+            W, S, tags = host[i]
+            R_ref, T, _ = oracle.beamform(W, S, tags, n_threads=NT)
+            assert_parity(jobs[i][4].cpu().numpy(), R_ref, T, what=f"batch job {i}")
+    for pl, _ in plans.values():
+        pl.close()
+
+
+def test_apply_batch_errors():
+    a, b = Plan(f=8), Plan(f=8, layout=Layout.PLANAR)
+    for pl in (a, b):
+        pl.set_precoders(torch.zeros(pl.w_shape(1), dtype=pl.dtype, device=DEV))
+    S = torch.zeros(a.s_shape(4), dtype=a.dtype, device=DEV)
+    R = torch.empty(a.r_shape(4), dtype=a.dtype, device=DEV)
+    Sp = torch.zeros(b.s_shape(4), dtype=b.dtype, device=DEV)
+    Rp = torch.empty(b.r_shape(4), dtype=b.dtype, device=DEV)
+    with pytest.raises(bf.BfError, match="layout"):
+        bf.apply_batch([(a, S, None, None, R), (b, Sp, None, None, Rp)])
+    perm = torch.zeros(4, dtype=torch.int32, device=DEV)
+    with pytest.raises(bf.BfError, match="job 0"):
+        bf.apply_batch([(a, S, perm, None, R)])
+    bf.apply_batch([])
+    for pl in (a, b):
+        pl.close()

@@ -14,7 +14,8 @@ static float run(const float *S, float *R, const float *Wimg, long long n, int r
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     bftc::TcParams p{};
-    p.Wimg = Wimg; p.S = S; p.R = R; p.n_items = n; p.n_groups = 1; p.wexact = wexact;
+    p.n_jobs = 1; p.job[0].Wimg = Wimg; p.job[0].S = S; p.job[0].R = R; p.job[0].n_items = n;
+    p.job[0].n_groups = 1; p.job[0].wexact = wexact; p.job[0].f = 36;
     k<<<sms, bftc::kThreads, smem>>>(p);
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
