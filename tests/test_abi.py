@@ -97,3 +97,18 @@ def test_filter_plan_validates_before_touching_gpu(bf):
     assert bf.filter_plan_create_status(0) == bf.Status.INVALID_VALUE
     if not gpu_available():
         assert bf.filter_plan_create_status(2048) == bf.Status.NO_DEVICE
+
+
+def test_batch_and_share_validation_without_gpu(bf):
+    """bf_apply_batch / bf_plan_set_sm_share argument checks (host-side, no GPU touched)."""
+    import ctypes as ct
+    from paper_1810_11451_b200._lib import BatchJob
+    L = bf.lib()
+    assert L.bf_apply_batch(None, 0, None) == bf.Status.OK                 # empty list: no-op
+    assert L.bf_apply_batch(None, 1, None) == bf.Status.INVALID_VALUE      # NULL list
+    assert L.bf_apply_batch(None, -1, None) == bf.Status.INVALID_VALUE
+    jobs = (BatchJob * 2)()
+    assert L.bf_apply_batch(jobs, 2, None) == bf.Status.INVALID_VALUE      # NULL plan
+    assert "plan is NULL" in L.bf_last_error().decode()
+    assert L.bf_plan_set_sm_share(None, 4) == bf.Status.INVALID_VALUE
+    assert ct.sizeof(BatchJob) == 48
