@@ -629,3 +629,47 @@ def test_apply_batch_errors():
     bf.apply_batch([])
     for pl in (a, b):
         pl.close()
+
+
+@pytest.mark.slow
+def test_c5_batched_windows_sampled():
+    """c5 in the bench's launch configuration: windows of 8 consecutive 4096-block chunks
+    (one per cell), each chunk routed, one bf_apply_batch per window on 146 SMs; sampled
+    blocks of every chunk against the oracle."""
+    wl = syn.workload("c5")
+    fc = syn.cell_flows(wl.seed, 8)
+    sms = torch.cuda.get_device_properties(DEV).multi_processor_count
+    plans = []
+    Ws = []
+    for cell in range(8):
+        W = syn.precoders(wl.seed, cell, 55, 64, int(fc[cell]), "none")
+        pl = Plan(f=int(fc[cell]))
+        pl.set_precoders(torch.from_numpy(W).to(DEV))
+        pl.set_sm_share(sms - 2)
+        plans.append(pl)
+        Ws.append(W)
+    for w in (0, 97, 255):
+        jobs, ids_of = [], []
+        for c in range(8 * w, 8 * w + 8):
+            f = int(fc[c % 8])
+            first = c * 4096
+            Sd = torch.empty((4096, f, 60), dtype=torch.complex64, device=DEV)
+            sync.gen_symbols(Sd, wl.seed, 0, f, 60, 0, first=first)
+            td = torch.empty(4096, dtype=torch.int32, device=DEV)
+            sync.gen_tags(td, wl.seed, 55, first=first)
+            perm, offs = plans[c % 8].route(td)
+            R = torch.empty((4096, 64, 60), dtype=torch.complex64, device=DEV)
+            jobs.append((plans[c % 8], Sd, perm, offs, R))
+            ids_of.append(np.arange(first, first + 4096, dtype=np.int64))
+        bf.apply_batch(jobs)
+        torch.cuda.synchronize()
+        for (pl, _, _, _, R), ids, c in zip(jobs, ids_of, range(8 * w, 8 * w + 8)):
+            sel = np.arange(c % 61, 4096, 61)
+            f = pl.f
+            S = syn.qam_symbols(wl.seed, 0, ids[sel], f, 60, syn.block_modulations(wl.seed, ids[sel]))
+            tags = syn.subband_tags(wl.seed, ids[sel], 55)
+            R_ref, T, _ = oracle.beamform(Ws[c % 8], S, tags, n_threads=NT)
+            assert_parity(R[torch.from_numpy(sel).to(DEV)].cpu().numpy(), R_ref, T,
+                          what=f"c5 window {w} chunk {c} (f={f})")
+    for pl in plans:
+        pl.close()

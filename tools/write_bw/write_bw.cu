@@ -91,6 +91,47 @@ __global__ void __launch_bounds__(128) w_bulk(float *R, long long nblk) {
     if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// NW warps per CTA, each lane storing VEC floats (4: STG.128, 8: STG.256) per instruction,
+// consecutive lanes consecutive addresses: the widest-store ceiling of the R stream.
+// order 0: contiguous block range per CTA; 1: grid-stride; 2: pseudo-random block order
+template <int VEC>
+__global__ void w_vec(float *R, long long nblk, int order) {
+    const long long per = (nblk + gridDim.x - 1) / gridDim.x;
+    const long long b0 = blockIdx.x * per, b1 = min(nblk, b0 + per);
+    for (long long it = b0; it < b1; ++it) {
+        long long blk = it;
+        if (order == 1) blk = (it - b0) * gridDim.x + blockIdx.x;
+        if (order == 2) blk = (it * 2654435761LL + 12345) % nblk;   // nblk a power of two: bijective
+        if (blk >= nblk) continue;
+        float *Rb = R + blk * 7680;
+        for (int i = threadIdx.x * VEC; i < 7680; i += blockDim.x * VEC) {
+            const float x = (float)i;
+            if (VEC == 8)
+                asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};"
+                             :: "l"(Rb + i), "f"(x) : "memory");
+            else
+                __stcs(reinterpret_cast<float4 *>(Rb + i), make_float4(x, x, x, x));
+        }
+    }
+}
+
+extern "C" int wbw_vec(int vec, int warps, int order, void *R, long long nblk, int reps, float *ms_out) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int rep = -1; rep < reps; ++rep) {
+        if (rep == 0) cudaEventRecord(a);
+        if (vec == 8) w_vec<8><<<sms, 32 * warps>>>((float *)R, nblk, order);
+        else w_vec<4><<<sms, 32 * warps>>>((float *)R, nblk, order);
+    }
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0; cudaEventElapsedTime(&ms, a, b);
+    *ms_out = ms / reps;
+    return (int)cudaGetLastError();
+}
+
 extern "C" int wbw_run(int mode, void *R, long long nblk, int ctas_per_sm, int reps, float *ms_out) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
