@@ -171,10 +171,13 @@ typedef struct {
  * over several precoder sets at once, e.g. consecutive streaming chunks of
  * different cells).  Equivalent to calling
  * bf_apply_routed for jobs[0..n_jobs) in order on `stream`, with bitwise equal
- * results; the tensor-core jobs are packed into launches of up to 16 jobs (each
+ * results — for plans whose AUTO choice is the FFMA kernel (small f), equal to
+ * the same call with the plan set to BF_VARIANT_TENSOR; jobs are packed into
+ * tensor-core launches of up to 16 jobs (each
  * job split over every CTA, so one kernel fill and drain is paid per pack instead
- * of per job).  f = 0 jobs and plans forced to BF_VARIANT_FFMA run as their own
- * applies.  Every plan must live on one device and share job 0's layout; the
+ * of per job).  Plans with BF_VARIANT_AUTO or _TENSOR join the packed tensor-core
+ * launches whatever their f; f = 0 jobs and plans set to BF_VARIANT_FFMA run as
+ * their own applies.  Every plan must live on one device and share job 0's layout; the
  * grid follows job 0's plan (bf_plan_set_sm_share), and its profiling record and
  * launch count take the packed launches.  Every job is validated before anything
  * is enqueued (BF_ERR_INVALID_VALUE / BF_ERR_MISALIGNED naming the job); a tagged

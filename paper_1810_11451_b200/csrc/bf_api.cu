@@ -40,10 +40,15 @@ constexpr int kRouteMaxTable = 65536;      // tiles x (groups + 1) entries
 constexpr int64_t kDefaultHostChunk = 2048;
 constexpr int kHostSlots = 3;
 constexpr size_t kMaxProfEvents = 1 << 16;  // timed launches kept between kernel_time() calls
-// AUTO variant table (measured, profiles/r01_sweep_f_*.jsonl: c3, 100 000 blocks
-// per f, both layouts): the tensor-core kernel is at least as fast as the FFMA
-// kernel for every f >= 1 (equal at f = 4, 2.2x at f = 36), so AUTO picks it.
-constexpr int kAutoTensorMinF = 1;
+// AUTO variant table, per layout (measured with
+// tools/sweep_f.py on c3's recipe, 100 000 blocks per f, profiles/r01_sweep_f_v3*.jsonl
+// and r01_sweep_auto_v3.jsonl): the smallest f from which the tensor-core kernel is
+// faster.  Below it both kernels are store-bound and the FFMA kernel's epilogue is
+// the cheaper one: interleaved f <= 6 (FFMA up to 7 % ahead; equal at f = 1),
+// planar f <= 10 (FFMA up to 26 % ahead: the tensor epilogue's planar stores,
+// DESIGN.md §6), fp16 output f <= 2.  From there on the tensor kernel wins, by
+// 2.2-2.6x at f = 36.
+constexpr int kAutoTensorMinF[3] = {7, 11, 3};   // [layout]
 
 BfKernelTable g_table;      // FFMA kernels [f][layout]
 BfKernelTable g_table_tc;   // tcgen05 split-TF32 kernels [f][layout]
@@ -466,7 +471,7 @@ bf_status check_tags_if_requested(bf_plan_t p, cudaStream_t st) {
 bool use_tensor(bf_plan_t p) {
     if (p->variant == BF_VARIANT_TENSOR) return true;
     if (p->variant == BF_VARIANT_FFMA) return false;
-    return p->f >= kAutoTensorMinF;
+    return p->f >= kAutoTensorMinF[p->layout];
 }
 
 int sms_used(bf_plan_t p) {
@@ -828,7 +833,7 @@ bf_status bf_apply_batch(const bf_batch_job *jobs, int n_jobs, void *stream) {
     }
     DeviceGuard guard(p0->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // f == 0 and FFMA-variant jobs run as their own applies, in order; tensor jobs are
+    // f == 0 and FFMA-variant jobs run as their own applies, in order; the others are
     // packed into launches of at most kMaxJobs jobs and kOffsSlots group offsets.
     bf_batch_job pack[bftc::kMaxJobs];
     int np = 0, slots = 0;
@@ -836,7 +841,10 @@ bf_status bf_apply_batch(const bf_batch_job *jobs, int n_jobs, void *stream) {
     for (int i = 0; i <= n_jobs; ++i) {
         const bool end = i == n_jobs;
         const bf_batch_job *jb = end ? nullptr : &jobs[i];
-        const bool tc = !end && jb->n_blocks > 0 && jb->plan->f > 0 && use_tensor(jb->plan);
+        // AUTO plans always join the pack (one launch for the window beats the small-f
+        // per-kernel edge of the FFMA kernel); plans set to FFMA run on their own
+        const bool tc = !end && jb->n_blocks > 0 && jb->plan->f > 0 &&
+                        jb->plan->variant != BF_VARIANT_FFMA;
         const int need = tc && jb->offsets_dev ? jb->plan->n_groups + 2 : 0;
         if (np > 0 && (end || !tc || np == bftc::kMaxJobs || slots + need > bftc::kOffsSlots)) {
             if ((s = launch_batch(pack, np, st)) != BF_OK) return s;

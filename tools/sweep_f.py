@@ -9,6 +9,7 @@ GB/s of algorithmic bytes, TFLOP/s of algorithmic FLOPs, fractions of the HBM
 and derived FP32 peaks.
 """
 import argparse
+import dataclasses
 import json
 import os
 import sys
@@ -37,14 +38,16 @@ def main():
     p32 = benchkit.fp32_peak_tflops(sms, peaks.get("sm_max_mhz", 1965.0))
     planar = a.layout == "planar"
     for f in [int(x) for x in a.flows.split(",")]:
-        wl = syn.workload("c3", f)
+        # off-sweep f (the AUTO table needs every f): c3's recipe with that f
+        wl = syn.workload("c3", f) if f in syn.C3_FLOWS else \
+            dataclasses.replace(syn.workload("c3", 1), name=f"c3like_f{f}", f=f, sub=f)
         n = min(a.blocks, wl.n_blocks)
         S, _ = sync.workload_device(wl, dev, n=n, planar=planar)
         W = syn.precoders(wl.seed, wl.sub, 1, 64, f, wl.w_norm)
         for variant in (["ffma", "tensor"] if f > 0 else ["auto"]):
             plan = bf.Plan(f=f, layout=a.layout, variant=variant)
             plan.set_precoders(torch.from_numpy(syn.to_planar(W) if planar else W).to(dev))
-            R = torch.empty(plan.r_shape(n), dtype=plan.dtype, device=dev)
+            R = torch.empty(plan.r_shape(n), dtype=plan.r_dtype, device=dev)
             for _ in range(3):
                 plan.apply(S, out=R)
             torch.cuda.synchronize()
@@ -59,7 +62,8 @@ def main():
             step_ms = e0.elapsed_time(e1) / a.reps
             kms, kn = plan.kernel_time()
             kern_ms = kms / kn if kn else step_ms
-            gbs = wl.block_bytes * n / (kern_ms * 1e-3) / 1e9
+            r_blk = 15360 if a.layout == "interleaved_f16out" else 30720
+            gbs = (480 * f + r_blk) * n / (kern_ms * 1e-3) / 1e9
             tf = wl.block_flops * n / (kern_ms * 1e-3) / 1e12
             print(json.dumps({"f": f, "variant": variant, "layout": a.layout, "blocks": n,
                               "kernel_ms": kern_ms, "step_ms": step_ms, "GBps": gbs,
