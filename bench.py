@@ -689,9 +689,12 @@ def run_c5(args, wl, world, rank, local, dev):
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": None,
                 "peak_basis": "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)",
-                "kernel": f"{'bftc::bf_tc_kernel' if variant == 'tensor' else 'bfk::bf_ffma_kernel'}"
-                          f"<f_c,0> (f_c = {','.join(str(int(x)) for x in fc)})",
-                "variant": variant, "basis": "pipeline: algorithmic bytes of every chunk / step device time",
+                "kernel": (f"bftc::bf_tc_kernel<0,0> (bf_apply_batch, {B} chunks per launch, "
+                           f"f_c = {','.join(str(int(x)) for x in fc)})") if B > 1 else
+                          (f"{'bftc::bf_tc_kernel' if variant == 'tensor' else 'bfk::bf_ffma_kernel'}"
+                           f"<f_c,0> (f_c = {','.join(str(int(x)) for x in fc)})"),
+                "variant": "tensor" if B > 1 and args.variant != "ffma" else variant,
+                "basis": "pipeline: algorithmic bytes of every chunk / step device time",
                 "kernel_ms_eager_sum": kern_ms / args.steps,
                 "mixed_f_roofline_ms": bytes_all / world / hbm / 1e6 / args.steps,
                 "algorithmic_bytes_per_step": bytes_all // args.steps,
