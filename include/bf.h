@@ -10,10 +10,10 @@
  *
  *   For every block n with precoder group g = group_idx[n] (0 when no tags):
  *       R[n][i][j] = sum_{k<f} W[g][i][k] * S[n][k][j]     complex fp32,
- *   accumulated with fp32 fused multiply-adds (4 FFMA per complex MAC,
- *   accumulators start at +0.0f).  Accuracy contract (BASELINE.json north_star
- *   item 4): |R - R_exact| <= 1e-5 * sum_k |W[g][i][k]| |S[n][k][j]| per
- *   element; bit-exact for f = 0 (+0.0) and for identity / selection W.
+ *   accumulated in fp32 from +0.0f (by CUDA-core FFMAs or by error-compensated
+ *   tensor-core MMAs, see bf_variant).  Accuracy contract (BASELINE.json
+ *   north_star item 4): |R - R_exact| <= 1e-5 * sum_k |W[g][i][k]| |S[n][k][j]|
+ *   per element; bit-exact for f = 0 (+0.0) and for identity / selection W.
  *
  * The calls follow the paper's statement: W is set once (bf_set_precoders),
  * then many S blocks are multiplied by it (bf_apply).  Multiple precoder
@@ -85,11 +85,14 @@ typedef enum {
 
 /* Kernel variant.  Both compute the same product within the same contract.
  *   BF_VARIANT_FFMA    CUDA-core kernel: 4 fp32 FFMA per complex MAC.
- *   BF_VARIANT_TENSOR  tcgen05 tensor-core kernel: S split into 3 tf32 terms,
- *                      W into 2, four kind::tf32 MMAs per K step, fp32
- *                      accumulation in TMEM (error-compensated split precision,
- *                      BASELINE.json north_star item 2).
- *   BF_VARIANT_AUTO    per-f choice from the measured variant table (default). */
+ *   BF_VARIANT_TENSOR  tcgen05 tensor-core kernel: S split exactly into 3 terms
+ *                      of 11-bit significands, W into 2; S1 W1 in kind::tf32 and
+ *                      the corrections S2 W1 + S1 W2 in one kind::f16 (bf16) MMA
+ *                      group (S2 W1 + S3 W1 + S1 W1 in tf32 when W is exactly
+ *                      tf32), fp32 accumulation in TMEM (error-compensated split
+ *                      precision, BASELINE.json north_star item 2).
+ *   BF_VARIANT_AUTO    per-(f, layout) choice from the measured variant table
+ *                      (default): FFMA at small f, tensor above. */
 typedef enum {
     BF_VARIANT_AUTO = 0,
     BF_VARIANT_FFMA = 1,

@@ -24,6 +24,8 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
 LIBBF = os.path.join(PKG, "libbf.so")
 LIBSYNTH = os.path.join(ROOT, "bf_synth", "libbfsynth.so")
 LIBPROBE = os.path.join(ROOT, "benchkit", "libbfprobe.so")
+DEMO = os.path.join(ROOT, "build", "bf_demo")
+CUDA_HOME = os.path.dirname(os.path.dirname(NVCC))
 
 
 def _stale(out: str, deps: list[str]) -> bool:
@@ -77,7 +79,15 @@ def build(verbose: bool = False) -> list[str]:
                 os.path.join(ROOT, "build", "synth"), verbose)
     nvcc_shared([os.path.join(ROOT, "benchkit", "csrc", "probes.cu")], LIBPROBE, [], [],
                 os.path.join(ROOT, "build", "probe"), verbose)
-    return [LIBBF, LIBSYNTH, LIBPROBE]
+    # a plain-C99 consumer of the C ABI (examples/bf_demo.c; run by tests/test_c_demo.py)
+    demo_src = os.path.join(ROOT, "examples", "bf_demo.c")
+    if shutil.which("gcc") and _stale(DEMO, [demo_src, LIBBF, os.path.join(inc, "bf.h")]):
+        os.makedirs(os.path.dirname(DEMO), exist_ok=True)
+        _run(["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", f"-I{inc}",
+              f"-I{os.path.join(CUDA_HOME, 'include')}", demo_src, f"-L{PKG}", "-lbf",
+              f"-L{os.path.join(CUDA_HOME, 'lib64')}", "-lcudart",
+              "-Wl,-rpath,$ORIGIN/../paper_1810_11451_b200", "-o", DEMO])
+    return [LIBBF, LIBSYNTH, LIBPROBE, DEMO]
 
 
 if __name__ == "__main__":
