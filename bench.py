@@ -282,7 +282,10 @@ def run_ours(args):
     clk = clocks.stop() if clocks else None
 
     elapsed_ms = shard.max_over_ranks(elapsed_ms, dev)
-    kern_avg_ms = shard.max_over_ranks(kern_ms / max(kern_n, 1), dev)
+    # f = 0 launches no beamforming kernel (a8: R := +0 by cudaMemsetAsync): the memset
+    # is the step's only work, timed by the step events
+    memset_only = kern_n == 0
+    kern_avg_ms = shard.max_over_ranks(elapsed_ms / args.steps if memset_only else kern_ms / kern_n, dev)
     launches = int(shard.sum_over_ranks(launches, dev))
     total_blocks = wl.n_blocks
     value = total_blocks * wl.b * args.steps / (elapsed_ms * 1e-3)
@@ -331,8 +334,8 @@ def run_ours(args):
                 "peak_basis": "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)",
                 "fp32_equivalent": {"achieved": achieved_tf, "unit": "TFLOP/s",
                                     "frac_of_derived_fp32_peak": achieved_tf / peak_max}}
-    roof["kernel"] = f"{'bftc::bf_tc_kernel' if variant == 'tensor' else 'bfk::bf_ffma_kernel'}" \
-                     f"<{wl.f},{1 if planar else 0}>"
+    roof["kernel"] = "cudaMemsetAsync (f = 0: R := +0)" if memset_only else \
+        f"{'bftc::bf_tc_kernel' if variant == 'tensor' else 'bfk::bf_ffma_kernel'}<{wl.f},{1 if planar else 0}>"
     roof["variant"] = variant
     if clk and clk.get("sm_mhz"):
         roof["frac_at_observed_clock"] = achieved_tf / benchkit.fp32_peak_tflops(sms, clk["sm_mhz"]) \
