@@ -559,13 +559,7 @@ bf_status apply_routed(bf_plan_t p, const void *S, const int32_t *perm, const in
 // first job's plan.
 bf_status launch_batch(const bf_batch_job *jobs, int n, cudaStream_t st) {
     bf_plan_t p0 = jobs[0].plan;
-    const BfKernelEntry &kern = g_table_tc[0][p0->layout];
-    static bool attr_set[64][3] = {};
-    if (!attr_set[p0->device & 63][p0->layout]) {
-        BF_CUDA(cudaFuncSetAttribute(kern.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kern.smem_bytes));
-        attr_set[p0->device & 63][p0->layout] = true;
-    }
+    const BfKernelEntry &kern = g_table_tc[0][p0->layout];   // smem attribute set at plan create
     bftc::TcParams tp{};
     int64_t tiles = 0;
     for (int i = 0; i < n; ++i) {
@@ -710,6 +704,10 @@ bf_status bf_plan_create(int n_ant, int f, int b, int layout, bf_plan_t *out) {
         e = cudaFuncSetAttribute(p->kern_tc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  p->kern_tc.smem_bytes);
         if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaFuncSetAttribute (tc)"); }
+        // the runtime-f kernel of bf_apply_batch for this layout (idempotent per device)
+        const BfKernelEntry &kb = g_table_tc[0][layout];
+        e = cudaFuncSetAttribute(kb.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kb.smem_bytes);
+        if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaFuncSetAttribute (batch)"); }
     }
     *out = p;
     return BF_OK;
