@@ -245,7 +245,7 @@ def run_ours(args):
     for _ in range(max(args.warmup, 0)):
         plan.apply(S, tags, out=R)
     torch.cuda.synchronize()
-    clocks = benchkit.ClockSampler(local).start() if rank == 0 else None
+    clocks = benchkit.ClockSampler(local, period_ms=25).start() if rank == 0 else None
     plan.set_profiling(True)
     plan.kernel_time()
     launches0 = plan.launch_count()
@@ -445,7 +445,7 @@ def run_filter(args, wl, world, rank, local, dev):
     for _ in range(max(args.warmup, 0)):
         plan.apply(s, out=y)
     torch.cuda.synchronize()
-    clocks = benchkit.ClockSampler(local).start() if rank == 0 else None
+    clocks = benchkit.ClockSampler(local, period_ms=25).start() if rank == 0 else None
     plan.set_profiling(True)
     plan.kernel_time()
     l0 = plan.launch_count()
@@ -642,7 +642,7 @@ def run_c5(args, wl, world, rank, local, dev):
     for _ in range(max(args.warmup, 0)):
         run_step()
     torch.cuda.synchronize()
-    clocks = benchkit.ClockSampler(local).start() if rank == 0 else None
+    clocks = benchkit.ClockSampler(local, period_ms=25).start() if rank == 0 else None
     if graph is None:
         for pl in plans:
             pl.set_profiling(True)
