@@ -29,19 +29,27 @@ namespace bff {
 
 constexpr int kN = 2048;
 constexpr int kThreads = 128;
-constexpr int kPad = kN + kN / 16;           // padded shared-memory slots (float2)
+constexpr int kPad = kN + kN / 8;            // padded shared-memory slots (float2): 2 per 16
 // Twiddle table tw[m] = w^m = e^{-2 pi i m / N} (fp64-evaluated, rounded once), read
 // through L1.  A pass needs w^(c r k) for r < R: the kernel loads the binary powers
 // w^(c k 2^e) from the table and forms the others with at most 3 complex products
 // (relative error <= 4 * 2^-24), which keeps 4 instead of R - 1 twiddles live.
 constexpr int kTwN = kN;
-// Per-pass tables in shared memory, [r][k] (lanes read consecutive words): pass 2
-// w^(8 r k) (r 1..15, k < 16), pass 3 w^(r k) (r 1..7, k < 256).
-constexpr int kTw2 = 0, kTw3 = kTw2 + 15 * 16, kTwS = kTw3 + 7 * 256;
+// Per-pass tables in shared memory, laid out so that a thread reads two twiddles
+// per 128-bit load: pass 2 [k][r - 1] (k < 16, rows of 18 slots: 15 twiddles
+// w^(8 r k), r = 1..15, padded so 8 lanes of an LDS.128 hit distinct banks),
+// pass 3 [r - 1][t] = (w^(r t), w^(r (t + 128))) for r = 1..7, t < 128 (a plan-owned
+// global table read through L1 — shared by the 5 CTAs of an SM, and keeping the
+// shared memory per CTA small enough for 5 resident CTAs).
+constexpr int kTw2Row = 18;
+constexpr int kTw2 = 0, kTwS = kTw2 + 16 * kTw2Row;
+constexpr int kTw3N = 7 * 128;                  // float4 entries of the pass-3 table
 
 
 
-__device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+// exchange-buffer index: 2 padding slots per 16 keep every access pattern below
+// conflict-free and make a pass-1 thread's 16 outputs 16-byte aligned (STS.128)
+__device__ __forceinline__ int pad(int i) { return i + 2 * (i >> 4); }
 
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
@@ -121,11 +129,15 @@ __device__ __forceinline__ void dft16(float2 (&v)[16]) {
 
 // One forward FFT of the CTA's signal (radix 16, 16, 8 Stockham).
 // In: v[q] = x[t + 128 q].  Out: v[q] = X[t + 128 q].
-__device__ __forceinline__ void fft2048(float2 (&v)[16], float2 *sm, const float2 *tw, int t) {
+__device__ __forceinline__ void fft2048(float2 (&v)[16], float2 *sm, const float2 *tw,
+                                        const float4 *__restrict__ tw3, int t) {
     // pass 1: Ns = 1, R = 16 (no twiddles); y[16 j + r]
     dft16(v);
 #pragma unroll
-    for (int r = 0; r < 16; ++r) sm[pad(16 * t + r)] = v[tr16(r)];
+    for (int r = 0; r < 16; r += 2) {
+        const float2 a = v[tr16(r)], b = v[tr16(r + 1)];
+        *reinterpret_cast<float4 *>(sm + pad(16 * t + r)) = make_float4(a.x, a.y, b.x, b.y);
+    }
     __syncthreads();
     // pass 2: Ns = 16, R = 16; twiddles w^(8 r k), k = j mod 16; y[(j/16) 256 + k + 16 r]
     {
@@ -133,7 +145,11 @@ __device__ __forceinline__ void fft2048(float2 (&v)[16], float2 *sm, const float
         for (int r = 0; r < 16; ++r) v[r] = sm[pad(t + 128 * r)];
         const int k = t & 15;
 #pragma unroll
-        for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], tw[kTw2 + (r - 1) * 16 + k]);
+        for (int r = 1; r < 16; r += 2) {
+            const float4 w = *reinterpret_cast<const float4 *>(tw + kTw2 + k * kTw2Row + (r - 1));
+            v[r] = cmul(v[r], make_float2(w.x, w.y));
+            if (r + 1 < 16) v[r + 1] = cmul(v[r + 1], make_float2(w.z, w.w));
+        }
         dft16(v);
         __syncthreads();
         const int base = (t >> 4) * 256 + k;
@@ -150,8 +166,9 @@ __device__ __forceinline__ void fft2048(float2 (&v)[16], float2 *sm, const float
         }
 #pragma unroll
         for (int r = 1; r < 8; ++r) {
-            v[2 * r] = cmul(v[2 * r], tw[kTw3 + (r - 1) * 256 + t]);
-            v[2 * r + 1] = cmul(v[2 * r + 1], tw[kTw3 + (r - 1) * 256 + t + 128]);
+            const float4 w = __ldg(tw3 + (r - 1) * 128 + t);
+            v[2 * r] = cmul(v[2 * r], make_float2(w.x, w.y));
+            v[2 * r + 1] = cmul(v[2 * r + 1], make_float2(w.z, w.w));
         }
         dft8<2>(v);        // butterfly t:       v[0], v[2], ..., v[14]
         dft8<2>(v + 1);    // butterfly t + 128: v[1], v[3], ..., v[15]
@@ -168,11 +185,13 @@ struct FParams {
                          // the prefetch stage, before the CTA writes it)
     const float2 *H;     // [2048] FFT of the filter sequence (plan-owned)
     const float2 *tw;    // [2048] twiddle table (plan-owned)
+    const float4 *tw3;   // [7][128] pass-3 twiddle pairs (plan-owned)
     int64_t n_sig;
-    int mode;            // 0: filter; 1: forward FFT only (builds H from h)
+    int mode;            // 0: filter (H holds DFT(h) / N); 1: forward FFT only;
+                         // 2: forward FFT scaled by 1/N (builds the plan's H from h)
 };
 
-__global__ void __launch_bounds__(kThreads, 4) filter_kernel(const FParams p) {
+__global__ void __launch_bounds__(kThreads, 5) filter_kernel(const FParams p) {
     // sm: exchange buffer; stage: the next signal, prefetched with one TMA bulk copy
     // (16 KB) while the current one is transformed.  Twiddles and H are read
     // through L1 (__ldg): every CTA on the SM shares the same 32 KB.
@@ -183,9 +202,9 @@ __global__ void __launch_bounds__(kThreads, 4) filter_kernel(const FParams p) {
     uint64_t *barp = reinterpret_cast<uint64_t *>(tws + kTwS);
     uint64_t &bar = *barp;
     const int t = threadIdx.x;
-    for (int i = t; i < kTwS; i += kThreads) {
-        const int m = i < kTw3 ? 8 * (i / 16 + 1) * (i % 16) : ((i - kTw3) / 256 + 1) * ((i - kTw3) % 256);
-        tws[i] = p.tw[m & (kN - 1)];
+    for (int i = t; i < kTwS; i += kThreads) {   // pass 2: [k][r - 1], rows of kTw2Row slots
+        const int k = i / kTw2Row, rr = i % kTw2Row;
+        tws[i] = p.tw[(rr < 15 ? 8 * (rr + 1) * k : 0) & (kN - 1)];
     }
     if (t == 0) {
         bfk::mbar_init(&bar, 1);
@@ -214,11 +233,12 @@ __global__ void __launch_bounds__(kThreads, 4) filter_kernel(const FParams p) {
             bfk::bulk_g2s(stage, p.s + nxt * kN, kN * 8, &bar, pol);
         }
         // forward FFT, MULT by H, inverse FFT as conj(FFT(conj(.))) / N — one copy of
-        // the transform code in a two-trip loop keeps register pressure at one FFT's
+        // the transform code in a two-trip loop keeps register pressure at one FFT's.
+        // The plan stores H / N (exact: N = 2^11), so the 1/N costs nothing here.
         const int trips = p.mode == 0 ? 2 : 1;
 #pragma unroll 1
         for (int trip = 0; trip < trips; ++trip) {
-            fft2048(v, sm, tws, t);
+            fft2048(v, sm, tws, p.tw3, t);
             if (trip == 0 && trips == 2) {
 #pragma unroll
                 for (int q = 0; q < 16; ++q) v[q] = conj2(cmul(v[q], __ldg(p.H + t + 128 * q)));
@@ -226,7 +246,10 @@ __global__ void __launch_bounds__(kThreads, 4) filter_kernel(const FParams p) {
         }
         if (p.mode == 0) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) v[q] = make_float2(v[q].x * inv_n, -v[q].y * inv_n);
+            for (int q = 0; q < 16; ++q) v[q] = conj2(v[q]);
+        } else if (p.mode == 2) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = make_float2(v[q].x * inv_n, v[q].y * inv_n);
         }
 #pragma unroll
         for (int q = 0; q < 16; ++q) __stcs(dst + t + 128 * q, v[q]);
@@ -240,6 +263,17 @@ __global__ void twiddle_kernel(float2 *tw) {
     double s, c;
     sincospi(-2.0 * (double)m / kN, &s, &c);
     tw[m] = make_float2((float)c, (float)s);
+}
+
+// tw3[(r - 1) 128 + t] = (w^(r t), w^(r (t + 128))), fp64-evaluated, rounded once.
+__global__ void twiddle3_kernel(float4 *tw3) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= kTw3N) return;
+    const int r = i / 128 + 1, t = i % 128;
+    double s0, c0, s1, c1;
+    sincospi(-2.0 * (double)((r * t) % kN) / kN, &s0, &c0);
+    sincospi(-2.0 * (double)((r * (t + 128)) % kN) / kN, &s1, &c1);
+    tw3[i] = make_float4((float)c0, (float)s0, (float)c1, (float)s1);
 }
 
 }  // namespace bff

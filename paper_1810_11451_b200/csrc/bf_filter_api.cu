@@ -18,6 +18,7 @@ using bfh::fail;
 struct bff_plan_s {
     int n = bff::kN, device = 0, num_sms = 0, ctas_per_sm = 0;
     float2 *tw = nullptr, *H = nullptr;
+    float4 *tw3 = nullptr;
     bool have_taps = false;
     bool profiling = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
@@ -30,7 +31,7 @@ namespace {
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 bf_status launch(bff_plan_t p, const float2 *s, float2 *y, int64_t n, int mode, cudaStream_t st) {
-    bff::FParams fp{s, y, p->H, p->tw, n, mode};
+    bff::FParams fp{s, y, p->H, p->tw, p->tw3, n, mode};
     const int64_t cap = (int64_t)p->num_sms * std::max(1, p->ctas_per_sm);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(n, cap));
     cudaEvent_t e1 = nullptr;
@@ -100,23 +101,27 @@ bf_status bff_plan_create(int n, bff_plan_t *out) {
                                                       bff::kThreads, bff::kSmemBytes);
     if (e != cudaSuccess) { delete p; return cuda_fail(e, "occupancy query"); }
     if (cudaMalloc(&p->tw, bff::kTwN * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc(&p->tw3, bff::kTw3N * sizeof(float4)) != cudaSuccess ||
         cudaMalloc(&p->H, bff::kN * sizeof(float2)) != cudaSuccess) {
         cudaGetLastError();
         cudaFree(p->tw);
+        cudaFree(p->tw3);
         cudaFree(p->H);
         delete p;
         return fail(BF_ERR_OUT_OF_MEMORY, "cudaMalloc of the filter plan tables failed");
     }
     bff::twiddle_kernel<<<(bff::kTwN + 255) / 256, 256>>>(p->tw);
+    bff::twiddle3_kernel<<<(bff::kTw3N + 255) / 256, 256>>>(p->tw3);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         cudaFree(p->tw);
+        cudaFree(p->tw3);
         cudaFree(p->H);
         delete p;
         return cuda_fail(e, "twiddle table");
     }
-    ++p->launches;
+    p->launches += 2;
     *out = p;
     return BF_OK;
 }
@@ -126,7 +131,8 @@ bf_status bff_set_taps(bff_plan_t p, const void *h_dev, void *stream) {
     if (!h_dev) return fail(BF_ERR_INVALID_VALUE, "h_dev is NULL");
     if (!aligned16(h_dev)) return fail(BF_ERR_MISALIGNED, "h_dev must be 16-byte aligned");
     DeviceGuard g(p->device);
-    bf_status s = launch(p, static_cast<const float2 *>(h_dev), p->H, 1, 1,
+    // the plan keeps DFT(h) / N (mode 2): the filter's inverse-transform scale, folded in
+    bf_status s = launch(p, static_cast<const float2 *>(h_dev), p->H, 1, 2,
                          static_cast<cudaStream_t>(stream));
     if (s == BF_OK) p->have_taps = true;
     return s;
@@ -154,6 +160,7 @@ bf_status bff_destroy(bff_plan_t p) {
     {
         DeviceGuard g(p->device);
         cudaFree(p->tw);
+        cudaFree(p->tw3);
         cudaFree(p->H);
         for (auto &ev : p->prof_events) {
             cudaEventDestroy(ev.first);
