@@ -186,61 +186,84 @@ __global__ void bf_route_hist(const int32_t *__restrict__ gidx, int64_t n, int G
         table[(int64_t)blockIdx.x * (G + 1) + b] = hist[b];
 }
 
-// Pass 2 (one CTA of 1024 threads): table[tile][bin] <- global start of the
-// tile's items of that bin; offsets[0..G] <- start of each bin, offsets[G+1] = n.
-__global__ void bf_route_scan(int32_t *__restrict__ table, int P, int G, int64_t n,
-                              int32_t *__restrict__ offsets) {
-    __shared__ int32_t tot[kMaxGroups + 2];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    for (int b = warp; b <= G; b += nwarps) {
-        int32_t carry = 0;
-        for (int t0 = 0; t0 < P; t0 += 32) {
-            const int t = t0 + lane;
-            const int32_t v = t < P ? table[(int64_t)t * (G + 1) + b] : 0;
-            int32_t inc = v;
+// Pass 2 (one CTA of 1024 threads per bin): table[tile][bin] <- start of the tile's
+// items within the bin (exclusive scan of the bin's column over the tiles, 1024 tiles
+// per step, every load in flight at once); bin_tot[bin] <- the bin's total.
+__global__ void __launch_bounds__(1024) bf_route_colscan(int32_t *__restrict__ table, int P, int G,
+                                                         int32_t *__restrict__ bin_tot) {
+    __shared__ int32_t wsum[32];
+    __shared__ int32_t btot;
+    const int b = blockIdx.x, nb = G + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t carry = 0;
+    for (int t0 = 0; t0 < P; t0 += 1024) {
+        const int t = t0 + threadIdx.x;
+        const int32_t v = t < P ? table[(int64_t)t * nb + b] : 0;
+        int32_t inc = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += u;
+        }
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {                          // exclusive prefix of the 32 warp totals
+            const int32_t w = wsum[lane];
+            int32_t wi = w;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
-                const int32_t u = __shfl_up_sync(0xffffffffu, inc, d);
-                if (lane >= d) inc += u;
+                const int32_t u = __shfl_up_sync(0xffffffffu, wi, d);
+                if (lane >= d) wi += u;
             }
-            if (t < P) table[(int64_t)t * (G + 1) + b] = carry + inc - v;
-            carry += __shfl_sync(0xffffffffu, inc, 31);
+            wsum[lane] = wi - w;
+            if (lane == 31) btot = wi;
         }
-        if (lane == 0) tot[b] = carry;
+        __syncthreads();
+        if (t < P) table[(int64_t)t * nb + b] = carry + wsum[warp] + inc - v;
+        carry += btot;
+        __syncthreads();                          // wsum / btot are reused by the next step
     }
-    __syncthreads();
-    if (warp == 0) {
+    if (threadIdx.x == 0) bin_tot[b] = carry;
+}
+
+// Exclusive scan of the G + 1 bin totals into start[] (shared), by warp 0.
+__device__ __forceinline__ void bin_starts(const int32_t *__restrict__ bin_tot, int nb,
+                                           int32_t *start) {
+    const int lane = threadIdx.x & 31;
+    if ((threadIdx.x >> 5) == 0) {
         int32_t carry = 0;
-        for (int b0 = 0; b0 <= G; b0 += 32) {
+        for (int b0 = 0; b0 < nb; b0 += 32) {
             const int b = b0 + lane;
-            const int32_t v = b <= G ? tot[b] : 0;
+            const int32_t v = b < nb ? bin_tot[b] : 0;
             int32_t inc = v;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const int32_t u = __shfl_up_sync(0xffffffffu, inc, d);
                 if (lane >= d) inc += u;
             }
-            if (b <= G) tot[b] = carry + inc - v;   // exclusive start of bin b
+            if (b < nb) start[b] = carry + inc - v;
             carry += __shfl_sync(0xffffffffu, inc, 31);
         }
     }
-    __syncthreads();
-    for (int b = threadIdx.x; b <= G; b += blockDim.x) offsets[b] = tot[b];
-    if (threadIdx.x == 0) offsets[G + 1] = (int32_t)n;
-    const int64_t entries = (int64_t)P * (G + 1);
-    for (int64_t e = threadIdx.x; e < entries; e += blockDim.x)
-        table[e] += tot[e % (G + 1)];
 }
 
 // Pass 3: stable scatter.  Each warp owns a contiguous sub-tile; ranks come
 // from __match_any_sync so the output order is (bin, block id) exactly.
 __global__ void bf_route_scatter(const int32_t *__restrict__ gidx, int64_t n, int G, int tile,
-                                 const int32_t *__restrict__ table, int32_t *__restrict__ perm) {
-    extern __shared__ int32_t cnt[];   // [8][G + 1]
+                                 const int32_t *__restrict__ table,
+                                 const int32_t *__restrict__ bin_tot, int32_t *__restrict__ perm,
+                                 int32_t *__restrict__ offsets) {
+    extern __shared__ int32_t cnt[];   // [8][G + 1], then start[G + 1]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nb = G + 1;
+    int32_t *start = cnt + 8 * nb;
     for (int e = threadIdx.x; e < 8 * nb; e += blockDim.x) cnt[e] = 0;
+    bin_starts(bin_tot, nb, start);
     __syncthreads();
+    if (blockIdx.x == 0) {                // offsets[0..G] = bin starts, offsets[G + 1] = n
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) offsets[b] = start[b];
+        if (threadIdx.x == 0) offsets[nb] = (int32_t)n;
+    }
     const int64_t ts = (int64_t)blockIdx.x * tile;
     const int per_warp = tile / 8;
     const int64_t ws = ts + (int64_t)warp * per_warp;
@@ -256,7 +279,7 @@ __global__ void bf_route_scatter(const int32_t *__restrict__ gidx, int64_t n, in
     }
     __syncthreads();
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-        int32_t run = table[(int64_t)blockIdx.x * nb + b];
+        int32_t run = start[b] + table[(int64_t)blockIdx.x * nb + b];
         for (int w = 0; w < 8; ++w) {
             const int32_t c = cnt[w * nb + b];
             cnt[w * nb + b] = run;
@@ -441,18 +464,21 @@ bf_status route(bf_plan_t p, const int32_t *gidx, int64_t n, int32_t *perm, int3
     if ((n + tile - 1) / tile > max_tiles) tile = (n + max_tiles - 1) / max_tiles;
     tile = (tile + kRouteThreads - 1) / kRouteThreads * kRouteThreads;
     const int64_t P = (n + tile - 1) / tile;
-    if ((s = grow(&p->table, &p->table_cap, P * (G + 1), "routing table")) != BF_OK) return s;
+    // table [P][G + 1] of per-tile bin counts, then the G + 1 bin totals
+    if ((s = grow(&p->table, &p->table_cap, (P + 1) * (G + 1), "routing table")) != BF_OK) return s;
+    int32_t *bin_tot = p->table + P * (G + 1);
     if ((s = grow(&p->err, &p->err_cap, 1, "routing flag")) != BF_OK) return s;
     BF_CUDA(cudaMemsetAsync(p->err, 0, sizeof(int32_t), st));
     const size_t hist_smem = (G + 1) * sizeof(int32_t);
     bf_route_hist<<<(unsigned)P, kRouteThreads, hist_smem, st>>>(gidx, n, G, (int)tile,
                                                                   p->table, p->err);
     if ((s = launched(p, "bf_route_hist launch")) != BF_OK) return s;
-    bf_route_scan<<<1, 1024, 0, st>>>(p->table, (int)P, G, n, offsets);
-    if ((s = launched(p, "bf_route_scan launch")) != BF_OK) return s;
-    const size_t sc_smem = 8 * (G + 1) * sizeof(int32_t);
+    bf_route_colscan<<<(unsigned)(G + 1), 1024, 0, st>>>(p->table, (int)P, G, bin_tot);
+    if ((s = launched(p, "bf_route_colscan launch")) != BF_OK) return s;
+    const size_t sc_smem = 9 * (G + 1) * sizeof(int32_t);
     bf_route_scatter<<<(unsigned)P, kRouteThreads, sc_smem, st>>>(gidx, n, G, (int)tile,
-                                                                    p->table, perm);
+                                                                    p->table, bin_tot, perm,
+                                                                    offsets);
     if ((s = launched(p, "bf_route_scatter launch")) != BF_OK) return s;
     return BF_OK;
 }
