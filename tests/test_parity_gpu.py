@@ -679,3 +679,50 @@ def test_c5_batched_windows_sampled():
                           what=f"c5 window {w} chunk {c} (f={f})")
     for pl in plans:
         pl.close()
+
+
+def test_apply_batch_in_cuda_graph():
+    """bf_apply_batch and bf_route captured into a CUDA graph (as the c5 bench runs them):
+    replays reproduce the eager results bitwise, also after the inputs change in place."""
+    plans, jobs, eager = [], [], []
+    for i, f in enumerate((36, 5, 17)):
+        pl = Plan(f=f)
+        pl.set_precoders(torch.from_numpy(syn.precoders(51, i, 7, 64, f, "unit_columns")).to(DEV))
+        S = torch.from_numpy(syn.qam_symbols(51, i, np.arange(999), f, 60, 64)).to(DEV)
+        T = torch.from_numpy(syn.subband_tags(51, np.arange(999) + i, 7)).to(DEV)
+        perm = torch.empty(999, dtype=torch.int32, device=DEV)
+        offs = torch.empty(9, dtype=torch.int32, device=DEV)
+        R = torch.empty((999, 64, 60), dtype=torch.complex64, device=DEV)
+        plans.append(pl)
+        jobs.append((pl, S, perm, offs, R, T))
+    side = torch.cuda.Stream()
+
+    def step():
+        for pl, S, perm, offs, R, T in jobs:
+            pl.route_into(T, perm, offs)
+        bf.apply_batch([(pl, S, perm, offs, R) for pl, S, perm, offs, R, _ in jobs])
+
+    with torch.cuda.stream(side):
+        step()
+    torch.cuda.synchronize()
+    eager = [j[4].clone() for j in jobs]
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        step()
+    for j in jobs:
+        j[4].zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    for j, e in zip(jobs, eager):
+        assert_bitwise(j[4].cpu().numpy(), e.cpu().numpy(), "graph replay")
+    jobs[1][1].mul_(-1)                      # S of job 1 changes in place: the replay follows
+    g.replay()
+    torch.cuda.synchronize()
+    replayed = jobs[1][4].clone()
+    with torch.cuda.stream(side):
+        step()
+    torch.cuda.synchronize()
+    assert_bitwise(replayed.cpu().numpy(), jobs[1][4].cpu().numpy(), "replay after S *= -1")
+    assert not torch.equal(replayed, eager[1])
+    for pl in plans:
+        pl.close()
