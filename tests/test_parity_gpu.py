@@ -726,3 +726,25 @@ def test_apply_batch_in_cuda_graph():
     assert not torch.equal(replayed, eager[1])
     for pl in plans:
         pl.close()
+
+
+def test_non_finite_inputs_stay_local(variant):
+    """A NaN or Inf in S[n][k][j] makes exactly column j of block n non-finite (for every
+    antenna with W[i][k] != 0) and leaves every other element equal to the clean run
+    (reading R16: IEEE propagation, no cross-talk).  Non-finite values are
+    outside the accuracy contract; the tensor path turns an Inf into NaN (its split
+    subtracts S1 from S), the FFMA path keeps IEEE infinities where they arise."""
+    f = 9
+    W = syn.precoders(61, 0, 1, 64, f, "unit_columns")
+    S = syn.qam_symbols(61, 0, np.arange(20), f, 60, 16)
+    clean = run_plan(W, S, variant=variant)
+    bad = S.copy()
+    bad[3, 2, 7] = complex(np.nan, 0.0)
+    bad[11, 8, 59] = complex(np.inf, 1.0)
+    got = run_plan(W, bad, variant=variant)
+    mask = np.zeros(got.shape, bool)
+    mask[3, :, 7] = True
+    mask[11, :, 59] = True
+    assert not np.isfinite(got[mask].view(np.float32)).all()
+    assert not np.isfinite(got[3, :, 7]).any()
+    assert_bitwise(np.where(mask, 0, got), np.where(mask, 0, clean), "unaffected elements")
