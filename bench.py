@@ -476,10 +476,16 @@ def run_filter(args, wl, world, rank, local, dev):
 
         import oracle
         thr = oracle.max_threads()
-        nb = max(thr, 32)
+        taps = syn.filter_taps(wl.n)
+        nb = max(thr, 32)                  # probe, then a sample sized to ~--cpu-seconds
+        t0 = _t.perf_counter()
+        oracle.filter_apply(syn.filter_signals(wl.seed, 0, np.arange(nb), wl.n, wl.M), taps,
+                            n_threads=thr)
+        per = (_t.perf_counter() - t0) / nb
+        nb = int(min(wl.n_signals, max(nb, args.cpu_seconds / max(per, 1e-9))))
         ss = syn.filter_signals(wl.seed, 0, np.arange(nb), wl.n, wl.M)
         t0 = _t.perf_counter()
-        oracle.filter_apply(ss, syn.filter_taps(wl.n), n_threads=thr)
+        oracle.filter_apply(ss, taps, n_threads=thr)
         dt = _t.perf_counter() - t0
         cpu = {"value": nb * wl.n / dt, "unit": "samples/s", "cores": thr, "kind": "oracle",
                "sample": f"{nb} signals of {wl.name} ({dt:.1f} s, fp64 O(n^2) DFTs)"}

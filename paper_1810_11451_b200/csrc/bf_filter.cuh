@@ -127,57 +127,79 @@ __device__ __forceinline__ void dft16(float2 (&v)[16]) {
     for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
 }
 
-// One forward FFT of the CTA's signal (radix 16, 16, 8 Stockham).
-// In: v[q] = x[t + 128 q].  Out: v[q] = X[t + 128 q].
-__device__ __forceinline__ void fft2048(float2 (&v)[16], float2 *sm, const float2 *tw,
+// NS forward FFTs of the CTA's NS signals at once (radix 16, 16, 8 Stockham): the
+// signals' instruction streams interleave (independent chains for the schedulers)
+// and share each pass's barriers.  In: v[s][q] = x_s[t + 128 q].  Out: v[s][q] =
+// X_s[t + 128 q].  sm holds NS exchange buffers of kPad slots.
+template <int NS>
+__device__ __forceinline__ void fft2048(float2 (&v)[NS][16], float2 *sm, const float2 *tw,
                                         const float4 *__restrict__ tw3, int t) {
     // pass 1: Ns = 1, R = 16 (no twiddles); y[16 j + r]
-    dft16(v);
 #pragma unroll
-    for (int r = 0; r < 16; r += 2) {
-        const float2 a = v[tr16(r)], b = v[tr16(r + 1)];
-        *reinterpret_cast<float4 *>(sm + pad(16 * t + r)) = make_float4(a.x, a.y, b.x, b.y);
+    for (int s = 0; s < NS; ++s) {
+        dft16(v[s]);
+#pragma unroll
+        for (int r = 0; r < 16; r += 2) {
+            const float2 a = v[s][tr16(r)], b = v[s][tr16(r + 1)];
+            *reinterpret_cast<float4 *>(sm + s * kPad + pad(16 * t + r)) = make_float4(a.x, a.y, b.x, b.y);
+        }
     }
     __syncthreads();
     // pass 2: Ns = 16, R = 16; twiddles w^(8 r k), k = j mod 16; y[(j/16) 256 + k + 16 r]
-    {
+    const int k = t & 15;
 #pragma unroll
-        for (int r = 0; r < 16; ++r) v[r] = sm[pad(t + 128 * r)];
-        const int k = t & 15;
+    for (int s = 0; s < NS; ++s) {
 #pragma unroll
-        for (int r = 1; r < 16; r += 2) {
-            const float4 w = *reinterpret_cast<const float4 *>(tw + kTw2 + k * kTw2Row + (r - 1));
-            v[r] = cmul(v[r], make_float2(w.x, w.y));
-            if (r + 1 < 16) v[r + 1] = cmul(v[r + 1], make_float2(w.z, w.w));
-        }
-        dft16(v);
-        __syncthreads();
-        const int base = (t >> 4) * 256 + k;
-#pragma unroll
-        for (int r = 0; r < 16; ++r) sm[pad(base + 16 * r)] = v[tr16(r)];
-        __syncthreads();
+        for (int r = 0; r < 16; ++r) v[s][r] = sm[s * kPad + pad(t + 128 * r)];
     }
+#pragma unroll
+    for (int r = 1; r < 16; r += 2) {
+        const float4 w = *reinterpret_cast<const float4 *>(tw + kTw2 + k * kTw2Row + (r - 1));
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            v[s][r] = cmul(v[s][r], make_float2(w.x, w.y));
+            if (r + 1 < 16) v[s][r + 1] = cmul(v[s][r + 1], make_float2(w.z, w.w));
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < NS; ++s) dft16(v[s]);
+    __syncthreads();
+    const int base = (t >> 4) * 256 + k;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) sm[s * kPad + pad(base + 16 * r)] = v[s][tr16(r)];
+    }
+    __syncthreads();
     // pass 3: Ns = 256, R = 8, butterflies j = t and t + 128; twiddles w^(r j); y[j + 256 r]
-    {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            v[2 * r] = sm[pad(t + 256 * r)];
-            v[2 * r + 1] = sm[pad(t + 128 + 256 * r)];
+            v[s][2 * r] = sm[s * kPad + pad(t + 256 * r)];
+            v[s][2 * r + 1] = sm[s * kPad + pad(t + 128 + 256 * r)];
         }
-#pragma unroll
-        for (int r = 1; r < 8; ++r) {
-            const float4 w = __ldg(tw3 + (r - 1) * 128 + t);
-            v[2 * r] = cmul(v[2 * r], make_float2(w.x, w.y));
-            v[2 * r + 1] = cmul(v[2 * r + 1], make_float2(w.z, w.w));
-        }
-        dft8<2>(v);        // butterfly t:       v[0], v[2], ..., v[14]
-        dft8<2>(v + 1);    // butterfly t + 128: v[1], v[3], ..., v[15]
-        __syncthreads();   // shared memory free for the next transform
-        // X[t + 256 r] = v[2 r], X[t + 128 + 256 r] = v[2 r + 1]  ->  v[q] = X[t + 128 q]
     }
+#pragma unroll
+    for (int r = 1; r < 8; ++r) {
+        const float4 w = __ldg(tw3 + (r - 1) * 128 + t);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            v[s][2 * r] = cmul(v[s][2 * r], make_float2(w.x, w.y));
+            v[s][2 * r + 1] = cmul(v[s][2 * r + 1], make_float2(w.z, w.w));
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        dft8<2>(v[s]);        // butterfly t:       v[0], v[2], ..., v[14]
+        dft8<2>(v[s] + 1);    // butterfly t + 128: v[1], v[3], ..., v[15]
+    }
+    __syncthreads();          // shared memory free for the next transform
+    // X[t + 256 r] = v[2 r], X[t + 128 + 256 r] = v[2 r + 1]  ->  v[q] = X[t + 128 q]
 }
 
-constexpr int kSmemBytes = (kN + kPad + kTwS) * 8 + 8;   // dynamic shared memory
+constexpr int kNS = 2;        // signals per CTA iteration
+constexpr int kSmemBytes = (kNS * kN + kNS * kPad + kTwS) * 8 + 8;   // dynamic shared memory
 
 struct FParams {
     const float2 *s;     // [n_sig][2048]
@@ -191,14 +213,14 @@ struct FParams {
                          // 2: forward FFT scaled by 1/N (builds the plan's H from h)
 };
 
-__global__ void __launch_bounds__(kThreads, 5) filter_kernel(const FParams p) {
-    // sm: exchange buffer; stage: the next signal, prefetched with one TMA bulk copy
-    // (16 KB) while the current one is transformed.  Twiddles and H are read
-    // through L1 (__ldg): every CTA on the SM shares the same 32 KB.
+__global__ void __launch_bounds__(kThreads, 3) filter_kernel(const FParams p) {
+    // stage: the CTA's next kNS signals, prefetched with TMA bulk copies (16 KB each)
+    // while the current ones are transformed; sm: kNS exchange buffers.  H and the
+    // pass-3 twiddles are read through L1 (shared by the CTAs of an SM).
     extern __shared__ __align__(128) unsigned char fsm[];
-    float2 *stage = reinterpret_cast<float2 *>(fsm);                 // kN
-    float2 *sm = stage + kN;                                           // kPad
-    float2 *tws = sm + kPad;                                           // kTwS
+    float2 *stage = reinterpret_cast<float2 *>(fsm);                 // kNS x kN
+    float2 *sm = stage + kNS * kN;                                     // kNS x kPad
+    float2 *tws = sm + kNS * kPad;                                     // kTwS
     uint64_t *barp = reinterpret_cast<uint64_t *>(tws + kTwS);
     uint64_t &bar = *barp;
     const int t = threadIdx.x;
@@ -212,47 +234,61 @@ __global__ void __launch_bounds__(kThreads, 5) filter_kernel(const FParams p) {
     }
     __syncthreads();
     const uint64_t pol = bfk::policy_evict_first();
-    int64_t sig = blockIdx.x;
-    if (t == 0 && sig < p.n_sig) {
-        bfk::mbar_arrive_expect_tx(&bar, kN * 8);
-        bfk::bulk_g2s(stage, p.s + sig * kN, kN * 8, &bar, pol);
-    }
+    const int64_t G = gridDim.x;
+    // signals of iteration base: base + s G, s < kNS
+    auto prefetch = [&](int64_t base) {
+        int cnt = 0;
+        for (int s = 0; s < kNS; ++s) cnt += base + s * G < p.n_sig;
+        if (cnt == 0) return;
+        bfk::mbar_arrive_expect_tx(&bar, (uint32_t)(cnt * kN * 8));
+        for (int s = 0; s < kNS; ++s)
+            if (base + s * G < p.n_sig)
+                bfk::bulk_g2s(stage + s * kN, p.s + (base + s * G) * kN, kN * 8, &bar, pol);
+    };
+    if (t == 0) prefetch(blockIdx.x);
     constexpr float inv_n = 1.0f / kN;
     uint32_t phase = 0;
-    for (; sig < p.n_sig; sig += gridDim.x) {
-        float2 *dst = p.y + sig * kN;
-        float2 v[16];
+    for (int64_t base = blockIdx.x; base < p.n_sig; base += kNS * G) {
+        float2 v[kNS][16];
         bfk::mbar_wait(&bar, phase);
         phase ^= 1u;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = stage[t + 128 * q];
-        __syncthreads();                                  // stage consumed by every thread
-        const int64_t nxt = sig + gridDim.x;
-        if (t == 0 && nxt < p.n_sig) {
-            bfk::mbar_arrive_expect_tx(&bar, kN * 8);
-            bfk::bulk_g2s(stage, p.s + nxt * kN, kN * 8, &bar, pol);
+        for (int s = 0; s < kNS; ++s) {
+            const bool ok = base + s * G < p.n_sig;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[s][q] = ok ? stage[s * kN + t + 128 * q] : make_float2(0.f, 0.f);
         }
+        __syncthreads();                                  // stage consumed by every thread
+        if (t == 0) prefetch(base + kNS * G);
         // forward FFT, MULT by H, inverse FFT as conj(FFT(conj(.))) / N — one copy of
         // the transform code in a two-trip loop keeps register pressure at one FFT's.
         // The plan stores H / N (exact: N = 2^11), so the 1/N costs nothing here.
         const int trips = p.mode == 0 ? 2 : 1;
 #pragma unroll 1
         for (int trip = 0; trip < trips; ++trip) {
-            fft2048(v, sm, tws, p.tw3, t);
+            fft2048<kNS>(v, sm, tws, p.tw3, t);
             if (trip == 0 && trips == 2) {
 #pragma unroll
-                for (int q = 0; q < 16; ++q) v[q] = conj2(cmul(v[q], __ldg(p.H + t + 128 * q)));
+                for (int q = 0; q < 16; ++q) {
+                    const float2 h = __ldg(p.H + t + 128 * q);
+#pragma unroll
+                    for (int s = 0; s < kNS; ++s) v[s][q] = conj2(cmul(v[s][q], h));
+                }
             }
         }
-        if (p.mode == 0) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) v[q] = conj2(v[q]);
-        } else if (p.mode == 2) {
+        for (int s = 0; s < kNS; ++s) {
+            const int64_t sig = base + s * G;
+            if (sig >= p.n_sig) break;
+            float2 *dst = p.y + sig * kN;
 #pragma unroll
-            for (int q = 0; q < 16; ++q) v[q] = make_float2(v[q].x * inv_n, v[q].y * inv_n);
+            for (int q = 0; q < 16; ++q) {
+                float2 o = v[s][q];
+                if (p.mode == 0) o = conj2(o);
+                else if (p.mode == 2) o = make_float2(o.x * inv_n, o.y * inv_n);
+                __stcs(dst + t + 128 * q, o);
+            }
         }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) __stcs(dst + t + 128 * q, v[q]);
     }
 }
 
