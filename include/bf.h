@@ -174,19 +174,20 @@ typedef struct {
  * over several precoder sets at once, e.g. consecutive streaming chunks of
  * different cells).  Equivalent to calling
  * bf_apply_routed for jobs[0..n_jobs) in order on `stream`, with bitwise equal
- * results — for plans whose AUTO choice is the FFMA kernel (small f), equal to
- * the same call with the plan set to BF_VARIANT_TENSOR; jobs are packed into
- * tensor-core launches of up to 16 jobs (each
- * job split over every CTA, so one kernel fill and drain is paid per pack instead
- * of per job).  Plans with BF_VARIANT_AUTO or _TENSOR join the packed tensor-core
- * launches whatever their f; f = 0 jobs and plans set to BF_VARIANT_FFMA run as
- * their own applies.  Every plan must live on one device and share job 0's layout; the
- * grid follows job 0's plan (bf_plan_set_sm_share), and its profiling record and
- * launch count take the packed launches.  Every job is validated before anything
- * is enqueued (BF_ERR_INVALID_VALUE / BF_ERR_MISALIGNED naming the job); a tagged
- * job whose plan has more than 1026 groups is BF_ERR_UNSUPPORTED.  n_jobs == 0 is a
- * no-op.  Jobs may share a plan (read-only), but a job's R must not overlap
- * another job's S or R (precondition, not checked). */
+ * results (for a plan whose AUTO choice is the FFMA kernel, equal to that call
+ * with the plan set to BF_VARIANT_TENSOR).
+ *   Packing: jobs whose plan is BF_VARIANT_AUTO or _TENSOR (any f >= 1) go into
+ *   tensor-core launches of up to 16 jobs, each job split over every CTA, so one
+ *   kernel fill and drain is paid per pack instead of per job; f = 0 jobs and
+ *   plans set to BF_VARIANT_FFMA run as their own applies, in order.
+ *   Grid, profiling record and launch count follow job 0's plan
+ *   (bf_plan_set_sm_share, bf_plan_set_profiling).
+ *   Every plan must live on one device and share job 0's layout.  Every job is
+ *   validated before anything is enqueued (BF_ERR_INVALID_VALUE /
+ *   BF_ERR_MISALIGNED naming the job); a tagged job whose plan has more than
+ *   1026 groups is BF_ERR_UNSUPPORTED.  n_jobs == 0 is a no-op.  Jobs may share
+ *   a plan (read-only), but a job's R must not overlap another job's S or R
+ *   (precondition, not checked). */
 bf_status bf_apply_batch(const bf_batch_job *jobs, int n_jobs, void *stream);
 
 /* Free the plan and everything it owns.  Call after its work has drained. */
@@ -214,12 +215,11 @@ bf_status bf_plan_set_host_chunk(bf_plan_t p, int64_t blocks);
 
 /* Number of SMs the beamforming kernel of later applies spreads over
  * (grid = sms x resident CTAs per SM, capped by the block count); 0 = every SM
- * of the device (the default), values above the SM count are clamped.  For
- * several plans applied concurrently on their own streams (e.g. one plan per
- * cell): giving each plan a share proportional to
- * its work lets the kernels run side by side instead of each one filling and
- * draining the whole GPU.  Never changes results (the block -> CTA split does
- * not enter the arithmetic).  BF_ERR_INVALID_VALUE if sms < 0. */
+ * of the device (the default), values above the SM count are clamped.  Keeps
+ * SMs free for concurrent work on other streams (the c5 bench leaves 2 SMs to
+ * its single-CTA routing kernels) or lets several plans share the GPU.  Never
+ * changes results (the block -> CTA split does not enter the arithmetic).
+ * BF_ERR_INVALID_VALUE if sms < 0. */
 bf_status bf_plan_set_sm_share(bf_plan_t p, int sms);
 
 /* Static description of the kernel chosen for this plan: grid and block size
