@@ -276,7 +276,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 
 // DBG (0 in the library) disables pieces for bottleneck experiments only
 // (tools/tc_exp): 1 = no MMA issue, 2 = no R stores, 4 = no split/tcgen05.st,
-// 8 = no S loads.  Results are wrong with DBG != 0.
+// 8 = no S loads, 16 = main product as fp16-kind MMAs (energy experiment).
+// Results are wrong with DBG != 0.
 template <int F, int LAYOUT, int DBG = 0>
 __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
     using L = TcSmem<F>;
@@ -554,14 +555,20 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
                 const bool run = grp != 1 || exact;
                 const bool bf16 = grp == 0 && !exact;
                 if (lane == 0) {
+                    // DBG & 16 (energy experiment): the S1 W1 group as ceil(KP / 16)
+                    // fp16-kind K = 16 MMAs on the same (reinterpreted) operands
+                    const int nkb = ((DBG & 16) && grp == 2) ? (KP + 15) / 16 : KP / 8;
                     if (run) {
 #pragma unroll
-                        for (int kb = 0; kb < KP / 8; ++kb) {
+                        for (int kb = 0; kb < nkb; ++kb) {
                             const uint64_t desc = tc::smem_desc(
                                 w_base + (uint32_t)(((bf16 ? KP / 4 : 0) + 2 * kb) * 16 * 128),
                                 16 * 128, 128);
                             if constexpr (!(DBG & 1)) {
-                                if (bf16)
+                                if ((DBG & 16) && grp == 2)
+                                    tc::mma_bf16_ts(d, tmem + at * kARegion + kb * 8, desc,
+                                                    idesc_c & ~((7u << 7) | (7u << 10)), kb != 0);
+                                else if (bf16)
                                     tc::mma_bf16_ts(d, tmem + at * kARegion + kb * 8, desc, idesc_c,
                                                     kb != 0);
                                 else
