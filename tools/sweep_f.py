@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--layout", default="interleaved")
     ap.add_argument("--flows", default=",".join(str(f) for f in syn.C3_FLOWS))
+    ap.add_argument("--variants", default="ffma,tensor")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     peaks = benchkit.measured_peaks()
@@ -44,7 +45,7 @@ def main():
         n = min(a.blocks, wl.n_blocks)
         S, _ = sync.workload_device(wl, dev, n=n, planar=planar)
         W = syn.precoders(wl.seed, wl.sub, 1, 64, f, wl.w_norm)
-        for variant in (["ffma", "tensor"] if f > 0 else ["auto"]):
+        for variant in (a.variants.split(",") if f > 0 else ["auto"]):
             plan = bf.Plan(f=f, layout=a.layout, variant=variant)
             plan.set_precoders(torch.from_numpy(syn.to_planar(W) if planar else W).to(dev))
             R = torch.empty(plan.r_shape(n), dtype=plan.r_dtype, device=dev)
