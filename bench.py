@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--config", default="c4", help="c2 | c3 | c4 (default) | c5")
     ap.add_argument("--f", type=int, default=36, help="flow count for --config c3")
     ap.add_argument("--layout", default="interleaved",
-                    choices=["interleaved", "planar", "interleaved_f16out"])
+                    choices=["interleaved", "planar", "interleaved_f16out", "interleaved_i16out"])
     ap.add_argument("--variant", default="auto", choices=["auto", "ffma", "tensor"],
                     help="kernel variant (auto = libbf's measured per-f table)")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -296,7 +296,7 @@ def run_ours(args):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_max = benchkit.fp32_peak_tflops(sms, peaks.get("sm_max_mhz", 1965.0))
     flops_launch = wl.block_flops * n_local
-    r_blk = 15360 if args.layout == "interleaved_f16out" else 30720
+    r_blk = 15360 if args.layout in ("interleaved_f16out", "interleaved_i16out") else 30720
     blk_bytes = 480 * wl.f + r_blk
     bytes_launch = blk_bytes * n_local
     achieved_tf = flops_launch / (kern_avg_ms * 1e-3) / 1e12
@@ -313,7 +313,7 @@ def run_ours(args):
     traffic, traffic_basis = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     kname = f"{'bf_tc_kernel' if plan.variant.name == 'TENSOR' else 'bf_ffma_kernel'}" \
-            f"<{wl.f},{1 if planar else 0}>"
+            f"<{wl.f},{int(plan.layout)}>"
     if os.path.exists(tpath):
         try:
             tr = json.load(open(tpath)).get(kname)
@@ -335,7 +335,7 @@ def run_ours(args):
                 "fp32_equivalent": {"achieved": achieved_tf, "unit": "TFLOP/s",
                                     "frac_of_derived_fp32_peak": achieved_tf / peak_max}}
     roof["kernel"] = "cudaMemsetAsync (f = 0: R := +0)" if memset_only else \
-        f"{'bftc::bf_tc_kernel' if variant == 'tensor' else 'bfk::bf_ffma_kernel'}<{wl.f},{1 if planar else 0}>"
+        f"{'bftc::bf_tc_kernel' if variant == 'tensor' else 'bfk::bf_ffma_kernel'}<{wl.f},{int(plan.layout)}>"
     roof["variant"] = variant
     if clk and clk.get("sm_mhz"):
         roof["frac_at_observed_clock"] = achieved_tf / benchkit.fp32_peak_tflops(sms, clk["sm_mhz"]) \

@@ -29,6 +29,7 @@
  *                          R [n_blocks][2][n_ant][b]
  *   Both layouts move the same bytes per block: S 8*f*b, R 8*n_ant*b.
  *   BF_LAYOUT_INTERLEAVED_F16OUT: as interleaved, R in fp16 pairs (4*n_ant*b).
+ *   BF_LAYOUT_INTERLEAVED_I16OUT: as interleaved, R in int16 pairs (4*n_ant*b).
  *
  * Supported domain: n_ant == 64, b == 60, 0 <= f <= 36, 1 <= n_groups <= 1024,
  * 0 <= n_blocks < 2^31.  Other shapes return BF_ERR_UNSUPPORTED (there is no
@@ -80,7 +81,13 @@ typedef enum {
      * once (round-to-nearest-even) from the fp32 result: 15,360 bytes per block
      * instead of 30,720 (reduced-precision fronthaul
      * output).  Accuracy: |R16 - R_exact| <= sqrt(2) 2^-11 |R_exact| + 1e-5 T. */
-    BF_LAYOUT_INTERLEAVED_F16OUT = 2
+    BF_LAYOUT_INTERLEAVED_F16OUT = 2,
+    /* W and S as BF_LAYOUT_INTERLEAVED, R written as interleaved int16 (re, im)
+     * fronthaul samples [n_blocks][n_ant][b]: round-to-nearest-even of R x 2^e from
+     * the fp32 result, saturated to [-32768, 32767], NaN -> 0 (SURVEY.md §8(f) row 4,
+     * "int16 fronthaul samples"); e = bf_plan_set_output_exponent, default 12.
+     * 15,360 bytes per block. */
+    BF_LAYOUT_INTERLEAVED_I16OUT = 3
 } bf_layout;
 
 /* Kernel variant.  Both compute the same product within the same contract.
@@ -212,6 +219,10 @@ bf_status bf_plan_get_variant(bf_plan_t p, int *resolved);
 
 /* Chunk size (blocks) of bf_apply_host's pipeline; 0 selects the default. */
 bf_status bf_plan_set_host_chunk(bf_plan_t p, int64_t blocks);
+
+/* int16 output layout: later applies write sat(rne(R x 2^e)); e in [-64, 64]
+ * (BF_ERR_INVALID_VALUE otherwise), default 12.  No effect on other layouts. */
+bf_status bf_plan_set_output_exponent(bf_plan_t p, int e);
 
 /* Number of SMs the beamforming kernel of later applies spreads over
  * (grid = sms x resident CTAs per SM, capped by the block count); 0 = every SM

@@ -17,6 +17,7 @@ EXPORTS = ("bf_plan_create", "bf_set_precoders", "bf_apply", "bf_apply_host", "b
            "bf_destroy", "bf_plan_set_profiling", "bf_plan_kernel_time",
            "bf_plan_launch_count", "bf_plan_set_host_chunk", "bf_plan_kernel_config",
            "bf_plan_set_variant", "bf_plan_get_variant", "bf_plan_set_sm_share",
+           "bf_plan_set_output_exponent",
            "bff_plan_create", "bff_set_taps", "bff_apply", "bff_fft", "bff_destroy",
            "bff_plan_set_profiling", "bff_plan_kernel_time", "bff_plan_launch_count",
            "bf_status_string", "bf_last_error", "bf_version")
@@ -37,6 +38,7 @@ class Layout(enum.IntEnum):
     INTERLEAVED = 0
     PLANAR = 1
     INTERLEAVED_F16OUT = 2    # R as fp16 (re, im) pairs
+    INTERLEAVED_I16OUT = 3    # R as int16 (re, im) fronthaul samples, x 2^e
 
 
 class Variant(enum.IntEnum):
@@ -86,6 +88,7 @@ def lib() -> ctypes.CDLL:
         "bf_plan_set_host_chunk": (i32, [vp, i64]),
         "bf_plan_set_variant": (i32, [vp, i32]),
         "bf_plan_set_sm_share": (i32, [vp, i32]),
+        "bf_plan_set_output_exponent": (i32, [vp, i32]),
         "bf_plan_get_variant": (i32, [vp, P(i32)]),
         "bf_plan_kernel_config": (i32, [vp, i64, P(i32), P(i32), P(i32), P(i32)]),
         "bf_status_string": (ctypes.c_char_p, [i32]),

@@ -38,6 +38,7 @@ constexpr int kRouteThreads = 256;         // 8 warps
 constexpr int kRouteMinTile = 512;          // small batches still spread over several CTAs
 constexpr int kRouteMaxTable = 65536;      // tiles x (groups + 1) entries
 constexpr int64_t kDefaultHostChunk = 2048;
+constexpr int kDefaultOutExp = 12;          // int16 output: |R| < 8 fits, 2^-12 resolution
 constexpr int kHostSlots = 3;
 constexpr size_t kMaxProfEvents = 1 << 16;  // timed launches kept between kernel_time() calls
 // AUTO variant table, per layout (measured with
@@ -48,7 +49,7 @@ constexpr size_t kMaxProfEvents = 1 << 16;  // timed launches kept between kerne
 // planar f <= 10 (FFMA up to 26 % ahead: the tensor epilogue's planar stores,
 // DESIGN.md §6), fp16 output f <= 2.  From there on the tensor kernel wins, by
 // 2.2-2.6x at f = 36.
-constexpr int kAutoTensorMinF[3] = {7, 11, 3};   // [layout]
+constexpr int kAutoTensorMinF[4] = {7, 11, 3, 3};   // [layout] (int16 out: as fp16 out)
 
 BfKernelTable g_table;      // FFMA kernels [f][layout]
 BfKernelTable g_table_tc;   // tcgen05 split-TF32 kernels [f][layout]
@@ -413,6 +414,7 @@ struct bf_plan_s {
     BfKernelEntry kern_tc{};    // tensor-core kernel of this (f, layout)
     int ctas_per_sm = 0;
     int sm_share = 0;           // bf_plan_set_sm_share (0 = every SM)
+    int out_exp = kDefaultOutExp;   // int16 output: R x 2^out_exp before the rounding
     int variant = BF_VARIANT_AUTO;
     float4 *Wp = nullptr;       // FFMA precoder image
     int64_t Wp_cap = 0;
@@ -539,6 +541,7 @@ bftc::TcJob tc_job(bf_plan_t p, const void *S, const int32_t *perm, const int32_
     j.n_items = n;
     j.n_groups = p->n_groups;
     j.f = p->f;
+    j.out_scale = ldexpf(1.0f, p->out_exp);
     return j;
 }
 
@@ -561,6 +564,7 @@ bf_status apply_routed(bf_plan_t p, const void *S, const int32_t *perm, const in
     kp.n_groups = p->n_groups;
     kp.perm = perm;
     kp.offsets = offsets;
+    kp.out_scale = ldexpf(1.0f, p->out_exp);
     const bool tensor = use_tensor(p);
     const int grid = grid_for(p, n, tensor);
     const BfKernelEntry &kern = tensor ? p->kern_tc : p->kern;
@@ -656,7 +660,7 @@ bf_status validate_layout_and_dims(int n_ant, int f, int b, int layout) {
         return fail(BF_ERR_INVALID_VALUE, "dimensions must satisfy n_ant >= 1, f >= 0, b >= 1 "
                                           "(got n_ant=%d f=%d b=%d)", n_ant, f, b);
     if (layout != BF_LAYOUT_INTERLEAVED && layout != BF_LAYOUT_PLANAR &&
-        layout != BF_LAYOUT_INTERLEAVED_F16OUT)
+        layout != BF_LAYOUT_INTERLEAVED_F16OUT && layout != BF_LAYOUT_INTERLEAVED_I16OUT)
         return fail(BF_ERR_INVALID_VALUE, "unknown layout %d", layout);
     if (n_ant != bfk::kAnt || b != bfk::kB || f > bfk::kMaxF)
         return fail(BF_ERR_UNSUPPORTED, "compiled domain is n_ant=64, b=60, 0<=f<=36 "
@@ -1005,6 +1009,13 @@ bf_status bf_plan_get_variant(bf_plan_t p, int *resolved) {
 bf_status bf_plan_set_host_chunk(bf_plan_t p, int64_t blocks) {
     if (!p || blocks < 0) return fail(BF_ERR_INVALID_VALUE, "invalid chunk");
     p->host_chunk = blocks == 0 ? kDefaultHostChunk : blocks;
+    return BF_OK;
+}
+
+bf_status bf_plan_set_output_exponent(bf_plan_t p, int e) {
+    if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
+    if (e < -64 || e > 64) return fail(BF_ERR_INVALID_VALUE, "output exponent %d outside [-64, 64]", e);
+    p->out_exp = e;
     return BF_OK;
 }
 

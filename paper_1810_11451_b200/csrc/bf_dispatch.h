@@ -8,7 +8,7 @@ struct BfKernelEntry {
     int smem_bytes;      // dynamic shared memory of that instantiation
 };
 
-using BfKernelTable = BfKernelEntry[37][3];   // [f][layout: interleaved, planar, f16 out]
+using BfKernelTable = BfKernelEntry[37][4];   // [f][layout: interleaved, planar, f16 out, i16 out]
                                               // (tensor table f = 0: the batch kernel)
 
 void bf_register_f01_06(BfKernelTable &t, BfKernelTable &tc);

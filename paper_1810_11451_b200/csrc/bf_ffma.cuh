@@ -47,11 +47,22 @@ constexpr int kRBlockFloats = 2 * kAnt * kB;   // 7680 floats = 30,720 B per blo
 // I/O formats (the kernels' LAYOUT parameter; include/bf.h bf_layout):
 //   0 interleaved complex fp32 S/W/R;  1 planar complex fp32 S/W/R;
 //   2 interleaved fp32 S/W, R as interleaved fp16 (re, im) pairs (SURVEY.md §8(f)
-//     row 4: halves the dominant R stream; R rounded once, RN, from fp32).
-__host__ __device__ constexpr int r_block_bytes(int layout) { return layout == 2 ? 15360 : 30720; }
+//     row 4: halves the dominant R stream; R rounded once, RN, from fp32);
+//   3 interleaved fp32 S/W, R as interleaved int16 (re, im) fronthaul samples:
+//     round-to-nearest-even of R x 2^e, saturated to [-32768, 32767] (NaN -> 0).
+__host__ __device__ constexpr bool r_is_16bit(int layout) { return layout == 2 || layout == 3; }
+__host__ __device__ constexpr int r_block_bytes(int layout) { return r_is_16bit(layout) ? 15360 : 30720; }
 __device__ __forceinline__ uint32_t pack_half2(float re, float im) {
     const __half2 h = __floats2half2_rn(re, im);
     return *reinterpret_cast<const uint32_t *>(&h);
+}
+// (sat_rne_s16(re * scale), sat_rne_s16(im * scale)), re in the low half; NaN -> 0.
+// (A clamp + 1.5 x 2^23 magic-add version measured slower in the tensor epilogue.)
+__device__ __forceinline__ uint32_t pack_i16x2(float re, float im, float scale) {
+    short a, b;
+    asm("cvt.rni.sat.s16.f32 %0, %1;" : "=h"(a) : "f"(re * scale));
+    asm("cvt.rni.sat.s16.f32 %0, %1;" : "=h"(b) : "f"(im * scale));
+    return (uint32_t)(uint16_t)a | ((uint32_t)(uint16_t)b << 16);
 }
 
 struct KParams {
@@ -59,9 +70,10 @@ struct KParams {
     const float *S;           // [n_blocks] x 2*F*60 floats
     const int32_t *perm;      // [n_items] block ids (group-sorted) or NULL = identity
     const int32_t *offsets;   // [n_groups + 2] group starts of the sorted order, or NULL = group 0
-    float *R;                 // [n_blocks] x 7680 floats
+    float *R;                 // [n_blocks] x 7680 floats (16-bit layouts: x 3840 words)
     int64_t n_items;
     int n_groups;
+    float out_scale;          // layout 3: 2^e applied before the int16 rounding
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
@@ -274,6 +286,9 @@ __global__ void __launch_bounds__(kThreads, 4) bf_ffma_kernel(const KParams p) {
                     } else if (LAYOUT == 2) {
                         __stcs(reinterpret_cast<unsigned int *>(Rb) + i * kB + j,
                                pack_half2(are[a][r], aim[a][r]));
+                    } else if (LAYOUT == 3) {
+                        __stcs(reinterpret_cast<unsigned int *>(Rb) + i * kB + j,
+                               pack_i16x2(are[a][r], aim[a][r], p.out_scale));
                     } else {
                         __stcs(Rb + i * kB + j, are[a][r]);
                         __stcs(Rb + kAnt * kB + i * kB + j, aim[a][r]);

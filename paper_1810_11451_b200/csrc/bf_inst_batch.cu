@@ -7,4 +7,5 @@ void bf_register_batch(BfKernelTable &tc) {
     tc[0][0] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<0, 0>), bftc::TcSmem<0>::kBytes};
     tc[0][1] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<0, 1>), bftc::TcSmem<0>::kBytes};
     tc[0][2] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<0, 2>), bftc::TcSmem<0>::kBytes};
+    tc[0][3] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<0, 3>), bftc::TcSmem<0>::kBytes};
 }

@@ -12,6 +12,8 @@ static void reg(BfKernelTable &t, BfKernelTable &tc) {
     tc[F][1] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 1>), bftc::TcSmem<F>::kBytes};
     t[F][2] = {reinterpret_cast<const void *>(&bfk::bf_ffma_kernel<F, 2>), bfk::Smem<F>::kBytes};
     tc[F][2] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 2>), bftc::TcSmem<F>::kBytes};
+    t[F][3] = {reinterpret_cast<const void *>(&bfk::bf_ffma_kernel<F, 3>), bfk::Smem<F>::kBytes};
+    tc[F][3] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 3>), bftc::TcSmem<F>::kBytes};
 }
 
 void bf_register_f19_24(BfKernelTable &t, BfKernelTable &tc) {

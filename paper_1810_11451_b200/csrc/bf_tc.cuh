@@ -82,6 +82,7 @@ struct TcJob {
     int64_t n_items;
     int n_groups;
     int f;
+    float out_scale;          // layout 3 (int16 output): 2^e before the rounding
 };
 
 struct TcParams {
@@ -121,7 +122,7 @@ struct JobCtx {
     int g_begin;              // group of begin
     int n_groups, f, kp;
     int wbytes;               // bytes of one group's B image
-    int pad_;
+    float out_scale;          // layout 3: 2^e before the int16 rounding
 };
 static_assert(sizeof(JobCtx) <= 96, "JobCtx slot");
 
@@ -317,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
         J.f = F > 0 ? F : q.f;
         J.kp = kp_of(J.f);
         J.wbytes = 2 * J.kp * 128 * 4;
+        J.out_scale = q.out_scale;
         J.begin = J.end = 0;
         J.g_begin = 0;
     }
@@ -622,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
             // raises the write bandwidth of 4 storing warps (tools/write_bw).
             const bool odd = (j & 1) != 0;
             if constexpr (!(DBG & 2)) {
-                if (LAYOUT == 0 || LAYOUT == 2) {
+                if (LAYOUT == 0 || LAYOUT == 2 || LAYOUT == 3) {
 #pragma unroll
                     for (int aa = 0; aa < 32; aa += 2) {
                         const int a = 32 * h + aa;
@@ -636,6 +638,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
                         if (valid) {
                             if (LAYOUT == 0) {
                                 __stcs(reinterpret_cast<float4 *>(Rb + 2 * e), w4);
+                            } else if (LAYOUT == 3) {   // int16 output: two (re, im) pairs
+                                __stcs(reinterpret_cast<uint2 *>(Rb) + e / 2,
+                                       make_uint2(bfk::pack_i16x2(w4.x, w4.y, J.out_scale),
+                                                  bfk::pack_i16x2(w4.z, w4.w, J.out_scale)));
                             } else {      // fp16 output: two (re, im) half pairs, 8 bytes
                                 __stcs(reinterpret_cast<uint2 *>(Rb) + e / 2,
                                        make_uint2(bfk::pack_half2(w4.x, w4.y),

@@ -57,7 +57,7 @@ class Plan:
     def r_shape(self, n: int):
         if self.layout == Layout.PLANAR:
             return (n, 2, self.n_ant, self.b)
-        if self.layout == Layout.INTERLEAVED_F16OUT:
+        if self.layout in (Layout.INTERLEAVED_F16OUT, Layout.INTERLEAVED_I16OUT):
             return (n, self.n_ant, self.b, 2)
         return (n, self.n_ant, self.b)
 
@@ -71,8 +71,12 @@ class Plan:
 
     @property
     def r_dtype(self):
-        """dtype of R (fp16 (re, im) pairs for INTERLEAVED_F16OUT)."""
-        return torch.float16 if self.layout == Layout.INTERLEAVED_F16OUT else self.dtype
+        """dtype of R (fp16 / int16 (re, im) pairs for the 16-bit output layouts)."""
+        if self.layout == Layout.INTERLEAVED_F16OUT:
+            return torch.float16
+        if self.layout == Layout.INTERLEAVED_I16OUT:
+            return torch.int16
+        return self.dtype
 
     def _check(self, t: torch.Tensor, name: str, shape, device=True, dtype=None):
         dtype = self.dtype if dtype is None else dtype
@@ -184,6 +188,10 @@ class Plan:
         v = ctypes.c_int()
         check(lib().bf_plan_get_variant(self._h, ctypes.byref(v)))
         return Variant(v.value)
+
+    def set_output_exponent(self, e: int) -> None:
+        """bf_plan_set_output_exponent: int16 output = sat(rne(R x 2^e))."""
+        check(lib().bf_plan_set_output_exponent(self._h, int(e)))
 
     def set_sm_share(self, sms: int) -> None:
         """bf_plan_set_sm_share: spread later applies over `sms` SMs (0 = all)."""

@@ -544,7 +544,8 @@ def test_cost_balanced_partition_covers_every_block(n, G, share):
     assert_parity(outs[0], R_ref, T, what=f"partition n={n} G={G}")
 
 
-@pytest.mark.parametrize("layout", [Layout.INTERLEAVED, Layout.PLANAR, Layout.INTERLEAVED_F16OUT])
+@pytest.mark.parametrize("layout", [Layout.INTERLEAVED, Layout.PLANAR, Layout.INTERLEAVED_F16OUT,
+                                    Layout.INTERLEAVED_I16OUT])
 @pytest.mark.parametrize("f", [1, 7, 36])
 def test_no_write_outside_R(f, layout, variant):
     """Out-of-bounds write check (compute-sanitizer is closed on this pool): R is a slice of
@@ -570,7 +571,8 @@ def test_no_write_outside_R(f, layout, variant):
     plan.close()
 
 
-@pytest.mark.parametrize("layout", [Layout.INTERLEAVED, Layout.PLANAR, Layout.INTERLEAVED_F16OUT])
+@pytest.mark.parametrize("layout", [Layout.INTERLEAVED, Layout.PLANAR, Layout.INTERLEAVED_F16OUT,
+                                    Layout.INTERLEAVED_I16OUT])
 def test_apply_batch_equals_routed_applies(layout):
     """bf_apply_batch over 19 jobs (more than one pack of 16): plans of different f, tagged
     and untagged, f = 0, an FFMA-forced plan, an empty job, a plan used twice — bitwise equal
@@ -748,3 +750,60 @@ def test_non_finite_inputs_stay_local(variant):
     assert not np.isfinite(got[mask].view(np.float32)).all()
     assert not np.isfinite(got[3, :, 7]).any()
     assert_bitwise(np.where(mask, 0, got), np.where(mask, 0, clean), "unaffected elements")
+
+
+
+# ---------------------------------------------------------------------------
+# int16 fronthaul output (BF_LAYOUT_INTERLEAVED_I16OUT)
+# ---------------------------------------------------------------------------
+def run_i16(W, S, tags, variant, e=None):
+    plan = Plan(f=W.shape[-1], layout=Layout.INTERLEAVED_I16OUT, variant=variant)
+    if e is not None:
+        plan.set_output_exponent(e)
+    plan.set_precoders(torch.from_numpy(np.ascontiguousarray(W)).to(DEV))
+    R = plan.apply(torch.from_numpy(np.ascontiguousarray(S)).to(DEV),
+                   None if tags is None else torch.from_numpy(tags).to(DEV))
+    torch.cuda.synchronize()
+    plan.close()
+    return R.cpu().numpy()
+
+
+def host_i16(R32, e):
+    """sat(rne(R x 2^e)) per component, NaN -> 0 (the layout's definition, bf.h)."""
+    out = []
+    for comp in (R32.real, R32.imag):
+        x = comp.astype(np.float64) * 2.0 ** e
+        x = np.where(np.isnan(x), 0.0, np.rint(x))
+        out.append(np.clip(x, -32768, 32767).astype(np.int16))
+    return np.stack(out, axis=-1)
+
+
+@pytest.mark.parametrize("e", [None, 3, 20])
+def test_i16_output_is_the_fp32_result_rounded_and_saturated(e, variant):
+    """R16 equals the same kernel's fp32 result times 2^e, rounded to nearest-even and
+    saturated (e = 20 saturates most samples), exactly; the default exponent is 12."""
+    wl = syn.workload("c4")
+    W, S, tags = syn.workload_inputs(wl, np.arange(501))
+    R16 = run_i16(W, S, tags, variant, e)
+    R32 = run_plan(W, S, tags, variant=variant)
+    assert np.array_equal(R16, host_i16(R32, 12 if e is None else e))
+    if e == 20:
+        assert (np.abs(R16.astype(np.int32)) >= 32767).mean() > 0.5
+
+
+def test_i16_identity_reproduces_integer_samples(variant):
+    """Identity W on S holding integers / 2^12: the int16 output is those integers exactly."""
+    f = 8
+    rng = np.random.default_rng(5)
+    S = (rng.integers(-2000, 2000, size=(9, f, 60)) + 1j * rng.integers(-2000, 2000, size=(9, f, 60)))
+    S = (S / 4096.0).astype(np.complex64)
+    W = np.zeros((1, 64, f), np.complex64)
+    W[0, np.arange(f), np.arange(f)] = 1
+    R16 = run_i16(W, S, None, variant)
+    assert np.array_equal(R16[:, :f, :, 0], np.rint(S.real * 4096).astype(np.int16))
+    assert np.array_equal(R16[:, :f, :, 1], np.rint(S.imag * 4096).astype(np.int16))
+    assert not R16[:, f:].any()
+    p = Plan(f=f, layout=Layout.INTERLEAVED_I16OUT)
+    with pytest.raises(bf.BfError):
+        p.set_output_exponent(65)
+    p.close()
