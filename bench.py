@@ -173,6 +173,46 @@ def host_ram_available() -> int:
     return 0
 
 
+def pcie_probe(torch, dev, nbytes: int = 1 << 30, reps: int = 4) -> dict:
+    """Pinned H2D and D2H copy bandwidth, each direction alone and both concurrently (two
+    streams, CUDA events).  The alone figures bound an e2e step whose copies overlap each
+    other and the kernels from above."""
+    hs = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    hr = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d1 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def run(h2d: bool, d2h: bool, n: int):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        torch.cuda.synchronize(dev)
+        if h2d:
+            with torch.cuda.stream(s1):
+                ev[0].record(s1)
+                for _ in range(n):
+                    d1.copy_(hs, non_blocking=True)
+                ev[1].record(s1)
+        if d2h:
+            with torch.cuda.stream(s2):
+                ev[2].record(s2)
+                for _ in range(n):
+                    hr.copy_(d2, non_blocking=True)
+                ev[3].record(s2)
+        torch.cuda.synchronize(dev)
+        gbs = lambda a, b: n * nbytes / (a.elapsed_time(b) * 1e-3) / 1e9  # noqa: E731
+        return (gbs(ev[0], ev[1]) if h2d else None), (gbs(ev[2], ev[3]) if d2h else None)
+
+    run(True, True, 1)                         # warm-up
+    h2d_alone, _ = run(True, False, reps)
+    _, d2h_alone = run(False, True, reps)
+    h2d_conc, d2h_conc = run(True, True, reps)
+    del hs, hr, d1, d2
+    return {"h2d_gbs": h2d_alone, "d2h_gbs": d2h_alone,
+            "h2d_gbs_concurrent": h2d_conc, "d2h_gbs_concurrent": d2h_conc,
+            "how": f"pinned copies, {nbytes >> 20} MiB x {reps}, each direction alone and both "
+                   "at once on two streams"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -385,6 +425,13 @@ def run_ours(args):
                "path": "bf_apply_host: pinned host S/tags -> H2D -> route+kernel -> D2H pinned R, "
                        "chunked on 3 streams"}
         del Sh, Rh
+        torch.cuda.empty_cache()
+        pc = pcie_probe(torch, dev)
+        t_floor = max(e2e["h2d_bytes_per_step"] / (pc["h2d_gbs"] * 1e9),
+                      e2e["d2h_bytes_per_step"] / (pc["d2h_gbs"] * 1e9)) / max(1, world)
+        pc["ceiling"] = n_e2e_total * wl.b / t_floor
+        pc["frac"] = e2e["value"] / pc["ceiling"]
+        e2e["pcie"] = pc
 
     # ---- CPU oracle baseline (rank 0, N = 1 only) -----------------------------------
     cpu = None
