@@ -38,6 +38,7 @@
 // TMEM: A terms at columns [0, 3 KP) (KP of f = 36 for the batch kernel), D double buffer at
 // [256, 384), [384, 512).
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -85,10 +86,20 @@ struct TcJob {
     float out_scale;          // layout 3 (int16 output): 2^e before the rounding
 };
 
-struct TcParams {
-    TcJob job[kMaxJobs];
+// Kernel parameters: n_jobs first, so a launch can pass a TcParams (16 jobs) to a
+// kernel declared with TcParamsN<1> — cudaLaunchKernel copies the kernel's parameter
+// size from the pointer, i.e. the common prefix.  The per-f kernels (bf_apply: one job)
+// take the 1-job form: 1.3 KB less parameter data per launch (~1 us of launch latency,
+// tools/launch_lat); the batch kernel (F = 0) takes all kMaxJobs.
+template <int NJ>
+struct TcParamsN {
     int n_jobs;
+    TcJob job[NJ];
 };
+using TcParams = TcParamsN<kMaxJobs>;
+template <int F>
+using TcParamsOf = TcParamsN<F == 0 ? kMaxJobs : 1>;
+static_assert(offsetof(TcParamsN<1>, job) == offsetof(TcParams, job), "TcParams prefix layout");
 
 template <int F>
 struct TcSmem {
@@ -280,7 +291,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // 8 = no S loads, 16 = main product as fp16-kind MMAs (energy experiment).
 // Results are wrong with DBG != 0.
 template <int F, int LAYOUT, int DBG = 0>
-__global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
+__global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> p) {
     using L = TcSmem<F>;
     // TMEM column stride of the three A regions: fixed across the jobs of a launch
     // (the split of a job's first tile must not overlap the previous job's regions
@@ -299,7 +310,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParams p) {
     int32_t *soffs = reinterpret_cast<int32_t *>(smem + L::kOffOffs);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_jobs = p.n_jobs;
+    constexpr int kNJ = F == 0 ? kMaxJobs : 1;
+    const int n_jobs = p.n_jobs < kNJ ? p.n_jobs : kNJ;
     // ---- prologue: jobs and their group offsets into shared memory, then this CTA's
     //      cost-balanced range of every job (one warp each, shuffle scans).
     if (threadIdx.x < n_jobs) {
