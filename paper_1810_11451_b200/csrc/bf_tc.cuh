@@ -288,7 +288,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 
 // DBG (0 in the library) disables pieces for bottleneck experiments only
 // (tools/tc_exp): 1 = no MMA issue, 2 = no R stores, 4 = no split/tcgen05.st,
-// 8 = no S loads, 16 = main product as fp16-kind MMAs (energy experiment).
+// 8 = no S loads, 16 = main product as fp16-kind MMAs (energy experiment), 32 (with 16) =
+// the split also writes S1 as packed fp16 (the instruction stream of a real fp16 main
+// product, without range handling).
 // Results are wrong with DBG != 0.
 template <int F, int LAYOUT, int DBG = 0>
 __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> p) {
@@ -419,8 +421,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                     mbar_arrive(bar_a_full + term);
                     continue;
                 }
+                // DBG 32: S1 as fp16 pairs over K rounded up to 16 (one more chunk at f = 36)
+                const int kend = ((DBG & 32) && term == 0) ? (KP + 15) / 16 * 16 : KP;
 #pragma unroll
-                for (int c0 = 0; c0 < KP; c0 += 8) {
+                for (int c0 = 0; c0 < kend; c0 += 8) {
                     float x[8];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
@@ -466,6 +470,12 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                             tc::tmem_st4(a_lane + kARegion + c0 / 2, w2);
                             tc::tmem_st4(a_lane + kARegion + KP / 2 + c0 / 2, w1);
                         }
+                    } else if ((DBG & 32) && term == 0) {
+                        uint32_t h[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e)
+                            h[e] = bfk::pack_half2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+                        if constexpr (!(DBG & 4)) tc::tmem_st4(a_lane + c0 / 2, h);
                     } else {
                         if constexpr (!(DBG & 4)) tc::tmem_st8(a_lane + term * kARegion + c0, v);
                     }

@@ -91,6 +91,7 @@ extern "C" float tcx_run(int dbg, const float *S, float *R, const float *Wimg, l
         case 7: return run<7>(S, R, Wimg, n, reps);
         case 15: return run<15>(S, R, Wimg, n, reps);
         case 16: return run<16>(S, R, Wimg, n, reps);
+        case 48: return run<48>(S, R, Wimg, n, reps);
     }
     return -2;
 }
