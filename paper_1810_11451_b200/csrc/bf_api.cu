@@ -42,14 +42,15 @@ constexpr int kDefaultOutExp = 12;          // int16 output: |R| < 8 fits, 2^-12
 constexpr int kHostSlots = 3;
 constexpr size_t kMaxProfEvents = 1 << 16;  // timed launches kept between kernel_time() calls
 // AUTO variant table, per layout (measured with
-// tools/sweep_f.py on c3's recipe, 100 000 blocks per f, profiles/r01_sweep_f_v3*.jsonl
-// and r01_sweep_auto_v3.jsonl): the smallest f from which the tensor-core kernel is
-// faster.  Below it both kernels are store-bound and the FFMA kernel's epilogue is
-// the cheaper one: interleaved f <= 6 (FFMA up to 7 % ahead; equal at f = 1),
-// planar f <= 10 (FFMA up to 26 % ahead: the tensor epilogue's planar stores,
-// DESIGN.md §6), fp16 output f <= 2.  From there on the tensor kernel wins, by
-// 2.2-2.6x at f = 36.
-constexpr int kAutoTensorMinF[4] = {7, 11, 3, 3};   // [layout] (int16 out: as fp16 out)
+// tools/sweep_f.py on c3's recipe, 100 000 blocks per f, both variants, every f <= 16
+// and every layout: profiles/r01_sweep_auto_v4.jsonl, with the FFMA kernel's staged
+// bulk-store epilogue for f <= 12): the smallest f from which the tensor-core kernel
+// is faster.  Below it both kernels are store-bound and the FFMA kernel's epilogue
+// (one 30 KB bulk store per block) is the cheaper one: interleaved f <= 8 (FFMA
+// 2-8 % ahead), planar f <= 10 (FFMA 15-40 % ahead: the tensor epilogue's planar
+// row stores), fp16 output f <= 3, int16 output f <= 7 (FFMA up to 2x
+// ahead at f = 1).  From there on the tensor kernel wins, by 2.2-2.6x at f = 36.
+constexpr int kAutoTensorMinF[4] = {9, 11, 4, 8};   // [layout]
 
 BfKernelTable g_table;      // FFMA kernels [f][layout]
 BfKernelTable g_table_tc;   // tcgen05 split-TF32 kernels [f][layout]

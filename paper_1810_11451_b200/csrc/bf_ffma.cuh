@@ -24,9 +24,11 @@
 //    conflicts were the top issue stall, see profiles/).  The paper's three fixes carry
 //    over: no extra FLOPs, every product fused, no permutes (re/im sit in
 //    separate registers).  Accumulators start at +0.0f (bit-exact identity).
-//  * Results go straight from registers to HBM with streaming 32-bit stores
-//    (re and im separately, so no even/odd pairing constrains the accumulators);
-//    a warp's two stores of a row cover whole 32-byte sectors.
+//  * Results: for F <= 12 (where this kernel is AUTO's choice and R is 95-99 % of the
+//    bytes) the block's R is staged in shared memory in its global layout and written
+//    by one 30 720 B bulk store; for larger F straight from registers to HBM with
+//    streaming 32-bit stores.  Both use 32-bit stores of re and im separately, so no
+//    even/odd pairing constrains the accumulators.
 #pragma once
 #include <cstdint>
 #include <cuda_fp16.h>
@@ -110,6 +112,22 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
         : "memory");
 }
+// Bulk store shared -> global (bulk-group completion), and the waits for its source
+// reads / full completion.
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes, uint64_t policy) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                 ::"l"(dst), "r"(smem_addr(src)), "r"(bytes), "l"(policy) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -130,7 +148,12 @@ struct Smem {
     static constexpr int kOffS = kWBytes;
     static constexpr int kOffBar = kOffS + kStages * kSBytes;     // multiple of 16
     static constexpr int kOffMeta = kOffBar + 4 * 8;
-    static constexpr int kBytes = kOffMeta + 4 * 8;
+    // Small f (the AUTO region of this kernel): the block's R is staged in shared
+    // memory in its global layout and leaves as ONE bulk store (30 720 B, full lines),
+    // instead of 80 scattered 32-bit stores per thread; 4 CTAs per SM still fit.
+    static constexpr bool kStageR = F <= 12;
+    static constexpr int kOffR = (kOffMeta + 4 * 8 + 127) / 128 * 128;
+    static constexpr int kBytes = kStageR ? kOffR + kRBlockFloats * 4 : kOffMeta + 4 * 8;
 };
 
 template <int F, int LAYOUT>
@@ -266,11 +289,19 @@ __global__ void __launch_bounds__(kThreads, 4) bf_ffma_kernel(const KParams p) {
                     }
             }
         }
+        // staged R: the previous block's bulk store must have read the staging buffer
+        if (L::kStageR && t == 0) bulk_wait_read();
         __syncthreads();                       // stage `stage` and meta are free again
         if (t == 0 && item + 2 < end) issue(stage, item + 2);
 
         if (valid) {
             float *Rb = p.R + blk * (r_block_bytes(LAYOUT) / 4);
+            float *Rd = L::kStageR ? reinterpret_cast<float *>(smem + L::kOffR) : Rb;
+            // staged: plain shared-memory stores; direct: streaming global stores
+            auto st32 = [&](float *a, uint32_t v) {
+                if (L::kStageR) *reinterpret_cast<uint32_t *>(a) = v;
+                else __stcs(reinterpret_cast<unsigned int *>(a), v);
+            };
 #pragma unroll
             for (int a = 0; a < kTA; ++a) {
                 const int i = ag * kTA + a;
@@ -281,22 +312,26 @@ __global__ void __launch_bounds__(kThreads, 4) bf_ffma_kernel(const KParams p) {
                         // two 32-bit stores instead of one float2: a 64-bit store would
                         // pin (re, im) to an even/odd register pair for the whole k loop,
                         // which forces register-bank conflicts in half of the FFMAs.
-                        __stcs(Rb + 2 * (i * kB + j), are[a][r]);
-                        __stcs(Rb + 2 * (i * kB + j) + 1, aim[a][r]);
+                        st32(Rd + 2 * (i * kB + j), __float_as_uint(are[a][r]));
+                        st32(Rd + 2 * (i * kB + j) + 1, __float_as_uint(aim[a][r]));
                     } else if (LAYOUT == 2) {
-                        __stcs(reinterpret_cast<unsigned int *>(Rb) + i * kB + j,
-                               pack_half2(are[a][r], aim[a][r]));
+                        st32(Rd + i * kB + j, pack_half2(are[a][r], aim[a][r]));
                     } else if (LAYOUT == 3) {
-                        __stcs(reinterpret_cast<unsigned int *>(Rb) + i * kB + j,
-                               pack_i16x2(are[a][r], aim[a][r], p.out_scale));
+                        st32(Rd + i * kB + j, pack_i16x2(are[a][r], aim[a][r], p.out_scale));
                     } else {
-                        __stcs(Rb + i * kB + j, are[a][r]);
-                        __stcs(Rb + kAnt * kB + i * kB + j, aim[a][r]);
+                        st32(Rd + i * kB + j, __float_as_uint(are[a][r]));
+                        st32(Rd + kAnt * kB + i * kB + j, __float_as_uint(aim[a][r]));
                     }
                 }
             }
+            if (L::kStageR) {
+                fence_proxy_async_smem();      // this thread's writes -> the bulk copy
+                __syncthreads();
+                if (t == 0) bulk_s2g(Rb, Rd, (uint32_t)r_block_bytes(LAYOUT), pol_stream);
+            }
         }
     }
+    if (L::kStageR && t == 0) bulk_wait_all();
 }
 
 }  // namespace bfk

@@ -63,7 +63,7 @@ def main():
             step_ms = e0.elapsed_time(e1) / a.reps
             kms, kn = plan.kernel_time()
             kern_ms = kms / kn if kn else step_ms
-            r_blk = 15360 if a.layout == "interleaved_f16out" else 30720
+            r_blk = 15360 if a.layout in ("interleaved_f16out", "interleaved_i16out") else 30720
             gbs = (480 * f + r_blk) * n / (kern_ms * 1e-3) / 1e9
             tf = wl.block_flops * n / (kern_ms * 1e-3) / 1e12
             print(json.dumps({"f": f, "variant": variant, "layout": a.layout, "blocks": n,
