@@ -42,15 +42,14 @@ constexpr int kDefaultOutExp = 12;          // int16 output: |R| < 8 fits, 2^-12
 constexpr int kHostSlots = 3;
 constexpr size_t kMaxProfEvents = 1 << 16;  // timed launches kept between kernel_time() calls
 // AUTO variant table, per layout (measured with
-// tools/sweep_f.py on c3's recipe, 100 000 blocks per f, both variants, every f <= 16
-// and every layout: profiles/r01_sweep_auto_v4.jsonl, with the FFMA kernel's staged
-// bulk-store epilogue for f <= 12): the smallest f from which the tensor-core kernel
-// is faster.  Below it both kernels are store-bound and the FFMA kernel's epilogue
-// (one 30 KB bulk store per block) is the cheaper one: interleaved f <= 8 (FFMA
-// 2-8 % ahead), planar f <= 10 (FFMA 15-40 % ahead: the tensor epilogue's planar
-// row stores), fp16 output f <= 3, int16 output f <= 7 (FFMA up to 2x
-// ahead at f = 1).  From there on the tensor kernel wins, by 2.2-2.6x at f = 36.
-constexpr int kAutoTensorMinF[4] = {9, 11, 4, 8};   // [layout]
+// tools/sweep_f.py on c3's recipe, 100 000 blocks per f, both variants, f <= 12, every
+// layout: profiles/r01_sweep_auto_v5.jsonl — both kernels with their staged bulk-store
+// epilogues): the smallest f from which the tensor-core kernel is faster.  Below it
+// both kernels are store-bound and within a few percent: interleaved f = 1 (equal),
+// planar f <= 6 (within +-4 %), fp16 output f <= 3 (FFMA 5-16 % ahead), int16 output
+// f <= 7 (FFMA up to 2x ahead at f = 1: the tensor epilogue's conversions).  From
+// there on the tensor kernel wins, by 2.2-2.6x at f = 36.
+constexpr int kAutoTensorMinF[4] = {2, 7, 4, 8};   // [layout]
 
 BfKernelTable g_table;      // FFMA kernels [f][layout]
 BfKernelTable g_table_tc;   // tcgen05 split-TF32 kernels [f][layout]

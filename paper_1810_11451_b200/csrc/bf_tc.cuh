@@ -110,7 +110,15 @@ struct TcSmem {
     // two W buffers: the producer prefetches the next group's image while the
     // current group's MMAs run (a reload no longer drains the tensor pipe)
     static constexpr int kJobBytes = kMaxJobs * 96;    // per-job context (JobCtx)
-    static constexpr int kFixed = 2 * kWBytes + 24 * 8 + 16 + kOffsSlots * 4 + kJobBytes;
+    static constexpr int kFixed0 = 2 * kWBytes + 24 * 8 + 16 + kOffsSlots * 4 + kJobBytes;
+    // R staging (f <= 24): the epilogue writes the tile's two blocks of R into shared
+    // memory in their global layout and one thread stores each block with a bulk copy
+    // (full lines, no partial sectors at planar row boundaries), when it fits next to
+    // a 2-stage S ring.
+    static constexpr int kRStageBytes = 2 * 30720;
+    static constexpr bool kStageR =
+        F > 0 && (kSmemLimit - kFixed0 - kRStageBytes - 128) / (2 * kSBlock) >= 2;
+    static constexpr int kFixed = kFixed0 + (kStageR ? kRStageBytes + 128 : 0);
     static constexpr int kStagesFit = (kSmemLimit - kFixed) / (2 * kSBlock);
     static constexpr int kStages = kStagesFit < kMaxStages ? kStagesFit : kMaxStages;
     static_assert(kStages >= 2, "S ring needs two stages");
@@ -119,7 +127,8 @@ struct TcSmem {
     static constexpr int kOffTmem = kOffBar + 24 * 8;
     static constexpr int kOffJobs = kOffTmem + 16;     // JobCtx[kMaxJobs]
     static constexpr int kOffOffs = kOffJobs + kJobBytes;   // group offsets of every job
-    static constexpr int kBytesUsed = kOffOffs + kOffsSlots * 4;
+    static constexpr int kOffR = (kOffOffs + kOffsSlots * 4 + 127) / 128 * 128;
+    static constexpr int kBytesUsed = kStageR ? kOffR + kRStageBytes : kOffOffs + kOffsSlots * 4;
     static constexpr int kBytes = kBytesUsed > kMinSmem ? kBytesUsed : kMinSmem;
 };
 
@@ -268,9 +277,15 @@ __device__ __forceinline__ void cta_range(const int32_t *offs, int G, int64_t n,
     }
 }
 
-// Named barrier 1 over the 4 epilogue warps (128 threads).
+// Named barrier 1 over the 8 epilogue warps (256 threads).
 __device__ __forceinline__ void epi_bar_sync() {
-    asm volatile("bar.sync 1, 128;" ::: "memory");
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // TMA bulk store shared -> global (bulk-group completion), L2 cache hint.
@@ -299,6 +314,9 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     // (the split of a job's first tile must not overlap the previous job's regions
     // that its last MMAs may still read).
     constexpr int kARegion = L::KP;
+    // staged R (see TcSmem::kStageR) except for int16 output, whose conversion-heavy
+    // epilogue measured faster with the warps storing independently
+    constexpr bool kStageR = L::kStageR && LAYOUT != 3;
     extern __shared__ __align__(1024) unsigned char smem[];
     float *Wsm = reinterpret_cast<float *>(smem);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::kOffBar);
@@ -623,6 +641,9 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         const int h = (warp - kEpiWarp0) >> 2;           // D columns [64 h, 64 h + 64)
         const int m = q * 32 + lane;
         const int bsel = m >= 60 ? 1 : 0, j = m - 60 * bsel;
+        const bool e0 = warp == kEpiWarp0 && lane == 0;  // issues the staged bulk stores
+        uint64_t pol_r = 0;
+        if (kStageR && e0) pol_r = bfk::policy_evict_first();
         for (int64_t t = 0; it.next(tl); ++t) {
             const JobCtx &J = jobs[tl.job];
             const int b = (int)(t & 1);
@@ -645,7 +666,40 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             // half the store instructions of one-RE-per-lane, which measurably
             // raises the write bandwidth of 4 storing warps (tools/write_bw).
             const bool odd = (j & 1) != 0;
-            if constexpr (!(DBG & 2)) {
+            if constexpr (!(DBG & 2) && kStageR) {
+                // staged: both blocks of the tile in their global layout in shared memory,
+                // then one bulk store per block by the first epilogue thread.  The previous
+                // tile's stores must have read the stage first.
+                constexpr int rbf = bfk::r_block_bytes(LAYOUT) / 4;   // floats per block
+                float *Rst = reinterpret_cast<float *>(smem + L::kOffR);
+                if (e0) bulk_wait_read();
+                epi_bar_sync();
+                if (valid) {
+                    float *Rt = Rst + bsel * rbf;
+#pragma unroll
+                    for (int aa = 0; aa < 32; ++aa) {
+                        const int a = 32 * h + aa;
+                        const float re = __uint_as_float(v[2 * aa]), im = __uint_as_float(v[2 * aa + 1]);
+                        if (LAYOUT == 0)
+                            *reinterpret_cast<float2 *>(Rt + 2 * (a * 60 + j)) = make_float2(re, im);
+                        else if (LAYOUT == 1) {
+                            Rt[a * 60 + j] = re;
+                            Rt[64 * 60 + a * 60 + j] = im;
+                        } else if (LAYOUT == 2)
+                            reinterpret_cast<uint32_t *>(Rt)[a * 60 + j] = bfk::pack_half2(re, im);
+                        else
+                            reinterpret_cast<uint32_t *>(Rt)[a * 60 + j] = bfk::pack_i16x2(re, im, J.out_scale);
+                    }
+                }
+                bfk::fence_proxy_async_smem();         // this thread's writes -> the bulk copies
+                epi_bar_sync();
+                if (e0) {
+                    for (int b2 = 0; b2 < tl.cnt; ++b2)
+                        bulk_s2g(J.R + block_of(J, tl.item + b2) * (int64_t)rbf, Rst + b2 * rbf,
+                                 (uint32_t)bfk::r_block_bytes(LAYOUT), pol_r);
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            } else if constexpr (!(DBG & 2)) {
                 if (LAYOUT == 0 || LAYOUT == 2 || LAYOUT == 3) {
 #pragma unroll
                     for (int aa = 0; aa < 32; aa += 2) {
@@ -687,6 +741,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             }
         }
     }
+    if (kStageR && warp == kEpiWarp0 && lane == 0) bulk_wait_all();   // stage read, stores done
     tc::fence_before_sync();
     __syncthreads();
     if (warp == 0) {
