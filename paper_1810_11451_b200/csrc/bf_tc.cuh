@@ -107,29 +107,40 @@ struct TcSmem {
     static constexpr int KP = kp_of(FS);
     static constexpr int kWBytes = 2 * KP * 128 * 4;   // W1 tf32 image + bf16 correction image
     static constexpr int kSBlock = 480 * FS;           // one block of S (slot stride)
-    // two W buffers: the producer prefetches the next group's image while the
-    // current group's MMAs run (a reload no longer drains the tensor pipe)
     static constexpr int kJobBytes = kMaxJobs * 96;    // per-job context (JobCtx)
-    static constexpr int kFixed0 = 2 * kWBytes + 24 * 8 + 16 + kOffsSlots * 4 + kJobBytes;
-    // R staging (f <= 24): the epilogue writes the tile's two blocks of R into shared
-    // memory in their global layout and one thread stores each block with a bulk copy
-    // (full lines, no partial sectors at planar row boundaries), when it fits next to
-    // a 2-stage S ring.
+    static constexpr int kMisc = 24 * 8 + 16 + kOffsSlots * 4 + kJobBytes;
+    // R staging: the epilogue writes the tile's two blocks of R into shared memory in
+    // their global layout and one thread stores each block with a bulk copy (full lines,
+    // no partial sectors at planar row boundaries).  Shared memory, in order of
+    // preference: two W buffers (the producer prefetches the next group's image while
+    // the current group's MMAs run) + R stage (f <= 25); one W buffer + R stage (the
+    // per-f kernels above f = 25: a group change then waits for the previous group's
+    // MMAs — a few times per CTA in a bench-sized launch); two W buffers, no stage (the
+    // batch kernel, whose short jobs change groups often).  Each with >= 2 S stages.
     static constexpr int kRStageBytes = 2 * 30720;
-    static constexpr bool kStageR =
-        F > 0 && (kSmemLimit - kFixed0 - kRStageBytes - 128) / (2 * kSBlock) >= 2;
-    static constexpr int kFixed = kFixed0 + (kStageR ? kRStageBytes + 128 : 0);
+    static constexpr int kFitA = (kSmemLimit - 2 * kWBytes - kMisc - kRStageBytes - 128) / (2 * kSBlock);
+    static constexpr int kFitB = (kSmemLimit - kWBytes - kMisc - kRStageBytes - 128) / (2 * kSBlock);
+    static constexpr bool kStageR = F > 0 && (kFitA >= 2 || kFitB >= 2);
+    static constexpr int kWBufs = (F > 0 && kFitA < 2 && kFitB >= 2) ? 1 : 2;
+    static constexpr int kFixed = kWBufs * kWBytes + kMisc + (kStageR ? kRStageBytes + 128 : 0);
     static constexpr int kStagesFit = (kSmemLimit - kFixed) / (2 * kSBlock);
-    static constexpr int kStages = kStagesFit < kMaxStages ? kStagesFit : kMaxStages;
+    // S ring depth: with the staged epilogue a deeper ring measured slower above f = 12
+    // (e.g. f = 20: 0.87 of the copy bandwidth with 4 stages, 0.94 with 2; f <= 12 gains
+    // from 4 — tools/sweep_f.py, BFTC_MAX_STAGES builds, profiles/r01_sweep_stages_v5.txt)
+    // (fp16 output, whose stores are half the bytes, keeps the deepest ring that fits)
+    static constexpr int kMaxS = (F > 0 && F <= 12) ? kMaxStages : (kMaxStages < 2 ? kMaxStages : 2);
+    static constexpr int kStagesAlloc = kStagesFit < kMaxStages ? kStagesFit : kMaxStages;
+    static constexpr int kStages = kStagesFit < kMaxS ? kStagesFit : kMaxS;
     static_assert(kStages >= 2, "S ring needs two stages");
-    static constexpr int kOffS = 2 * kWBytes;          // kStages x 2 blocks
-    static constexpr int kOffBar = kOffS + kStages * 2 * kSBlock;   // 24 mbarrier slots
+    static constexpr int kOffS = kWBufs * kWBytes;     // kStagesAlloc x 2 blocks
+    static constexpr int kOffBar = kOffS + kStagesAlloc * 2 * kSBlock;   // 24 mbarrier slots
     static constexpr int kOffTmem = kOffBar + 24 * 8;
     static constexpr int kOffJobs = kOffTmem + 16;     // JobCtx[kMaxJobs]
     static constexpr int kOffOffs = kOffJobs + kJobBytes;   // group offsets of every job
     static constexpr int kOffR = (kOffOffs + kOffsSlots * 4 + 127) / 128 * 128;
     static constexpr int kBytesUsed = kStageR ? kOffR + kRStageBytes : kOffOffs + kOffsSlots * 4;
     static constexpr int kBytes = kBytesUsed > kMinSmem ? kBytesUsed : kMinSmem;
+    static_assert(kBytesUsed <= kSmemLimit, "shared memory");
 };
 
 // A job as the roles see it (shared memory), with this CTA's share of it.
@@ -317,13 +328,14 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     // staged R (see TcSmem::kStageR) except for int16 output, whose conversion-heavy
     // epilogue measured faster with the warps storing independently
     constexpr bool kStageR = L::kStageR && LAYOUT != 3;
+    constexpr int kRing = LAYOUT == 2 ? L::kStagesAlloc : L::kStages;   // S ring depth used
     extern __shared__ __align__(1024) unsigned char smem[];
     float *Wsm = reinterpret_cast<float *>(smem);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::kOffBar);
     // a_full[t] / a_free[t]: TMEM A region of split term t (0: S1, 1: S2, 2: S3)
     uint64_t *bar_a_full = bars + 0, *bar_a_free = bars + 3, *bar_d_full = bars + 6,
              *bar_d_free = bars + 8, *bar_wfull = bars + 10, *bar_wfree = bars + 12,
-             *bar_s_full = bars + 14, *bar_s_empty = bars + 14 + L::kStages;
+             *bar_s_full = bars + 14, *bar_s_empty = bars + 14 + kRing;
     float *Ss = reinterpret_cast<float *>(smem + L::kOffS);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L::kOffTmem);
     JobCtx *jobs = reinterpret_cast<JobCtx *>(smem + L::kOffJobs);
@@ -389,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             bfk::mbar_init(bar_wfull + i, 1);
             bfk::mbar_init(bar_wfree + i, 1);
         }
-        for (int i = 0; i < L::kStages; ++i) {
+        for (int i = 0; i < kRing; ++i) {
             bfk::mbar_init(bar_s_full + i, 1);
             bfk::mbar_init(bar_s_empty + i, 128);
         }
@@ -415,8 +427,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             const int f = F > 0 ? F : J.f;
             const int KP = F > 0 ? L::KP : J.kp;
             const bool valid = m < 120 && bsel < tl.cnt;
-            const int stage = (int)(t % L::kStages);
-            bfk::mbar_wait(bar_s_full + stage, (uint32_t)((t / L::kStages) & 1));
+            const int stage = (int)(t % kRing);
+            bfk::mbar_wait(bar_s_full + stage, (uint32_t)((t / kRing) & 1));
             const float *Sb = Ss + (stage * 2 + (valid ? bsel : 0)) * (L::kSBlock / 4);
             // Term order S2, S3, S1 mirrors the MMA order, so each region is rewritten
             // as soon as the previous tile's MMAs on it have completed and the tensor
@@ -506,9 +518,9 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         }
     } else if (warp == kProdWarp) {
         // ------------------------------------------------------------ S producer (TMA bulk)
-        // It also loads each group segment's B image (W) into W buffer (segment & 1)
-        // as it reaches the segment's first tile — up to kStages tiles ahead of the
-        // MMAs — once the segment two back has released that buffer (wfree).
+        // It also loads each group segment's B image (W) into W buffer (segment mod
+        // kWBufs) as it reaches the segment's first tile — up to kStages tiles ahead of
+        // the MMAs — once the segment kWBufs back has released that buffer (wfree).
         const uint64_t pol = bfk::policy_evict_first();
         int cur_g = -1, cur_j = -1;
         int64_t seg = -1;
@@ -522,14 +534,15 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             const int64_t nb1 = have_nx && nx.cnt > 1 ? block_of(jobs[nx.job], nx.item + 1) : 0;
             const JobCtx &J = jobs[tl.job];
             const int f = F > 0 ? F : J.f;
-            const int stage = (int)(t % L::kStages);
+            const int stage = (int)(t % kRing);
             if (tl.g != cur_g || tl.job != cur_j) {
                 cur_g = tl.g;
                 cur_j = tl.job;
                 ++seg;
-                const int wb = (int)(seg & 1);
+                constexpr int NB = L::kWBufs;
+                const int wb = (int)(seg % NB);
                 const int wbytes = F > 0 ? L::kWBytes : J.wbytes;
-                if (seg >= 2) bfk::mbar_wait(bar_wfree + wb, (uint32_t)(((seg >> 1) - 1) & 1));
+                if (seg >= NB) bfk::mbar_wait(bar_wfree + wb, (uint32_t)(((seg / NB) - 1) & 1));
                 if (lane == 0) {
                     bfk::mbar_arrive_expect_tx(bar_wfull + wb, (uint32_t)wbytes);
                     bfk::bulk_g2s(Wsm + wb * (L::kWBytes / 4), J.Wimg + (int64_t)tl.g * (wbytes / 4),
@@ -537,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 }
                 __syncwarp();
             }
-            bfk::mbar_wait(bar_s_empty + stage, (uint32_t)(((t / L::kStages) & 1) ^ 1));
+            bfk::mbar_wait(bar_s_empty + stage, (uint32_t)(((t / kRing) & 1) ^ 1));
             if (DBG & 8) {
                 if (lane == 0) mbar_arrive(bar_s_full + stage);
             } else if (lane == 0) {
@@ -569,11 +582,11 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             if (tl.g != cur_g || tl.job != cur_j) {   // new group segment: W prefetched by the producer
                 exact = __ldg(J.wexact + tl.g) != 0;
                 // the previous segment's buffer is free once every MMA issued so far completed
-                if (seg >= 0 && lane == 0) tc::mma_commit(bar_wfree + (int)(seg & 1));
+                if (seg >= 0 && lane == 0) tc::mma_commit(bar_wfree + (int)(seg % L::kWBufs));
                 __syncwarp();
                 ++seg;
-                const int wb = (int)(seg & 1);
-                bfk::mbar_wait(bar_wfull + wb, (uint32_t)((seg >> 1) & 1));
+                const int wb = (int)(seg % L::kWBufs);
+                bfk::mbar_wait(bar_wfull + wb, (uint32_t)((seg / L::kWBufs) & 1));
                 w_base = tc::smem_u32(Wsm + wb * (L::kWBytes / 4));
                 cur_g = tl.g;
                 cur_j = tl.job;
