@@ -113,15 +113,15 @@ struct TcSmem {
     // their global layout and one thread stores each block with a bulk copy (full lines,
     // no partial sectors at planar row boundaries).  Shared memory, in order of
     // preference: two W buffers (the producer prefetches the next group's image while
-    // the current group's MMAs run) + R stage (f <= 25); one W buffer + R stage (the
-    // per-f kernels above f = 25: a group change then waits for the previous group's
-    // MMAs — a few times per CTA in a bench-sized launch); two W buffers, no stage (the
-    // batch kernel, whose short jobs change groups often).  Each with >= 2 S stages.
+    // the current group's MMAs run) + R stage (f <= 25); one W buffer + R stage (above
+    // f = 25 and the runtime-f batch kernel: a group change then waits for the previous
+    // group's MMAs, which measured cheaper than the unstaged epilogue even for c5's
+    // short, group-rich jobs: +3 %).  Each with >= 2 S stages.
     static constexpr int kRStageBytes = 2 * 30720;
     static constexpr int kFitA = (kSmemLimit - 2 * kWBytes - kMisc - kRStageBytes - 128) / (2 * kSBlock);
     static constexpr int kFitB = (kSmemLimit - kWBytes - kMisc - kRStageBytes - 128) / (2 * kSBlock);
-    static constexpr bool kStageR = F > 0 && (kFitA >= 2 || kFitB >= 2);
-    static constexpr int kWBufs = (F > 0 && kFitA < 2 && kFitB >= 2) ? 1 : 2;
+    static constexpr bool kStageR = kFitA >= 2 || kFitB >= 2;
+    static constexpr int kWBufs = (kFitA < 2 && kFitB >= 2) ? 1 : 2;
     static constexpr int kFixed = kWBufs * kWBytes + kMisc + (kStageR ? kRStageBytes + 128 : 0);
     static constexpr int kStagesFit = (kSmemLimit - kFixed) / (2 * kSBlock);
     // S ring depth: with the staged epilogue a deeper ring measured slower above f = 12
