@@ -325,9 +325,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     // (the split of a job's first tile must not overlap the previous job's regions
     // that its last MMAs may still read).
     constexpr int kARegion = L::KP;
-    // staged R (see TcSmem::kStageR) except for int16 output, whose conversion-heavy
-    // epilogue measured faster with the warps storing independently
-    constexpr bool kStageR = L::kStageR && LAYOUT != 3;
+    // staged R (see TcSmem::kStageR); int16 output at f <= 12 measured faster with the
+    // warps storing independently (0.41 vs 0.50 ms per 10^5 blocks; staged wins above:
+    // f = 36 0.70 vs 0.84 — tools/sweep_f.py, profiles/r01_sweep_i16_v6.txt)
+    constexpr bool kStageR = L::kStageR && (LAYOUT != 3 || F == 0 || F > 12);
     constexpr int kRing = LAYOUT == 2 ? L::kStagesAlloc : L::kStages;   // S ring depth used
     extern __shared__ __align__(1024) unsigned char smem[];
     float *Wsm = reinterpret_cast<float *>(smem);
@@ -689,6 +690,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 epi_bar_sync();
                 if (valid) {
                     float *Rt = Rst + bsel * rbf;
+                    const float osc = J.out_scale;
 #pragma unroll
                     for (int aa = 0; aa < 32; ++aa) {
                         const int a = 32 * h + aa;
@@ -701,7 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                         } else if (LAYOUT == 2)
                             reinterpret_cast<uint32_t *>(Rt)[a * 60 + j] = bfk::pack_half2(re, im);
                         else
-                            reinterpret_cast<uint32_t *>(Rt)[a * 60 + j] = bfk::pack_i16x2(re, im, J.out_scale);
+                            reinterpret_cast<uint32_t *>(Rt)[a * 60 + j] = bfk::pack_i16x2(re, im, osc);
                     }
                 }
                 bfk::fence_proxy_async_smem();         // this thread's writes -> the bulk copies
@@ -711,6 +713,33 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                         bulk_s2g(J.R + block_of(J, tl.item + b2) * (int64_t)rbf, Rst + b2 * rbf,
                                  (uint32_t)bfk::r_block_bytes(LAYOUT), pol_r);
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            } else if constexpr (!(DBG & 2) && (LAYOUT == 2 || LAYOUT == 3)) {
+                // 16-bit output, direct stores (int16 output at f <= 12; see kStageR): pack
+                // all 16 pairs first — the shuffles need every lane — then one branch
+                // around the stores, and the output scale read once per tile.
+                const float osc = J.out_scale;
+                uint2 pk[16];
+#pragma unroll
+                for (int aa = 0; aa < 32; aa += 2) {
+                    const float re0 = __uint_as_float(v[2 * aa]), im0 = __uint_as_float(v[2 * aa + 1]);
+                    const float re1 = __uint_as_float(v[2 * aa + 2]), im1 = __uint_as_float(v[2 * aa + 3]);
+                    const float gr = __shfl_xor_sync(0xffffffffu, odd ? re0 : re1, 1);
+                    const float gi = __shfl_xor_sync(0xffffffffu, odd ? im0 : im1, 1);
+                    // even lane: antenna a, REs j, j+1; odd lane: antenna a+1, REs j-1, j
+                    const float4 w4 = odd ? make_float4(gr, gi, re1, im1) : make_float4(re0, im0, gr, gi);
+                    pk[aa / 2] = LAYOUT == 3
+                                     ? make_uint2(bfk::pack_i16x2(w4.x, w4.y, osc), bfk::pack_i16x2(w4.z, w4.w, osc))
+                                     : make_uint2(bfk::pack_half2(w4.x, w4.y), bfk::pack_half2(w4.z, w4.w));
+                }
+                if (valid) {
+                    uint2 *Rw = reinterpret_cast<uint2 *>(Rb);
+#pragma unroll
+                    for (int aa = 0; aa < 32; aa += 2) {
+                        const int a = 32 * h + aa;
+                        const int e = (a + (odd ? 1 : 0)) * 60 + j - (odd ? 1 : 0);   // element index
+                        __stcs(Rw + e / 2, pk[aa / 2]);
+                    }
                 }
             } else if constexpr (!(DBG & 2)) {
                 if (LAYOUT == 0 || LAYOUT == 2 || LAYOUT == 3) {
