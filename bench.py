@@ -173,6 +173,14 @@ def host_ram_available() -> int:
     return 0
 
 
+# What the beamforming product is computed in (the line's "dtype" is its fp32 summary).
+ARITH = {
+    "tensor": "tcgen05 split precision: S1*W1 tf32 + (S2*W1 + S1*W2) one bf16 group, fp32 accumulate "
+              "in TMEM (tf32-exact W: S1+S2+S3 tf32 terms, bit-exact copies); DESIGN.md §7",
+    "ffma": "fp32 FFMA, 4 per complex MAC, k ascending",
+}
+
+
 def pcie_probe(torch, dev, nbytes: int = 1 << 30, reps: int = 4) -> dict:
     """Pinned H2D and D2H copy bandwidth, each direction alone and both concurrently (two
     streams, CUDA events).  The alone figures bound an e2e step whose copies overlap each
@@ -456,7 +464,9 @@ def run_ours(args):
                        if wl.tagged else f"dp{world}",
                        "l2": "inputs larger than L2 (S+R >> 126 MB)" if not small
                        else "L2 flushed between steps (512 MB write outside the timed events)",
-                       "kernel": cfg, "gpu": gpu_name, "w_broadcast_ms": t_bc * 1e3},
+                       "kernel": cfg, "gpu": gpu_name, "w_broadcast_ms": t_bc * 1e3,
+                       "arith": "none (f = 0: R := +0, memset)" if memset_only
+                       else ARITH.get(roof.get("variant"), "?")},
             "flops_per_s": total_blocks * wl.block_flops * args.steps / (elapsed_ms * 1e-3),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,
