@@ -807,3 +807,37 @@ def test_i16_identity_reproduces_integer_samples(variant):
     with pytest.raises(bf.BfError):
         p.set_output_exponent(65)
     p.close()
+
+
+# ---------------------------------------------------------------------------
+# every shared-memory configuration of the tensor kernel (TcSmem: double or single W
+# buffer, R stage or not, ring depth; int16 direct vs staged), with many group changes
+# per CTA (2 SMs), so the single-W-buffer reload path runs for every f that uses it
+# ---------------------------------------------------------------------------
+def run_shared(W, S, tags, layout, share):
+    plan = Plan(f=W.shape[-1], layout=layout, variant=Variant.TENSOR)
+    plan.set_sm_share(share)
+    conv = syn.to_planar if layout == Layout.PLANAR else np.ascontiguousarray
+    plan.set_precoders(torch.from_numpy(conv(W)).to(DEV))
+    R = plan.apply(torch.from_numpy(conv(S)).to(DEV), torch.from_numpy(tags).to(DEV))
+    torch.cuda.synchronize()
+    plan.close()
+    R = R.cpu().numpy()
+    return syn.from_planar(R) if layout == Layout.PLANAR else R
+
+
+@pytest.mark.parametrize("f", [3, 12, 13, 20, 25, 26, 27, 31, 33, 36])
+def test_smem_configs_with_group_changes(f):
+    G, n = 13, 600
+    W = syn.precoders(71, f, G, 64, f, "unit_columns")
+    S = syn.qam_symbols(71, f, np.arange(n), f, 60, 64)
+    tags = syn.subband_tags(71, np.arange(n), G)
+    R_ref, T, _ = oracle.beamform(W, S, tags, n_threads=NT)
+    R32 = run_shared(W, S, tags, Layout.INTERLEAVED, 2)
+    assert_parity(R32, R_ref, T, what=f"f={f} interleaved, 2 SMs")
+    assert np.array_equal(R32, run_plan(W, S, tags, variant=Variant.TENSOR)), "partition-dependent"
+    assert_parity(run_shared(W, S, tags, Layout.PLANAR, 2), R_ref, T, what=f"f={f} planar, 2 SMs")
+    h = run_shared(W, S, tags, Layout.INTERLEAVED_F16OUT, 3).astype(np.float64)
+    expect16 = R32.real.astype(np.float16).astype(np.float64) + 1j * R32.imag.astype(np.float16).astype(np.float64)
+    assert np.array_equal(h[..., 0] + 1j * h[..., 1], expect16)
+    assert np.array_equal(run_shared(W, S, tags, Layout.INTERLEAVED_I16OUT, 3), host_i16(R32, 12))
