@@ -11,30 +11,33 @@
 //                      n = 2i  : kk=2k -> Wr[i][k],  kk=2k+1 -> -Wi[i][k]
 //                      n = 2i+1: kk=2k -> Wi[i][k],  kk=2k+1 ->  Wr[i][k]
 //   D [m][n]   (TMEM)  = R[blk][i][j] re / im, fp32 accumulate.
-// Split precision (error-compensated 3xTF32, BASELINE.json north_star item 2):
+// Split precision (error-compensated, BASELINE.json north_star item 2):
 // S = S1 + S2 + S3 exactly (three tf32 terms, each rounded to 11 bits),
-// W' = W1 + W2 (+ 2^-22 residual, split once per W).  Three MMA terms per K
-// step: S2 W1 + S1 W1 + S1 W2 for general W; S2 W1 + S3 W1 + S1 W1 when the
-// group's W is exactly tf32 (W2 == 0: identity, selection, small integers),
-// which makes copy-like precoders bit-exact.  The split of tile t+1 rewrites
-// S2, S3, S1 (in the MMA's order) as soon as tile t's MMAs on each completed.
-// Dropped terms are <= ~2^-21 T; the fp32 (truncating) tensor accumulation
-// over 3 x KP/8 MMAs stays near 2e-6 T at f = 36, inside the
-// 1e-5 T contract.
+// W' = W1 + W2 (+ 2^-22 residual, split once per W).  General W: the corrections
+// S2 W1 + S1 W2 as one bf16 MMA group over K'' = 2 KP, then S1 W1 in tf32; when the
+// group's W is exactly tf32 (W2 == 0: identity, selection, small integers) S2 W1 +
+// S3 W1 + S1 W1 in tf32, which makes copy-like precoders bit-exact.  The split of
+// tile t+1 rewrites each term region as soon as tile t's MMAs on it completed.
+// Dropped terms are <= ~2^-21 T; with the tensor accumulation the error stays
+// near 2e-6 T at f = 36, inside the 1e-5 T contract.
 //
 // One CTA (14 warps) per SM, persistent over a cost-balanced range of the
 // group-sorted block list (cta_range); tiles are 2 consecutive blocks of one group.
 //   warp 13    producer: cp.async.bulk (TMA bulk engine) of each block's 480 F
 //              contiguous bytes into a 2-4-stage shared-memory ring, completing on
 //              mbarriers, up to kStages tiles ahead of the split; and the pre-split
-//              B image (W) of each group segment into one of two W buffers, so a
-//              group change does not stall the tensor pipe;
+//              B image (W) of each group segment into its W buffer (two where shared
+//              memory allows: the next group's image loads while the current one's
+//              MMAs run);
 //   warps 0-3  split: LDS S (conflict-free, one RE column per lane), split into
-//              3 tf32 terms, tcgen05.st into the A region (one TMEM lane per RE);
+//              the terms, tcgen05.st into the A regions (one TMEM lane per RE);
 //   warp 4     MMA issuer (one thread);
-//   warps 5-12 epilogue (two per lane quarter, half the D columns each): tcgen05.ld of a whole D row (128 columns), release of
-//              the TMEM buffer, then stores of two adjacent REs per lane (lane
-//              pairs trade one shuffle) — 256 contiguous bytes per antenna row.
+//   warps 5-12 epilogue (two per lane quarter, half the D columns each): tcgen05.ld
+//              of the thread's D row half, release of the TMEM buffer, then the
+//              tile's two R blocks written into a shared-memory stage in their
+//              global layout and stored by one thread with one bulk copy per block
+//              (int16 output at f <= 12: direct 8-byte stores instead).
+// Shared memory per f: TcSmem (W buffers, S ring depth, R stage).
 // TMEM: A terms at columns [0, 3 KP) (KP of f = 36 for the batch kernel), D double buffer at
 // [256, 384), [384, 512).
 #pragma once
@@ -329,6 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     // warps storing independently (0.41 vs 0.50 ms per 10^5 blocks; staged wins above:
     // f = 36 0.70 vs 0.84 — tools/sweep_f.py, profiles/r01_sweep_i16_v6.txt)
     constexpr bool kStageR = L::kStageR && (LAYOUT != 3 || F == 0 || F > 12);
+    static_assert(kStageR || LAYOUT == 2 || LAYOUT == 3, "fp32 layouts always use the staged epilogue");
     constexpr int kRing = LAYOUT == 2 ? L::kStagesAlloc : L::kStages;   // S ring depth used
     extern __shared__ __align__(1024) unsigned char smem[];
     float *Wsm = reinterpret_cast<float *>(smem);
@@ -675,10 +679,6 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             tc::tmem_ld_wait();
             tc::fence_before_sync();
             mbar_arrive(bar_d_free + b);                 // TMEM buffer b may be overwritten
-            // Lane pairs (j even, j + 1) trade values with one shuffle so every lane
-            // stores two adjacent REs at once (STG.128 interleaved, STG.64 planar):
-            // half the store instructions of one-RE-per-lane, which measurably
-            // raises the write bandwidth of 4 storing warps (tools/write_bw).
             const bool odd = (j & 1) != 0;
             if constexpr (!(DBG & 2) && kStageR) {
                 // staged: both blocks of the tile in their global layout in shared memory,
@@ -715,9 +715,11 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
             } else if constexpr (!(DBG & 2) && (LAYOUT == 2 || LAYOUT == 3)) {
-                // 16-bit output, direct stores (int16 output at f <= 12; see kStageR): pack
-                // all 16 pairs first — the shuffles need every lane — then one branch
-                // around the stores, and the output scale read once per tile.
+                // 16-bit output, direct stores (int16 output at f <= 12; see kStageR).
+                // Lane pairs (j even, j + 1) trade values with one shuffle so every lane
+                // stores two adjacent REs (8 bytes) at once; all 16 pairs are packed
+                // first — the shuffles need every lane — then one branch around the
+                // stores, and the output scale is read once per tile.
                 const float osc = J.out_scale;
                 uint2 pk[16];
 #pragma unroll
@@ -739,45 +741,6 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                         const int a = 32 * h + aa;
                         const int e = (a + (odd ? 1 : 0)) * 60 + j - (odd ? 1 : 0);   // element index
                         __stcs(Rw + e / 2, pk[aa / 2]);
-                    }
-                }
-            } else if constexpr (!(DBG & 2)) {
-                if (LAYOUT == 0 || LAYOUT == 2 || LAYOUT == 3) {
-#pragma unroll
-                    for (int aa = 0; aa < 32; aa += 2) {
-                        const int a = 32 * h + aa;
-                        const float re0 = __uint_as_float(v[2 * aa]), im0 = __uint_as_float(v[2 * aa + 1]);
-                        const float re1 = __uint_as_float(v[2 * aa + 2]), im1 = __uint_as_float(v[2 * aa + 3]);
-                        const float gr = __shfl_xor_sync(0xffffffffu, odd ? re0 : re1, 1);
-                        const float gi = __shfl_xor_sync(0xffffffffu, odd ? im0 : im1, 1);
-                        // even lane: antenna a, REs j, j+1; odd lane: antenna a+1, REs j-1, j
-                        const float4 w4 = odd ? make_float4(gr, gi, re1, im1) : make_float4(re0, im0, gr, gi);
-                        const int e = (a + (odd ? 1 : 0)) * 60 + j - (odd ? 1 : 0);   // element index
-                        if (valid) {
-                            if (LAYOUT == 0) {
-                                __stcs(reinterpret_cast<float4 *>(Rb + 2 * e), w4);
-                            } else if (LAYOUT == 3) {   // int16 output: two (re, im) pairs
-                                __stcs(reinterpret_cast<uint2 *>(Rb) + e / 2,
-                                       make_uint2(bfk::pack_i16x2(w4.x, w4.y, J.out_scale),
-                                                  bfk::pack_i16x2(w4.z, w4.w, J.out_scale)));
-                            } else {      // fp16 output: two (re, im) half pairs, 8 bytes
-                                __stcs(reinterpret_cast<uint2 *>(Rb) + e / 2,
-                                       make_uint2(bfk::pack_half2(w4.x, w4.y),
-                                                  bfk::pack_half2(w4.z, w4.w)));
-                            }
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int aa = 0; aa < 32; ++aa) {
-                        const int a = 32 * h + aa;
-                        const float re = __uint_as_float(v[2 * aa]), im = __uint_as_float(v[2 * aa + 1]);
-                        const float g = __shfl_xor_sync(0xffffffffu, odd ? re : im, 1);
-                        // even lane: re plane, REs j, j+1; odd lane: im plane, REs j-1, j
-                        const float2 w2 = odd ? make_float2(g, im) : make_float2(re, g);
-                        if (valid)
-                            __stcs(reinterpret_cast<float2 *>(Rb + (odd ? 64 * 60 : 0) + a * 60 + j - (odd ? 1 : 0)),
-                                   w2);
                     }
                 }
             }
