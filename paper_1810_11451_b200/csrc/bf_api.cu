@@ -616,7 +616,10 @@ bf_status launch_batch(const bf_batch_job *jobs, int n, cudaStream_t st) {
 bf_status apply_device(bf_plan_t p, const void *S, const int32_t *gidx, void *R, int64_t n,
                        cudaStream_t st) {
     if (n == 0) return BF_OK;
-    if (p->f > 0 && gidx && p->n_groups > 1) {
+    // tagged blocks are always routed — also with one group, so that tags outside
+    // [0, n_groups) leave their blocks unwritten as bf.h states (a caller with one W
+    // and no tags passes group_idx = NULL and skips the routing)
+    if (p->f > 0 && gidx) {
         bf_status s;
         if ((s = grow(&p->perm, &p->perm_cap, n, "perm")) != BF_OK) return s;
         if ((s = grow(&p->offsets, &p->offsets_cap, p->n_groups + 2, "offsets")) != BF_OK) return s;
@@ -898,7 +901,7 @@ bf_status bf_apply_host(bf_plan_t p, const void *S_host, const int32_t *group_id
     if (s != BF_OK || n_blocks == 0) return s;
     DeviceGuard guard(p->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const bool tagged = group_idx_host != nullptr && p->n_groups > 1;
+    const bool tagged = group_idx_host != nullptr;
     if ((s = ensure_host_pipeline(p, tagged)) != BF_OK) return s;
     const int64_t C = p->host_chunk;
     const size_t s_blk = (size_t)480 * p->f, r_blk = (size_t)bfk::r_block_bytes(p->layout);

@@ -291,6 +291,27 @@ def test_invalid_tags_are_left_unwritten_and_checked(monkeypatch, variant):
     assert e.value.status == bf.Status.INVALID_VALUE
 
 
+def test_invalid_tags_with_one_group(variant):
+    """One precoder group and tags: the tags are still honoured (bf.h), so a tag other than 0
+    leaves its block unwritten — the single-group shortcut applies only to group_idx = NULL.
+    Found by tools/stress_tc.py."""
+    W = syn.precoders(8, 12, 1, 64, 12, "unit_columns")
+    S = syn.qam_symbols(8, 12, np.arange(50), 12, 60, 64)
+    tags = np.zeros(50, np.int32)
+    tags[[3, 40]] = [1, -7]
+    plan = Plan(f=12, variant=variant)
+    plan.set_precoders(torch.from_numpy(W).to(DEV))
+    R = torch.full((50, 64, 60), 7.0, dtype=torch.complex64, device=DEV)
+    plan.apply(torch.from_numpy(S).to(DEV), torch.from_numpy(tags).to(DEV), out=R)
+    torch.cuda.synchronize()
+    Rn = R.cpu().numpy()
+    assert (Rn[[3, 40]] == 7.0).all()
+    ok = np.setdiff1d(np.arange(50), [3, 40])
+    R_ref, T, _ = oracle.beamform(W, S[ok], None, n_threads=NT)
+    assert_parity(Rn[ok], R_ref, T, what="one group, valid tags")
+    plan.close()
+
+
 # ---------------------------------------------------------------------------
 # error paths of the C ABI
 # ---------------------------------------------------------------------------
