@@ -9,7 +9,9 @@ reloads and the staged / direct epilogues meet many shapes the fixed tests do no
 Per trial: fp32 layouts must agree within 2e-5 * T (T = sum |w||s|, both kernels are
 inside 1e-5 * T of the exact result), blocks with invalid tags must be left untouched by
 both, and the 16-bit layouts must equal the tensor kernel's own fp32 result rounded (fp16
-RN; int16 sat(rne(R * 2^12))).  Not a test of the oracle (tests/ does that); a bug hunt.
+RN; int16 sat(rne(R * 2^12))).  Then random bf_apply_batch job lists (any f, one layout,
+tagged or not) against the jobs' own apply_routed calls, bitwise.  Not a test of the oracle
+(tests/ does that); a bug hunt.
 """
 import argparse
 import json
@@ -95,8 +97,49 @@ def main():
                           "max_err_over_T": float((err[valid] / (T[valid] + 1e-30)).max()) if n_bad < n else 0.0,
                           "ok": ok, "untouched": untouched, "planar_eq": planar_eq, "f16_eq": f16_eq,
                           "i16_eq": i16_eq}), flush=True)
-    print(json.dumps({"trials": a.trials, "failed": bad, "seconds": time.time() - t0}))
-    return 1 if bad else 0
+    # bf_apply_batch: random job lists (any f, one layout, some untagged) must equal the
+    # jobs' own apply_routed calls on the tensor kernel, bitwise
+    from paper_1810_11451_b200 import apply_batch
+    bbad = 0
+    for trial in range(a.trials // 4):
+        layout = [Layout.INTERLEAVED, Layout.PLANAR, Layout.INTERLEAVED_F16OUT,
+                  Layout.INTERLEAVED_I16OUT][int(rng.integers(0, 4))]
+        jobs, refs, keep = [], [], []
+        for _ in range(int(rng.integers(1, 17))):
+            f = int(rng.integers(1, 37))
+            n = int(rng.choice([1, 3, 64, 777, 4096]))
+            G = int(rng.choice([1, 7, 55]))
+            p = Plan(f=f, layout=layout, variant=Variant.AUTO)
+            Wc = torch.randn(G, 64, f, dtype=torch.complex64, device=DEV) / f ** 0.5
+            Sc = torch.randn(n, f, 60, dtype=torch.complex64, device=DEV)
+            if layout == Layout.PLANAR:
+                Wc = torch.stack([Wc.real, Wc.imag], 1).contiguous()
+                Sc = torch.stack([Sc.real, Sc.imag], 1).contiguous()
+            p.set_precoders(Wc)
+            if rng.random() < 0.3:
+                perm = offs = None
+            else:
+                tags = torch.from_numpy(rng.integers(0, G, n).astype(np.int32)).to(DEV)
+                perm, offs = p.route(tags)
+            out = torch.zeros(p.r_shape(n), dtype=p.r_dtype, device=DEV)
+            jobs.append((p, Sc, perm, offs, out))
+            q = Plan(f=f, layout=layout, variant=Variant.TENSOR)
+            q.set_precoders(Wc)
+            ref = torch.zeros_like(out)
+            q.apply_routed(Sc, perm, offs, out=ref)
+            refs.append(ref)
+            keep += [p, q]
+        apply_batch(jobs)
+        torch.cuda.synchronize()
+        eq = all(torch.equal(j[4], r) for j, r in zip(jobs, refs))
+        bbad += 0 if eq else 1
+        print(json.dumps({"batch_trial": trial, "layout": layout.name, "jobs": len(jobs),
+                          "f": [j[0].f for j in jobs], "equal": eq}), flush=True)
+        for p in keep:
+            p.close()
+    print(json.dumps({"trials": a.trials, "failed": bad, "batch_trials": a.trials // 4,
+                      "batch_failed": bbad, "seconds": time.time() - t0}))
+    return 1 if bad or bbad else 0
 
 
 if __name__ == "__main__":
