@@ -567,6 +567,70 @@ def run_filter(args, wl, world, rank, local, dev):
     bytes_launch = wl.signal_bytes * n_loc
     achieved = bytes_launch / (kavg * 1e-3) / 1e9
     value = wl.n_signals * wl.n * args.steps / (elapsed * 1e-3)
+    # DRAM bytes per signal from the committed ncu capture, scaled to this launch
+    traffic, tbasis = None, None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["bff::filter_kernel"]
+        traffic = tr["dram_bytes_per_signal"] * n_loc
+        tbasis = f"{tr['capture']}: {tr['dram_bytes_per_signal']:.0f} B/signal x {n_loc} signals"
+    except (OSError, KeyError, ValueError):
+        pass
+
+    # ---- e2e: pinned host signals -> H2D -> filter -> D2H, chunked on three streams --------
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        chunk = 16384
+        n_e2e = n_loc if args.e2e_blocks <= 0 else min(args.e2e_blocks, n_loc)
+        sh = torch.empty((n_e2e, wl.n), dtype=torch.complex64).pin_memory()
+        sh.copy_(s[:n_e2e])
+        yh = torch.empty_like(sh).pin_memory()
+        del s, y
+        torch.cuda.empty_cache()
+        slots = 3
+        dS = [torch.empty((chunk, wl.n), dtype=torch.complex64, device=dev) for _ in range(slots)]
+        st_h2d, st_cmp, st_d2h = (torch.cuda.Stream(dev) for _ in range(3))
+        ev_h = [torch.cuda.Event() for _ in range(slots)]
+        ev_c = [torch.cuda.Event() for _ in range(slots)]
+        ev_d = [torch.cuda.Event() for _ in range(slots)]
+
+        def e2e_step():
+            for i, c0 in enumerate(range(0, n_e2e, chunk)):
+                k, nc = i % slots, min(chunk, n_e2e - c0)
+                with torch.cuda.stream(st_h2d):
+                    if i >= slots:
+                        st_h2d.wait_event(ev_d[k])          # slot k's previous result left
+                    dS[k][:nc].copy_(sh[c0:c0 + nc], non_blocking=True)
+                    ev_h[k].record(st_h2d)
+                st_cmp.wait_event(ev_h[k])
+                plan.apply(dS[k][:nc], out=dS[k][:nc], stream=st_cmp)   # in place
+                ev_c[k].record(st_cmp)
+                with torch.cuda.stream(st_d2h):
+                    st_d2h.wait_event(ev_c[k])
+                    yh[c0:c0 + nc].copy_(dS[k][:nc], non_blocking=True)
+                    ev_d[k].record(st_d2h)
+            main.wait_stream(st_d2h)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(main)
+        st_h2d.wait_stream(main)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+            st_h2d.wait_stream(main)
+        f1.record(main)
+        torch.cuda.synchronize()
+        e2e_ms = shard.max_over_ranks(f0.elapsed_time(f1), dev)
+        n_tot = int(shard.sum_over_ranks(n_e2e, dev))
+        e2e = {"value": n_tot * wl.n * args.e2e_steps / (e2e_ms * 1e-3), "unit": "samples/s",
+               "h2d_bytes_per_step": n_tot * wl.n * 8, "d2h_bytes_per_step": n_tot * wl.n * 8,
+               "steps": args.e2e_steps, "signals_per_step": n_tot,
+               "ms_per_step": e2e_ms / args.e2e_steps,
+               "path": "pinned host signals -> H2D -> FilterPlan.apply (bff_apply, in place) -> "
+                       "D2H pinned, 16384-signal chunks on three streams"}
+        del sh, yh, dS
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import time as _t
@@ -596,11 +660,12 @@ def run_filter(args, wl, world, rank, local, dev):
                        "parallelism": f"dp{world}", "l2": "inputs larger than L2",
                        "gpu": torch.cuda.get_device_name(dev)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
-                         "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                         "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                         "traffic_basis": tbasis,
                          "kernel": "bff::filter_kernel", "kernel_ms": kavg,
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "peak_basis": peak_basis(peaks)},
-            "cpu_baseline": cpu, "e2e": None, "gpu_launches": launches, "clocks": clk,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
