@@ -61,6 +61,18 @@ def test_bench_c2_single_gpu_contract():
     assert d["e2e"]["h2d_bytes_per_step"] == 770 * 480 * 36
     assert d["e2e"]["d2h_bytes_per_step"] == 770 * 30720
     assert d["gpu_launches"] >= 5
+    assert d["config"]["submission"] == "cuda_graph"
+    assert "split precision" in d["config"]["arith"]
+
+
+def test_bench_filter_contract():
+    d = _run(["--config", "fl1", "--steps", "3", "--warmup", "3", "--cpu-seconds", "1",
+              "--e2e-steps", "1"])
+    for k in KEYS:
+        assert k in d, k
+    assert d["unit"] == "samples/s" and d["value"] > 0
+    assert 0 < d["roofline"]["frac"] < 1.2 and d["roofline"]["traffic"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == d["e2e"]["d2h_bytes_per_step"] == (1 << 18) * 2048 * 8
 
 
 def test_bench_c4_two_ranks_share_gpu():
