@@ -47,9 +47,10 @@ constexpr size_t kMaxProfEvents = 1 << 16;  // timed launches kept between kerne
 // epilogues): the smallest f from which the tensor-core kernel is faster.  Below it
 // both kernels are store-bound and within a few percent: interleaved f = 1 (equal),
 // planar f <= 6 (within +-4 %), fp16 output f <= 3 (FFMA 5-16 % ahead), int16 output
-// f <= 2 (FFMA 0.32 vs 0.41 ms at f = 1; profiles/r01_sweep_i16_v6.txt).  From there on
+// f <= 3 (FFMA 0.32 vs 0.43 ms at f = 1; profiles/r01_sweep_auto_v7.jsonl, 18-warp tensor
+// kernel).  From there on
 // the tensor kernel wins, by 2.2-2.6x at f = 36.
-constexpr int kAutoTensorMinF[4] = {2, 7, 4, 3};   // [layout]
+constexpr int kAutoTensorMinF[4] = {2, 7, 4, 4};   // [layout]
 
 BfKernelTable g_table;      // FFMA kernels [f][layout]
 BfKernelTable g_table_tc;   // tcgen05 split-TF32 kernels [f][layout]

@@ -21,18 +21,19 @@
 // Dropped terms are <= ~2^-21 T; with the tensor accumulation the error stays
 // near 2e-6 T at f = 36, inside the 1e-5 T contract.
 //
-// One CTA (14 warps) per SM, persistent over a cost-balanced range of the
+// One CTA (18 warps) per SM, persistent over a cost-balanced range of the
 // group-sorted block list (cta_range); tiles are 2 consecutive blocks of one group.
-//   warp 13    producer: cp.async.bulk (TMA bulk engine) of each block's 480 F
+//   warp 17    producer: cp.async.bulk (TMA bulk engine) of each block's 480 F
 //              contiguous bytes into a 2-4-stage shared-memory ring, completing on
 //              mbarriers, up to kStages tiles ahead of the split; and the pre-split
 //              B image (W) of each group segment into its W buffer (two where shared
 //              memory allows: the next group's image loads while the current one's
 //              MMAs run);
-//   warps 0-3  split: LDS S (conflict-free, one RE column per lane), split into
+//   warps 0-7  split (two per TMEM lane quarter, each half of the K columns above
+//              f = 12): LDS S (conflict-free, one RE column per lane), split into
 //              the terms, tcgen05.st into the A regions (one TMEM lane per RE);
-//   warp 4     MMA issuer (one thread);
-//   warps 5-12 epilogue (two per lane quarter, half the D columns each): tcgen05.ld
+//   warp 8     MMA issuer (one thread);
+//   warps 9-16 epilogue (two per lane quarter, half the D columns each): tcgen05.ld
 //              of the thread's D row half, release of the TMEM buffer, then the
 //              tile's two R blocks written into a shared-memory stage in their
 //              global layout and stored by one thread with one bulk copy per block
@@ -50,12 +51,12 @@
 
 namespace bftc {
 
-constexpr int kThreads = 448;
-constexpr int kSplitWarps = 4;
-constexpr int kMmaWarp = 4;
-constexpr int kEpiWarp0 = 5;
+constexpr int kSplitWarps = 8;        // two per TMEM lane quarter, half the K columns each
+constexpr int kMmaWarp = 8;
+constexpr int kEpiWarp0 = 9;
 constexpr int kEpiWarps = 8;          // two per TMEM lane quarter, 64 D columns each
-constexpr int kProdWarp = 13;
+constexpr int kProdWarp = 17;
+constexpr int kThreads = 32 * (kProdWarp + 1);
 #ifndef BFTC_MAX_STAGES
 #define BFTC_MAX_STAGES 4
 #endif
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
     if (threadIdx.x == 32) {
         for (int i = 0; i < 3; ++i) {
-            bfk::mbar_init(bar_a_full + i, 128);
+            bfk::mbar_init(bar_a_full + i, 32 * kSplitWarps);
             bfk::mbar_init(bar_a_free + i, 1);
         }
         bfk::mbar_init(bar_d_full + 0, 1);
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         }
         for (int i = 0; i < kRing; ++i) {
             bfk::mbar_init(bar_s_full + i, 1);
-            bfk::mbar_init(bar_s_empty + i, 128);
+            bfk::mbar_init(bar_s_empty + i, 32 * kSplitWarps);
         }
         bfk::mbar_fence_init();
     }
@@ -422,9 +423,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
 
     if (warp < kSplitWarps) {
         // ------------------------------------------------------------ split warps
-        const int m = warp * 32 + lane;                  // TMEM lane == A row
+        const int m = (warp & 3) * 32 + lane;            // TMEM lane == A row
+        const int ks = warp >> 2;                        // K half: chunks [0, h) or [h, end)
         const int bsel = m >= 60 ? 1 : 0, j = m - 60 * bsel;
-        const uint32_t a_lane = tmem + ((uint32_t)(warp * 32) << 16);
+        const uint32_t a_lane = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         int cur_g = -1, cur_j = -1;
         bool cur_exact = false;
         for (int64_t t = 0; it.next(tl); ++t) {
@@ -458,8 +460,13 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 }
                 // DBG 32: S1 as fp16 pairs over K rounded up to 16 (one more chunk at f = 36)
                 const int kend = ((DBG & 32) && term == 0) ? (KP + 15) / 16 * 16 : KP;
+                // this warp's K chunks; at f <= 12 (<= 3 chunks) the second warp of each
+                // quarter only keeps the barrier counts (splitting measured slower there)
+                const int c_half = (F > 0 && F <= 12) ? kend : ((kend / 8 + 1) >> 1) * 8;
+                const int c_beg = ks ? c_half : 0, c_end = ks ? kend : c_half;
 #pragma unroll
                 for (int c0 = 0; c0 < kend; c0 += 8) {
+                    if (c0 < c_beg || c0 >= c_end) continue;
                     float x[8];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
@@ -672,6 +679,52 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             bfk::mbar_wait(bar_d_full + b, u & 1);
             tc::fence_after_sync();
             const uint32_t d = tmem + ((uint32_t)(q * 32) << 16) + kDCol0 + 128 * b + 64 * h;
+            if constexpr (!(DBG & 2) && !kStageR && (LAYOUT == 2 || LAYOUT == 3)) {
+                // 16-bit output, direct stores (int16 output at f <= 12; see kStageR), in
+                // two halves of 16 antennas to stay inside the register budget of 18 warps:
+                // load 32 D columns, pack, store; the TMEM buffer is released after the
+                // second load (the MMA needs it again only two tiles later).  Lane pairs
+                // (j even, j + 1) trade values with one shuffle so every lane stores two
+                // adjacent REs (8 bytes) at once; a half's 8 pairs are packed first — the
+                // shuffles need every lane — then one branch around their stores.
+                const bool odd = (j & 1) != 0;
+                const float osc = J.out_scale;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    uint32_t v[32];
+                    tc::tmem_ld16(d + 32 * half, *reinterpret_cast<uint32_t(*)[16]>(v));
+                    tc::tmem_ld16(d + 32 * half + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+                    tc::tmem_ld_wait();
+                    if (half == 1) {
+                        tc::fence_before_sync();
+                        mbar_arrive(bar_d_free + b);     // TMEM buffer b may be overwritten
+                    }
+                    uint2 pk[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int aa = 2 * i;            // antenna pair within the half
+                        const float re0 = __uint_as_float(v[2 * aa]), im0 = __uint_as_float(v[2 * aa + 1]);
+                        const float re1 = __uint_as_float(v[2 * aa + 2]), im1 = __uint_as_float(v[2 * aa + 3]);
+                        const float gr = __shfl_xor_sync(0xffffffffu, odd ? re0 : re1, 1);
+                        const float gi = __shfl_xor_sync(0xffffffffu, odd ? im0 : im1, 1);
+                        // even lane: antenna a, REs j, j+1; odd lane: antenna a+1, REs j-1, j
+                        const float4 w4 = odd ? make_float4(gr, gi, re1, im1) : make_float4(re0, im0, gr, gi);
+                        pk[i] = LAYOUT == 3
+                                    ? make_uint2(bfk::pack_i16x2(w4.x, w4.y, osc), bfk::pack_i16x2(w4.z, w4.w, osc))
+                                    : make_uint2(bfk::pack_half2(w4.x, w4.y), bfk::pack_half2(w4.z, w4.w));
+                    }
+                    if (valid) {
+                        uint2 *Rw = reinterpret_cast<uint2 *>(Rb);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int a = 32 * h + 16 * half + 2 * i;
+                            const int e = (a + (odd ? 1 : 0)) * 60 + j - (odd ? 1 : 0);   // element index
+                            __stcs(Rw + e / 2, pk[i]);
+                        }
+                    }
+                }
+                continue;
+            }
             uint32_t v[64];
 #pragma unroll
             for (int c0 = 0; c0 < 64; c0 += 16)
@@ -713,35 +766,6 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                         bulk_s2g(J.R + block_of(J, tl.item + b2) * (int64_t)rbf, Rst + b2 * rbf,
                                  (uint32_t)bfk::r_block_bytes(LAYOUT), pol_r);
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                }
-            } else if constexpr (!(DBG & 2) && (LAYOUT == 2 || LAYOUT == 3)) {
-                // 16-bit output, direct stores (int16 output at f <= 12; see kStageR).
-                // Lane pairs (j even, j + 1) trade values with one shuffle so every lane
-                // stores two adjacent REs (8 bytes) at once; all 16 pairs are packed
-                // first — the shuffles need every lane — then one branch around the
-                // stores, and the output scale is read once per tile.
-                const float osc = J.out_scale;
-                uint2 pk[16];
-#pragma unroll
-                for (int aa = 0; aa < 32; aa += 2) {
-                    const float re0 = __uint_as_float(v[2 * aa]), im0 = __uint_as_float(v[2 * aa + 1]);
-                    const float re1 = __uint_as_float(v[2 * aa + 2]), im1 = __uint_as_float(v[2 * aa + 3]);
-                    const float gr = __shfl_xor_sync(0xffffffffu, odd ? re0 : re1, 1);
-                    const float gi = __shfl_xor_sync(0xffffffffu, odd ? im0 : im1, 1);
-                    // even lane: antenna a, REs j, j+1; odd lane: antenna a+1, REs j-1, j
-                    const float4 w4 = odd ? make_float4(gr, gi, re1, im1) : make_float4(re0, im0, gr, gi);
-                    pk[aa / 2] = LAYOUT == 3
-                                     ? make_uint2(bfk::pack_i16x2(w4.x, w4.y, osc), bfk::pack_i16x2(w4.z, w4.w, osc))
-                                     : make_uint2(bfk::pack_half2(w4.x, w4.y), bfk::pack_half2(w4.z, w4.w));
-                }
-                if (valid) {
-                    uint2 *Rw = reinterpret_cast<uint2 *>(Rb);
-#pragma unroll
-                    for (int aa = 0; aa < 32; aa += 2) {
-                        const int a = 32 * h + aa;
-                        const int e = (a + (odd ? 1 : 0)) * 60 + j - (odd ? 1 : 0);   // element index
-                        __stcs(Rw + e / 2, pk[aa / 2]);
-                    }
                 }
             }
         }
