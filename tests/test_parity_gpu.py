@@ -862,3 +862,23 @@ def test_smem_configs_with_group_changes(f):
     expect16 = R32.real.astype(np.float16).astype(np.float64) + 1j * R32.imag.astype(np.float16).astype(np.float64)
     assert np.array_equal(h[..., 0] + 1j * h[..., 1], expect16)
     assert np.array_equal(run_shared(W, S, tags, Layout.INTERLEAVED_I16OUT, 3), host_i16(R32, 12))
+
+
+@pytest.mark.parametrize("layout", [Layout.INTERLEAVED, Layout.PLANAR])
+@pytest.mark.parametrize("f", [5, 13, 36])
+def test_exact_and_general_groups_interleaved(f, layout):
+    """Groups whose W is exactly tf32 (selection: the S1/S2/S3 path, bit-exact) and general
+    groups (S1 alternating between two TMEM regions) in one launch, many group changes per CTA
+    (2 SMs): every block against the oracle, the selection groups bit for bit."""
+    G, n = 6, 2400
+    W = syn.precoders(33, f, G, 64, f, "unit_columns")
+    for g in (1, 4):                                   # selection precoders: tf32-exact
+        W[g] = 0
+        W[g][np.arange(64), np.arange(64) % f] = 1 if g == 1 else -2
+    S = syn.qam_symbols(33, f, np.arange(n), f, 60, 64)
+    tags = syn.subband_tags(33, np.arange(n), G)
+    R_ref, T, _ = oracle.beamform(W, S, tags, n_threads=NT)
+    R = run_shared(W, S, tags, layout, 2)
+    assert_parity(R, R_ref, T, what=f"f={f} exact+general")
+    sel = np.isin(tags, [1, 4])
+    assert np.array_equal(R[sel], R_ref[sel]), "selection groups must be bit-exact"
