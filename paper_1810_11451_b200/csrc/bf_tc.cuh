@@ -439,14 +439,41 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             const float *Sb = Ss + (stage * 2 + (valid ? bsel : 0)) * (L::kSBlock / 4);
             // Term order S2, S3, S1 mirrors the MMA order, so each region is rewritten
             // as soon as the previous tile's MMAs on it have completed and the tensor
-            // pipe keeps running on the other terms meanwhile.  S is re-read from the
-            // ring for every term (cheap LDS) instead of being held in 2F registers.
+            // pipe keeps running on the other terms meanwhile.
             // tcgen05.st is warp-collective: every lane stores (invalid rows store 0).
             const uint32_t par = (uint32_t)((t & 1) ^ 1);
             if (tl.g != cur_g || tl.job != cur_j) {
                 cur_g = tl.g;
                 cur_j = tl.job;
                 cur_exact = __ldg(J.wexact + tl.g) != 0;
+            }
+            // This warp's K chunks of the thread's row of S (half of them above f = 12) are
+            // read from the ring once into registers and the slot is released at once; the
+            // term passes split from registers.
+            constexpr int kSlots = (F > 0 && F <= 12) ? L::KP / 8 : ((L::KP / 8 + 1) >> 1);
+            const int c_half0 = (F > 0 && F <= 12) ? KP : ((KP / 8 + 1) >> 1) * 8;
+            const int c_beg0 = ks ? c_half0 : 0, c_end0 = ks ? KP : c_half0;
+            float xs[kSlots * 8];
+#pragma unroll
+            for (int i = 0; i < kSlots; ++i) {
+                const int c0 = c_beg0 + 8 * i;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int k = c0 / 2 + q;
+                    float re = 0.0f, im = 0.0f;
+                    if (c0 < c_end0 && k < f && valid) {
+                        if (LAYOUT != 1) {
+                            const float2 v = reinterpret_cast<const float2 *>(Sb)[k * 60 + j];
+                            re = v.x;
+                            im = v.y;
+                        } else {
+                            re = Sb[k * 60 + j];
+                            im = Sb[f * 60 + k * 60 + j];
+                        }
+                    }
+                    xs[8 * i + 2 * q] = re;
+                    xs[8 * i + 2 * q + 1] = im;
+                }
             }
 #pragma unroll
             for (int pass = 0; pass < 3; ++pass) {
@@ -465,26 +492,12 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 const int c_half = (F > 0 && F <= 12) ? kend : ((kend / 8 + 1) >> 1) * 8;
                 const int c_beg = ks ? c_half : 0, c_end = ks ? kend : c_half;
 #pragma unroll
-                for (int c0 = 0; c0 < kend; c0 += 8) {
-                    if (c0 < c_beg || c0 >= c_end) continue;
+                for (int i = 0; i < kSlots; ++i) {
+                    const int c0 = c_beg + 8 * i;
+                    if (c0 >= c_end) break;
                     float x[8];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int k = c0 / 2 + q;
-                        float re = 0.0f, im = 0.0f;
-                        if (k < f && valid) {
-                            if (LAYOUT != 1) {
-                                const float2 v = reinterpret_cast<const float2 *>(Sb)[k * 60 + j];
-                                re = v.x;
-                                im = v.y;
-                            } else {
-                                re = Sb[k * 60 + j];
-                                im = Sb[f * 60 + k * 60 + j];
-                            }
-                        }
-                        x[2 * q] = re;
-                        x[2 * q + 1] = im;
-                    }
+                    for (int e = 0; e < 8; ++e) x[e] = xs[8 * i + e];
                     uint32_t v[8];
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
