@@ -6,7 +6,8 @@ at 64 antennas, f = 36, b = 60, and % of roofline at 1/2/4/8 B200).
     torchrun --nproc-per-node N ... bench.py --gpus N      (one rank per GPU, NCCL)
 
 A step is one bf_apply over the whole (per-rank shard of the) workload: block ->
-group routing + the FFMA beamforming kernel, inputs resident in HBM.  The
+group routing + the beamforming kernel AUTO picks (the tcgen05 split-precision
+kernel at f = 36), inputs resident in HBM.  The
 default workload is config c4 (BASELINE.json configs[3], the metric's
 headline: 55 precoders 64x36, 2^20 tagged 64-QAM blocks), which fits one GPU;
 S (18.1 GB) + R (32.2 GB) exceed the 126 MB L2, so no flush is needed.
@@ -50,6 +51,12 @@ def parse():
                     help="target CPU work of the oracle baseline sample")
     ap.add_argument("--c5-chunks", type=int, default=0, help="c5: chunks per step (0 = all 2048)")
     ap.add_argument("--no-graph", action="store_true", help="c5: launch eagerly, no CUDA graph")
+    ap.add_argument("--steady-seconds", type=float, default=10.0,
+                    help="after the timed burst, back-to-back steps for this long: steady-state "
+                         "throughput, SM clock and power under the board's power cap (0 = off)")
+    ap.add_argument("--parity-stride", type=int, default=16,
+                    help="check every k-th block of each rank's output against the oracle after "
+                         "the timed region (c4: 65 536 of 2^20 blocks; c2: every block)")
     ap.add_argument("--c5-batch", type=int, default=8,
                     help="c5: consecutive chunks per bf_apply_batch launch (1 = one bf_apply_routed per chunk)")
     return ap.parse_args()
@@ -161,6 +168,112 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+# parity of the timed output (outputs are checked against the oracle
+# before a number is printed).  Runs after the timed region, on the R it
+# left behind; every rank checks its own shard.
+# ---------------------------------------------------------------------------
+TOL = 1e-5   # BASELINE.json north_star item 4: |R_gpu - R_ref| <= 1e-5 sum_k |w_ik| |s_kj|
+
+
+def _bound_T(W, S, tags):
+    """T[n][i][j] = sum_k |W[g(n)][i][k]| |S[n][k][j]| in fp64 (the tolerance scale), as a
+    plain matrix product of the moduli."""
+    Wa = np.abs(W.astype(np.complex128))
+    Sa = np.abs(S.astype(np.complex128))
+    g = np.zeros(len(S), np.int64) if tags is None else tags.astype(np.int64)
+    return np.matmul(Wa[g], Sa)
+
+
+def compare_block_sample(R_ref, T, got, layout: str, out_exp: int = 12):
+    """Worst error of sampled output blocks in units of their limit (<= 1 passes):
+    fp32 layouts |dR| <= 1e-5 T (complex modulus); fp16 output |dR| <= sqrt(2) 2^-11 |R| +
+    1e-5 T + 2^-24; int16 output |R16 2^-e - R| <= sqrt(2) 2^-(e+1) + 1e-5 T off saturation."""
+    ref = R_ref.astype(np.complex128)
+    if layout in ("interleaved", "planar"):
+        err = np.abs(got.astype(np.complex128) - ref)
+        lim = TOL * T
+        rel = np.where(T > 0, err / np.where(T > 0, T, 1.0), np.where(err > 0, np.inf, 0.0))
+        worst_T = float(rel.max()) if rel.size else 0.0
+        ok = bool((err <= lim).all())
+        return {"worst_err_over_T": worst_T, "ok": ok}
+    g = got.astype(np.float64)
+    if layout == "interleaved_f16out":
+        val = g[..., 0] + 1j * g[..., 1]
+        lim = np.sqrt(2) * 2.0 ** -11 * np.abs(ref) + TOL * T + 2.0 ** -24
+        unsat = np.ones(val.shape, bool)
+    else:
+        val = (g[..., 0] + 1j * g[..., 1]) * 2.0 ** -out_exp
+        lim = np.sqrt(2) * 2.0 ** -(out_exp + 1) + TOL * T
+        big = 32767 * 2.0 ** -out_exp
+        unsat = (np.abs(ref.real) < big) & (np.abs(ref.imag) < big)
+    err = np.abs(val - ref)
+    rel = np.where(unsat, err / lim, 0.0)
+    return {"worst_err_over_limit": float(rel.max()) if rel.size else 0.0,
+            "ok": bool((rel <= 1.0).all()), "saturated_elements": int((~unsat).sum())}
+
+
+def parity_of_blocks(wl, R_dev, local_pos, global_ids, layout, out_exp=12, chunk=4096,
+                     inputs=None):
+    """Regenerate the sampled blocks on the host (bf_synth), run the oracle on them and
+    compare with the device output R_dev[local_pos].  inputs(global_ids) -> (W, S, tags)
+    overrides the workload's own generator (c5)."""
+    import torch
+
+    import bf_synth as syn
+    import oracle
+    thr = oracle.max_threads()
+    res = {"blocks": int(len(local_pos)), "ok": True}
+    worst_key = "worst_err_over_T" if layout in ("interleaved", "planar") else "worst_err_over_limit"
+    worst = 0.0
+    sat = 0
+    t0 = time.perf_counter()
+    for c0 in range(0, len(local_pos), chunk):
+        lp = np.asarray(local_pos[c0:c0 + chunk])
+        gid = np.asarray(global_ids[c0:c0 + chunk])
+        W, S, tags = inputs(gid) if inputs else syn.workload_inputs(wl, gid)
+        R_ref, _, _ = oracle.beamform(W, S, tags, n_threads=thr, bound=False)
+        T = _bound_T(W, S, tags)
+        got = R_dev[torch.from_numpy(lp).to(R_dev.device)].cpu().numpy()
+        if layout == "planar":
+            got = syn.from_planar(got)
+        r = compare_block_sample(R_ref, T, got, layout, out_exp)
+        worst = max(worst, r[worst_key])
+        sat += r.get("saturated_elements", 0)
+        res["ok"] = res["ok"] and r["ok"]
+    res[worst_key] = worst
+    if layout == "interleaved_i16out":
+        res["saturated_elements"] = sat
+    res["tol"] = TOL
+    res["oracle_threads"] = thr
+    res["check_s"] = time.perf_counter() - t0
+    return res
+
+
+def reduce_parity(res: dict, dev, world: int) -> dict:
+    """Every rank's parity result on rank 0: ok = all ranks ok, worst = max over ranks."""
+    if world == 1:
+        return res
+    import torch
+    import torch.distributed as dist
+    key = "worst_err_over_T" if "worst_err_over_T" in res else "worst_err_over_limit"
+    t = torch.tensor([res[key], 0.0 if res["ok"] else 1.0, float(res["blocks"])], dtype=torch.float64,
+                     device=dev)
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    rows = [o.cpu().tolist() for o in out]
+    return {**res, key: max(r[0] for r in rows), "ok": all(r[1] == 0.0 for r in rows),
+            "blocks": int(sum(r[2] for r in rows)),
+            "per_rank": [{key: r[0], "ok": r[1] == 0.0, "blocks": int(r[2])} for r in rows]}
+
+
+def refuse(line: dict, parity: dict) -> int:
+    """A parity failure prints no throughput (the number would be of a wrong result)."""
+    print(json.dumps({"metric": line.get("metric"), "value": None, "error": "parity check failed",
+                      "parity": parity, "config": line.get("config")}), flush=True)
+    return 3
+
+
+# ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 def host_ram_available() -> int:
@@ -182,8 +295,9 @@ def peak_basis(peaks: dict) -> str:
 
 # What the beamforming product is computed in (the line's "dtype" is its fp32 summary).
 ARITH = {
-    "tensor": "tcgen05 split precision: S1*W1 tf32 + (S2*W1 + S1*W2) one bf16 group, fp32 accumulate "
-              "in TMEM (tf32-exact W: S1+S2+S3 tf32 terms, bit-exact copies); DESIGN.md §7",
+    "tensor": "tcgen05 split precision, all kind::tf32 (exact products): S2*W1 + S1*W2 + S1*W1, fp32 "
+              "accumulate in TMEM (tf32-exact W: S2*W1 + S3*W1 + S1*W1, bit-exact copies); out-of-domain "
+              "blocks recomputed with FFMA arithmetic; DESIGN.md §7",
     "ffma": "fp32 FFMA, 4 per complex MAC, k ascending",
 }
 
@@ -247,6 +361,11 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         if backend == "nccl":
+            # NCCL's communicator-init log (ranks, NVLS / NVLink transport) for the run's
+            # record; to stderr so that stdout keeps the single JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
@@ -377,7 +496,7 @@ def run_ours(args):
     total_blocks = wl.n_blocks
     value = total_blocks * wl.b * args.steps / (elapsed_ms * 1e-3)
 
-    # ---- roofline of the dominant kernel (bf_ffma_kernel) ---------------------------
+    # ---- roofline of the dominant kernel (AUTO: bf_tc_kernel at f = 36) -------------
     peaks = benchkit.measured_peaks()
     cfg = plan.kernel_config(n_local)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -392,8 +511,8 @@ def run_ours(args):
     ai = wl.block_flops / blk_bytes
     variant = plan.variant.name.lower()
     # FFMA kernel: bound by the FP32 pipe when AI x HBM exceeds the FFMA peak.
-    # Tensor kernel: 4 split-TF32 MMAs per K step at ~1.1 PFLOP/s nominal leave
-    # it HBM-bound at every f (the tensor pipe runs < 50 % busy, profiles/).
+    # Tensor kernel: 3 KP/8 tf32 MMAs (K = 8) per 2-block tile at ~1.1 PFLOP/s
+    # nominal leave it HBM-bound at every f (tensor pipe < 50 % busy, profiles/).
     fp32_bound = variant == "ffma" and ai * hbm / 1e3 > peak_max
     # dram bytes of the same kernel from the committed `ncu --set full` capture
     # (profiles/traffic.json, per block), scaled to this launch's block count
@@ -432,6 +551,21 @@ def run_ours(args):
     roof["kernel_share_of_step"] = kern_avg_ms * args.steps / elapsed_ms
     roof["algorithmic_bytes_per_launch"] = bytes_launch
     roof["algorithmic_flops_per_launch"] = flops_launch
+
+    # ---- parity of the timed output: a seeded sample of every rank's blocks vs the oracle
+    stride = 1 if n_local <= 4096 else max(1, args.parity_stride)
+    local_pos = np.arange(0, n_local, stride, dtype=np.int64)
+    parity = parity_of_blocks(wl, R, local_pos, ids[local_pos], args.layout, out_exp=12)
+    parity["sample"] = (f"every {stride}th block of each rank's output after the timed steps, "
+                        "regenerated on the host (bf_synth) and compared with the fp64 oracle")
+    parity = reduce_parity(parity, dev, world)
+
+    # ---- steady state: the same step back to back for --steady-seconds (the timed burst
+    #      above is ~0.2 s; the board's 1000 W cap takes ~0.3 s to bite)
+    steady = None
+    if args.steady_seconds > 0 and not small:
+        steady = steady_state(args, plan, S, tags, R, local, rank, world, dev,
+                              bytes_launch, n_local * wl.b, peaks["hbm_gbs"])
 
     # ---- e2e through the public API with host buffers ---------------------------------
     e2e = None
@@ -496,11 +630,12 @@ def run_ours(args):
             "metric": "beamformed REs/s (64 ant, f=36, b=60)", "value": value, "unit": "REs/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "parity": parity,
             "config": {"workload": wl.name, "desc": wl.desc, "n_ant": wl.n_ant, "f": wl.f,
                        "b": wl.b, "blocks": wl.n_blocks, "groups": wl.n_groups,
                        "layout": args.layout, "parallelism": f"dp{world} (blocks sharded by subband)"
                        if wl.tagged else f"dp{world}",
+                       "world_size": world, "backend": dist.get_backend() if world > 1 else None,
                        "l2": "inputs larger than L2 (S+R >> 126 MB)" if not small
                        else "L2 flushed between steps (512 MB write outside the timed events)",
                        "submission": "eager" if not small else submission,
@@ -509,17 +644,82 @@ def run_ours(args):
                        else ARITH.get(roof.get("variant"), "?")},
             "flops_per_s": total_blocks * wl.block_flops * args.steps / (elapsed_ms * 1e-3),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk,
+            "clocks": clk, "steady": steady,
         }
         if "tflops" in os.environ.get("BF_BENCH_PROBE", "tflops"):
             try:
                 line["ffma_probe"] = benchkit.ffma_probe()
             except Exception as ex:  # pragma: no cover
                 line["ffma_probe"] = {"error": str(ex)}
-        print(json.dumps(line), flush=True)
+        if not parity["ok"]:
+            rc = refuse(line, parity)
+        else:
+            print(json.dumps(line), flush=True)
+            rc = 0
+    else:
+        rc = 0 if parity["ok"] else 3
     if world > 1:
         dist.destroy_process_group()
-    return 0
+    return rc
+
+
+def steady_state(args, plan, S, tags, R, local, rank, world, dev, bytes_launch, res_launch, hbm):
+    """Back-to-back steps for args.steady_seconds of host time, the queue kept two batches
+    deep; per-launch kernel times from libbf's CUDA events, clocks / power sampled by
+    nvidia-smi.  Reports the mean over the window and one batch timed after it."""
+    import statistics
+
+    import torch
+    import torch.distributed as dist
+
+    import benchkit
+    from paper_1810_11451_b200 import shard
+    if world > 1:
+        dist.barrier()
+    clk = benchkit.ClockSampler(local, period_ms=50).start() if rank == 0 else None
+    plan.set_profiling(True)
+    plan.kernel_time()
+    batch = max(1, int(0.15 / max(1e-4, bytes_launch / (hbm * 1e9))))   # ~150 ms per batch
+    ev = [torch.cuda.Event(), torch.cuda.Event()]
+    t0, nb, n_app = time.perf_counter(), 0, 0
+    while time.perf_counter() - t0 < args.steady_seconds:
+        for _ in range(batch):
+            plan.apply(S, tags, out=R)
+        n_app += batch
+        ev[nb % 2].record()
+        if nb >= 1:
+            ev[(nb - 1) % 2].synchronize()          # keep one batch queued behind this one
+        nb += 1
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    kms, kn = plan.kernel_time()
+    plan.set_profiling(False)
+    c = clk.stop() if clk else None
+    per = kms / max(kn, 1)                      # mean over the whole window
+    # one more batch, profiled on its own: the board is at its settled clock by now
+    plan.set_profiling(True)
+    plan.kernel_time()
+    for _ in range(batch):
+        plan.apply(S, tags, out=R)
+    torch.cuda.synchronize()
+    kms2, kn2 = plan.kernel_time()
+    plan.set_profiling(False)
+    late = kms2 / max(kn2, 1)
+    late = shard.max_over_ranks(late, dev)
+    per = shard.max_over_ranks(per, dev)
+    out = {"seconds": wall, "applies": n_app,
+           "kernel_ms_mean": per, "kernel_ms_settled": late,
+           "REs_per_s_mean": res_launch * world / (per * 1e-3),
+           "REs_per_s_settled": res_launch * world / (late * 1e-3),
+           "GBps_mean": bytes_launch / (per * 1e-3) / 1e9,
+           "GBps_settled": bytes_launch / (late * 1e-3) / 1e9,
+           "frac_settled": bytes_launch / (late * 1e-3) / 1e9 / hbm,
+           "how": f"{n_app} back-to-back steps over {wall:.1f} s (queue two {batch}-step batches "
+                  f"deep), then {batch} more timed alone at the settled clock; per-launch kernel "
+                  "time from libbf's CUDA events; nvidia-smi every 50 ms"}
+    if c:
+        out["clocks"] = c
+    return out
 
 
 def run_filter(args, wl, world, rank, local, dev):
@@ -567,6 +767,20 @@ def run_filter(args, wl, world, rank, local, dev):
     bytes_launch = wl.signal_bytes * n_loc
     achieved = bytes_launch / (kavg * 1e-3) / 1e9
     value = wl.n_signals * wl.n * args.steps / (elapsed * 1e-3)
+    # parity of the timed output: every 256th signal of the rank vs the fp64 oracle
+    # (per signal max_k |y - y_ref| <= 1e-5 ||s||_2 max|H|, reading F3)
+    import oracle
+    t0p = time.perf_counter()
+    lp = np.arange(0, n_loc, 256, dtype=np.int64)
+    ss = syn.filter_signals(wl.seed, 0, first + lp, wl.n, wl.M)
+    y_ref, bnd = oracle.filter_apply(ss, syn.filter_taps(wl.n), n_threads=oracle.max_threads())
+    got = y[torch.from_numpy(lp).to(dev)].cpu().numpy()
+    rel = np.abs(got.astype(np.complex128) - y_ref.astype(np.complex128)).max(axis=1) / bnd
+    parity = {"blocks": int(len(lp)), "unit": "signals", "worst_err_over_bound": float(rel.max()),
+              "ok": bool((rel <= TOL).all()), "tol": TOL, "check_s": time.perf_counter() - t0p,
+              "sample": "every 256th signal of each rank's output after the timed steps vs the "
+                        "fp64 O(n^2) DFT oracle"}
+    parity = reduce_parity({**parity, "worst_err_over_T": parity["worst_err_over_bound"]}, dev, world)
     # DRAM bytes per signal from the committed ncu capture, scaled to this launch
     traffic, tbasis = None, None
     try:
@@ -666,11 +880,15 @@ def run_filter(args, wl, world, rank, local, dev):
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "peak_basis": peak_basis(peaks)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "parity": parity,
         }
-        print(json.dumps(line), flush=True)
+        if parity["ok"]:
+            print(json.dumps(line), flush=True)
+        else:
+            refuse(line, parity)
     if world > 1:
         dist.destroy_process_group()
-    return 0
+    return 0 if parity["ok"] else 3
 
 
 def run_c5(args, wl, world, rank, local, dev):
@@ -709,7 +927,13 @@ def run_c5(args, wl, world, rank, local, dev):
         plans.append(pl)
     torch.cuda.synchronize()
     t_bc = time.perf_counter() - t_bc
-    _, nloc = shard.chunk_shard(0, chunk, rank, world)
+    # Whole windows of B consecutive chunks (one chunk of every cell at B = 8) are dealt
+    # round-robin to ranks (window w -> rank w mod world; shard.window_shard): every rank
+    # sees the same per-cell f mix and each launch keeps whole 4096-block chunks.
+    B = max(1, args.c5_batch)                # chunks per bf_apply_batch launch (window)
+    my_wins = shard.window_shard(n_chunks, B, rank, world)
+    my_chunks = [c for w in my_wins for c in w]
+    nloc = chunk
     # The apply kernels leave 2 SMs free so the routing of the next chunks (one CTA
     # each, on the route stream) never waits for an SM (bf_plan_set_sm_share).
     # tools/c5_exp.py measured the alternatives: one stream per cell with SM shares
@@ -730,18 +954,21 @@ def run_c5(args, wl, world, rank, local, dev):
     # in total) cannot stay resident: windows write a 4-slot ring.  Window w applies on
     # stream w % 2, so one window's tail overlaps the next one's head.
     NSLOT = 4
-    chunk_f = [int(fc[c % n_cells]) for c in range(n_chunks)]
-    s_off = np.concatenate([[0], np.cumsum([nloc * f * 60 for f in chunk_f])]).astype(np.int64)
-    S_all = torch.empty(int(s_off[-1]), dtype=torch.complex64, device=dev)
-    T_all = torch.empty((n_chunks, nloc), dtype=torch.int32, device=dev)
-    for c in range(n_chunks):
-        first, cnt = shard.chunk_shard(c, chunk, rank, world)
-        Sv = S_all[int(s_off[c]):int(s_off[c]) + cnt * chunk_f[c] * 60].view(cnt, chunk_f[c], 60)
-        sync.gen_symbols(Sv, wl.seed, 0, chunk_f[c], 60, 0, first=first)
-        sync.gen_tags(T_all[c, :cnt], wl.seed, wl.n_groups, first=first)
+    pos = {c: i for i, c in enumerate(my_chunks)}          # chunk id -> local slot in S_all
+    chunk_f = {c: int(fc[c % n_cells]) for c in my_chunks}
+    s_off = np.concatenate([[0], np.cumsum([nloc * chunk_f[c] * 60 for c in my_chunks])]).astype(np.int64)
+    S_all = torch.empty(max(1, int(s_off[-1])), dtype=torch.complex64, device=dev)
+    T_all = torch.empty((max(1, len(my_chunks)), nloc), dtype=torch.int32, device=dev)
+
+    def s_view(c):
+        o = int(s_off[pos[c]])
+        return S_all[o:o + nloc * chunk_f[c] * 60].view(nloc, chunk_f[c], 60)
+
+    for c in my_chunks:
+        sync.gen_symbols(s_view(c), wl.seed, 0, chunk_f[c], 60, 0, first=c * chunk)
+        sync.gen_tags(T_all[pos[c]], wl.seed, wl.n_groups, first=c * chunk)
     torch.cuda.synchronize()
-    B = max(1, args.c5_batch)                # chunks per bf_apply_batch launch (window)
-    n_win = (n_chunks + B - 1) // B
+    n_win = len(my_wins)
     P_ring = [[torch.empty(nloc, dtype=torch.int32, device=dev) for _ in range(B)] for _ in range(NSLOT)]
     O_ring = [[torch.empty(wl.n_groups + 2, dtype=torch.int32, device=dev) for _ in range(B)]
               for _ in range(NSLOT)]
@@ -763,19 +990,16 @@ def run_c5(args, wl, world, rank, local, dev):
         side.wait_event(ev_fork)
         for s_ in range(NSLOT):
             ev_use[s_].record(main)
-        for w in range(n_win):
+        for w, win in enumerate(my_wins):
             s = w % NSLOT
             ap = main if w % 2 == 0 else side
             jobs = []
             with torch.cuda.stream(rstream):
                 rstream.wait_event(ev_use[s])
-                for i, c in enumerate(range(w * B, min((w + 1) * B, n_chunks))):
-                    f = chunk_f[c]
-                    _, cnt = shard.chunk_shard(c, chunk, rank, world)
-                    Sv = S_all[int(s_off[c]):int(s_off[c]) + cnt * f * 60].view(cnt, f, 60)
-                    route_plan.route_into(T_all[c, :cnt], P_ring[s][i][:cnt], O_ring[s][i])
-                    jobs.append((plans[c % n_cells], Sv, P_ring[s][i][:cnt], O_ring[s][i],
-                                 R_ring[s][i][:cnt]))
+                for i, c in enumerate(win):
+                    route_plan.route_into(T_all[pos[c]], P_ring[s][i], O_ring[s][i])
+                    jobs.append((plans[c % n_cells], s_view(c), P_ring[s][i], O_ring[s][i],
+                                 R_ring[s][i]))
                 ev_rt[s].record(rstream)
             ap.wait_event(ev_rt[s])
             if B == 1:
@@ -845,6 +1069,26 @@ def run_c5(args, wl, world, rank, local, dev):
     kern_ms = shard.max_over_ranks(kern_ms, dev)
     launches = int(shard.sum_over_ranks(launches, dev))
     clk = clocks.stop() if clocks else None
+    # ---- parity: the ring still holds the R of this rank's last NSLOT windows of the last
+    #      step; every 8th block of each of those chunks against the oracle
+    def c5_inputs(cell, f):
+        def gen(gid):
+            W = syn.precoders(wl.seed, cell, wl.n_groups, 64, f, "none")
+            S = syn.qam_symbols(wl.seed, 0, gid, f, 60, syn.block_modulations(wl.seed, gid))
+            return W, S, syn.subband_tags(wl.seed, gid, wl.n_groups)
+        return gen
+    parts = []
+    for w in range(max(0, n_win - NSLOT), n_win):
+        for i, c in enumerate(my_wins[w]):
+            lp = np.arange(0, nloc, 8, dtype=np.int64)
+            parts.append(parity_of_blocks(wl, R_ring[w % NSLOT][i], lp, c * chunk + lp, "interleaved",
+                                          inputs=c5_inputs(c % n_cells, chunk_f[c])))
+    parity = {"blocks": sum(p_["blocks"] for p_ in parts), "ok": all(p_["ok"] for p_ in parts),
+              "worst_err_over_T": max([p_["worst_err_over_T"] for p_ in parts] or [0.0]),
+              "tol": TOL, "check_s": sum(p_["check_s"] for p_ in parts),
+              "sample": f"every 8th block of the chunks of each rank's last {NSLOT} windows "
+                        "(the R ring after the timed steps) vs the fp64 oracle"}
+    parity = reduce_parity(parity, dev, world)
     total_blocks = n_chunks * chunk
     blocks_by_f = [(int(fc[c % n_cells]), chunk) for c in range(n_chunks)]
     bytes_all = sum(480 * (f + 64) * nb for f, nb in blocks_by_f) * args.steps
@@ -877,7 +1121,8 @@ def run_c5(args, wl, world, rank, local, dev):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "c5", "desc": wl.desc, "chunks_per_step": n_chunks,
                        "blocks_per_step": total_blocks, "cells_f": [int(x) for x in fc],
-                       "parallelism": f"dp{world} (every chunk split evenly across ranks)",
+                       "parallelism": f"dp{world} (whole {B}-chunk windows dealt round-robin to ranks)",
+                       "world_size": world, "backend": dist.get_backend() if world > 1 else None,
                        "l2": "S resident (74.5 GB at N=1, >> L2); R streamed through a 4-slot ring",
                        "gpu": torch.cuda.get_device_name(dev), "w_broadcast_ms": t_bc * 1e3,
                        "launch_mode": mode, "apply_streams": 2, "ring_slots": NSLOT,
@@ -885,12 +1130,15 @@ def run_c5(args, wl, world, rank, local, dev):
                        "apply_sms": sms - route_sms, "route_sms": route_sms,
                        },
             "flops_per_s": flops_all / (elapsed_ms * 1e-3), "roofline": roof, "cpu_baseline": None,
-            "e2e": None, "gpu_launches": launches, "clocks": clk,
+            "e2e": None, "gpu_launches": launches, "clocks": clk, "parity": parity,
         }
-        print(json.dumps(line), flush=True)
+        if parity["ok"]:
+            print(json.dumps(line), flush=True)
+        else:
+            refuse(line, parity)
     if world > 1:
         dist.destroy_process_group()
-    return 0
+    return 0 if parity["ok"] else 3
 
 
 def main():

@@ -204,6 +204,36 @@ def qam_symbols(seed: int, sub: int, block_ids, f: int, b: int, M,
     return out
 
 
+KIND_GS = 7       # Gaussian S (accuracy tests: continuous values instead of QAM levels)
+
+
+def gaussian_symbols(seed: int, sub: int, block_ids, f: int, b: int,
+                     exp_spread: int = 0) -> np.ndarray:
+    """complex64 S blocks [n][f][b] of fp32 CN(0,1) draws (Box-Muller in fp64, one rounding),
+    for accuracy tests whose inputs must exercise every significand bit (QAM levels exercise
+    only a handful).  exp_spread > 0 multiplies each element by 2^u, u uniform in
+    [-exp_spread, exp_spread] (wide dynamic range inside a block)."""
+    block_ids = np.asarray(block_ids, dtype=np.int64).reshape(-1)
+    if f > S_STRIDE_K or b > S_STRIDE_J:
+        raise ValueError("f <= 64 and b <= 256 in the S index space")
+    n = block_ids.astype(np.uint64).reshape(-1, 1, 1)
+    k = np.arange(f, dtype=np.uint64).reshape(1, -1, 1)
+    j = np.arange(b, dtype=np.uint64).reshape(1, 1, -1)
+    e = (n * np.uint64(S_STRIDE_K) + k) * np.uint64(S_STRIDE_J) + j
+    key = stream_key(seed, KIND_GS, sub)
+    h1 = counter_hash(key, e * np.uint64(3))
+    h2 = counter_hash(key, e * np.uint64(3) + np.uint64(1))
+    u1 = ((h1 >> np.uint64(11)).astype(np.float64) + 1.0) * (2.0 ** -53)   # (0, 1]
+    u2 = _unit53(h2)
+    r = np.sqrt(-np.log(u1))
+    z = r * np.cos(2.0 * np.pi * u2) + 1j * (r * np.sin(2.0 * np.pi * u2))
+    if exp_spread > 0:
+        h3 = counter_hash(key, e * np.uint64(3) + np.uint64(2))
+        u = _bounded(h3, 2 * exp_spread + 1) - exp_spread
+        z = z * np.ldexp(1.0, u)
+    return z.astype(np.complex64)
+
+
 def subband_tags(seed: int, block_ids, n_groups: int) -> np.ndarray:
     """int32 tag in [0, n_groups) per block, uniform (configs c4, c5)."""
     h = counter_hash(stream_key(seed, KIND_TAG, 0), np.asarray(block_ids, dtype=np.uint64))

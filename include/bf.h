@@ -13,7 +13,10 @@
  *   accumulated in fp32 from +0.0f (by CUDA-core FFMAs or by error-compensated
  *   tensor-core MMAs, see bf_variant).  Accuracy contract (BASELINE.json
  *   north_star item 4): |R - R_exact| <= 1e-5 * sum_k |W[g][i][k]| |S[n][k][j]|
- *   per element; bit-exact for f = 0 (+0.0) and for identity / selection W.
+ *   per element (complex modulus; DESIGN.md §7 proves it for both kernels, given
+ *   finite inputs whose nonzero products |w||s| are normal fp32 numbers, i.e. no
+ *   underflow); bit-exact for f = 0 (+0.0) and for identity / selection W.
+ *   Non-finite inputs propagate per IEEE to the elements that use them.
  *
  * The calls follow the paper's statement: W is set once (bf_set_precoders),
  * then many S blocks are multiplied by it (bf_apply).  Multiple precoder
@@ -93,13 +96,18 @@ typedef enum {
 /* Kernel variant.  Both compute the same product within the same contract.
  *   BF_VARIANT_FFMA    CUDA-core kernel: 4 fp32 FFMA per complex MAC.
  *   BF_VARIANT_TENSOR  tcgen05 tensor-core kernel: S split exactly into 3 terms
- *                      of 11-bit significands, W into 2; S1 W1 in kind::tf32 and
- *                      the corrections S2 W1 + S1 W2 in one kind::f16 (bf16) MMA
- *                      group (S2 W1 + S3 W1 + S1 W1 in tf32 when W is exactly
- *                      tf32), fp32 accumulation in TMEM (error-compensated split
- *                      precision, BASELINE.json north_star item 2).
+ *                      of 11-bit significands, W into 2 (+ a 2^-22 residual);
+ *                      S2 W1 + S1 W2 + S1 W1 as kind::tf32 MMAs (S2 W1 + S3 W1 +
+ *                      S1 W1 when W is exactly tf32), every product exact, fp32
+ *                      accumulation in TMEM (error-compensated split precision,
+ *                      BASELINE.json north_star item 2).  Tensor domain: nonzero
+ *                      |s|, |w| in [2^-40, 2^40); blocks with an S value outside
+ *                      it (or NaN / Inf) and blocks of groups with a W entry
+ *                      outside it are recomputed inside the same launch with the
+ *                      FFMA kernel's arithmetic (bitwise equal to BF_VARIANT_FFMA).
  *   BF_VARIANT_AUTO    per-(f, layout) choice from the measured variant table
- *                      (default): FFMA at small f, tensor above. */
+ *                      (default): FFMA at small f, tensor above; FFMA whenever a
+ *                      precoder entry lies outside the tensor domain. */
 typedef enum {
     BF_VARIANT_AUTO = 0,
     BF_VARIANT_FFMA = 1,
@@ -126,8 +134,10 @@ bf_status bf_plan_create(int n_ant, int f, int b, int layout, bf_plan_t *out);
 
 /* Copy n_groups precoders from device memory W_dev (layout as above, 16-byte
  * aligned) into the plan, re-laid out for the kernel, ordered on `stream`.
- * After the stream reaches this point the caller may free W_dev.  With f == 0
- * W_dev may be NULL.  Replaces any previous precoders. */
+ * With f == 0 W_dev may be NULL.  Replaces any previous precoders.  For f > 0
+ * this call synchronises `stream` once before returning (it reads back the
+ * per-group tensor-domain flags that BF_VARIANT_AUTO's choice depends on), so
+ * the caller may free W_dev when it returns; not for use inside stream capture. */
 bf_status bf_set_precoders(bf_plan_t p, const void *W_dev, int n_groups, void *stream);
 
 /* R_dev = W[group_idx[n]] x S_dev[n] for n in [0, n_blocks), on `stream`.

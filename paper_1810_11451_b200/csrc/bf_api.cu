@@ -98,14 +98,14 @@ __global__ void bf_relayout_w(const float *__restrict__ W, int n_groups, int F, 
 }
 
 // Builds the pre-split B image of one or more groups (bf_set_precoders):
-// img[g][t][kc][ng][r][e] = term t of B'[n = 8 ng + r][kk = 4 kc + e].
+// img[g][t][kc][ng][r][e] = term t of B'[n = 8 ng + r][kk = 4 kc + e], t = 0: W1, 1: W2.
 __global__ void bf_tc_build_wimg(const float *__restrict__ W, int n_groups, int F, int layout,
                                  float *__restrict__ img) {
     // Per group: [W1 tf32 core matrices: KP/4 K-chunks x 16 row groups x 8 rows x 4]
-    //            [bf16 correction image: K'' = 2 KP as KP/4 chunks of 8 bf16, rows n;
-    //             K'' < KP -> bf16(W1[n][K'']), K'' >= KP -> bf16(W2[n][K'' - KP])]
-    // with B'[n][kk] the real embedding (n = 2i + c_out, kk = 2k + c_in) and
-    // W1 = tf32(B'), W2 = tf32(B' - W1).
+    //            [W2, the same layout]
+    // with B'[n][kk] the real embedding (n = 2i + c_out, kk = 2k + c_in),
+    // W1 = tf32(B'), W2 = tf32(B' - W1) (both round to nearest; B' = W1 + W2 + W3 with
+    // |W3| <= 2^-22 |B'|).
     const int KP = bftc::kp_of(F);
     const int64_t half = (int64_t)KP * 128;            // 32-bit words per part
     const int64_t per_group = 2 * half;
@@ -114,9 +114,14 @@ __global__ void bf_tc_build_wimg(const float *__restrict__ W, int n_groups, int 
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t g = idx / per_group;
         const int rem = (int)(idx - g * per_group);
-        auto bprime = [&](int n, int kk) -> float {
-            const int i = n >> 1, cout = n & 1, k = kk >> 1, cin = kk & 1;
-            if (k >= F) return 0.0f;
+        const int part = rem < half ? 0 : 1;
+        const int w = rem - part * (int)half;
+        const int kc = w / 512, r2 = w % 512;
+        const int ng = r2 / 32, r = (r2 / 4) % 8, e = r2 % 4;
+        const int n = ng * 8 + r, kk = kc * 4 + e;
+        const int i = n >> 1, cout = n & 1, k = kk >> 1, cin = kk & 1;
+        float v = 0.0f;
+        if (k < F) {
             float wr, wi;
             if (layout != BF_LAYOUT_PLANAR) {
                 wr = W[((g * 64 + i) * F + k) * 2];
@@ -126,43 +131,46 @@ __global__ void bf_tc_build_wimg(const float *__restrict__ W, int n_groups, int 
                 wi = W[(g * 2 + 1) * 64 * F + i * F + k];
             }
             // B'[2i][2k] = wr, B'[2i][2k+1] = -wi, B'[2i+1][2k] = wi, B'[2i+1][2k+1] = wr
-            return cout == 0 ? (cin == 0 ? wr : -wi) : (cin == 0 ? wi : wr);
-        };
-        if (rem < half) {                               // W1, tf32
-            const int kc = rem / 512, r2 = rem % 512;
-            const int ng = r2 / 32, r = (r2 / 4) % 8, e = r2 % 4;
-            img[idx] = tc::to_tf32(bprime(ng * 8 + r, kc * 4 + e));
-        } else {                                        // bf16 pair (K'' = 2 e2, 2 e2 + 1)
-            const int w = rem - (int)half;
-            const int kc = w / 512, r2 = w % 512;
-            const int ng = r2 / 32, r = (r2 / 4) % 8, e2 = r2 % 4;
-            const int n = ng * 8 + r;
-            float pair[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int kk2 = kc * 8 + 2 * e2 + h;
-                const int kk = kk2 < KP ? kk2 : kk2 - KP;
-                const float v = bprime(n, kk);
-                const float w1 = tc::to_tf32(v);
-                pair[h] = kk2 < KP ? w1 : tc::to_tf32(v - w1);
-            }
-            const __nv_bfloat162 b2 = __floats2bfloat162_rn(pair[0], pair[1]);   // .x low
-            img[idx] = __uint_as_float(*reinterpret_cast<const uint32_t *>(&b2));
+            v = cout == 0 ? (cin == 0 ? wr : -wi) : (cin == 0 ? wi : wr);
         }
+        const float w1 = tc::to_tf32(v);
+        img[idx] = part == 0 ? w1 : tc::to_tf32(v - w1);
     }
 }
 
-// wexact[g] = 1 when group g's W is exactly representable in tf32: the W2 part of
-// its bf16 correction image (the last quarter of the group image) is all zero.  The
-// tensor kernel then multiplies S3 in tf32 instead of running the bf16 corrections.
-__global__ void bf_tc_wexact(const float *__restrict__ img, int KP, int32_t *__restrict__ wexact) {
+// Per-group flags (one CTA per group): bit 0 = W exactly tf32 (its W2 image is all zero:
+// the tensor kernel then multiplies S3 instead of W2 and copy-like W is bit-exact);
+// bit 1 = some entry outside the tensor domain (nonzero |w| < 2^-40, |w| >= 2^40, NaN,
+// Inf): those groups' blocks are recomputed by the kernel's fix-up.
+__global__ void bf_tc_wflags(const float *__restrict__ W, const float *__restrict__ img, int F,
+                             int KP, int32_t *__restrict__ wflags) {
     const int64_t per_group = 2LL * KP * 128;
-    const float *w2 = img + blockIdx.x * per_group + per_group / 2 + per_group / 4;
-    int nz = 0;
-    for (int i = threadIdx.x; i < KP * 128 / 2; i += blockDim.x)
-        nz |= (__float_as_uint(w2[i]) & 0x7FFF7FFFu) != 0u;
+    const float *w2 = img + blockIdx.x * per_group + per_group / 2;
+    int nz = 0, bad = 0;
+    for (int i = threadIdx.x; i < KP * 128; i += blockDim.x)
+        nz |= (__float_as_uint(w2[i]) & 0x7FFFFFFFu) != 0u;
+    const uint32_t *wg = reinterpret_cast<const uint32_t *>(W) + (int64_t)blockIdx.x * 128 * F;
+    for (int i = threadIdx.x; i < 128 * F; i += blockDim.x) {   // the group's 64 x F complex
+        const uint32_t u = wg[i] & 0x7FFFFFFFu;
+        bad |= !(u == 0u || (u >= bftc::kDomLo && u < bftc::kDomHi));
+    }
     nz = __syncthreads_or(nz);
-    if (threadIdx.x == 0) wexact[blockIdx.x] = nz ? 0 : 1;
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x == 0) wflags[blockIdx.x] = (nz ? 0 : 1) | (bad ? 2 : 0);
+}
+
+// a8 with tags (f = 0): +0.0 for every block whose tag is in [0, G); blocks with other
+// tags are left unwritten, as bf.h states, and flagged for BF_CHECK=1.
+__global__ void bf_zero_tagged(const int32_t *__restrict__ gidx, int64_t n, int G,
+                               int vec_per_block, uint4 *__restrict__ R, int32_t *__restrict__ err) {
+    const int64_t total = n * vec_per_block;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t blk = idx / vec_per_block;
+        const int32_t g = __ldg(gidx + blk);
+        if ((unsigned)g < (unsigned)G) R[idx] = make_uint4(0u, 0u, 0u, 0u);
+        else if (idx == blk * vec_per_block) atomicOr(err, 1);
+    }
 }
 
 __device__ __forceinline__ int route_bin(int32_t g, int G) {
@@ -421,8 +429,9 @@ struct bf_plan_s {
     int64_t Wp_cap = 0;
     float *Wimg = nullptr;      // tensor-core (pre-split B) precoder image
     int64_t Wimg_cap = 0;
-    int32_t *wexact = nullptr;  // per group: W exactly tf32
+    int32_t *wexact = nullptr;  // per group: bit 0 W exactly tf32, bit 1 outside the tensor domain
     int64_t wexact_cap = 0;
+    bool w_in_domain = true;    // every group inside the tensor domain (AUTO may pick tensor)
     // routing workspace
     int32_t *perm = nullptr, *table = nullptr, *offsets = nullptr, *err = nullptr;
     int64_t perm_cap = 0, table_cap = 0, offsets_cap = 0, err_cap = 0;
@@ -497,10 +506,13 @@ bf_status check_tags_if_requested(bf_plan_t p, cudaStream_t st) {
 }
 
 // Per-f variant table: which kernel BF_VARIANT_AUTO runs.
+// Precoders outside the tensor domain send AUTO to the FFMA kernel; an
+// explicit BF_VARIANT_TENSOR still runs the tensor kernel, whose fix-up then recomputes
+// those groups' blocks with FFMA arithmetic.
 bool use_tensor(bf_plan_t p) {
     if (p->variant == BF_VARIANT_TENSOR) return true;
     if (p->variant == BF_VARIANT_FFMA) return false;
-    return p->f >= kAutoTensorMinF[p->layout];
+    return p->w_in_domain && p->f >= kAutoTensorMinF[p->layout];
 }
 
 int sms_used(bf_plan_t p) {
@@ -534,6 +546,7 @@ bftc::TcJob tc_job(bf_plan_t p, const void *S, const int32_t *perm, const int32_
                    void *R, int64_t n) {
     bftc::TcJob j{};
     j.Wimg = p->Wimg;
+    j.Wp = p->Wp;
     j.S = static_cast<const float *>(S);
     j.perm = perm;
     j.offsets = offsets;
@@ -617,6 +630,18 @@ bf_status launch_batch(const bf_batch_job *jobs, int n, cudaStream_t st) {
 bf_status apply_device(bf_plan_t p, const void *S, const int32_t *gidx, void *R, int64_t n,
                        cudaStream_t st) {
     if (n == 0) return BF_OK;
+    if (p->f == 0 && gidx) {   // a8 with tags: zero the validly tagged blocks only
+        bf_status s;
+        if ((s = grow(&p->err, &p->err_cap, 1, "routing flag")) != BF_OK) return s;
+        BF_CUDA(cudaMemsetAsync(p->err, 0, sizeof(int32_t), st));
+        const int vpb = bfk::r_block_bytes(p->layout) / 16;
+        const int64_t total = n * vpb;
+        const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)p->num_sms * 8);
+        bf_zero_tagged<<<blocks, 256, 0, st>>>(gidx, n, p->n_groups, vpb, static_cast<uint4 *>(R),
+                                                p->err);
+        if ((s = launched(p, "bf_zero_tagged launch")) != BF_OK) return s;
+        return check_tags_if_requested(p, st);
+    }
     // tagged blocks are always routed — also with one group, so that tags outside
     // [0, n_groups) leave their blocks unwritten as bf.h states (a caller with one W
     // and no tags passes group_idx = NULL and skips the routing)
@@ -748,6 +773,7 @@ bf_status bf_plan_create(int n_ant, int f, int b, int layout, bf_plan_t *out) {
 }
 
 bf_status bf_set_precoders(bf_plan_t p, const void *W_dev, int n_groups, void *stream) {
+    bfh::NvtxRange nvtx_("bf_set_precoders");
     if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
     if (n_groups < 1) return fail(BF_ERR_INVALID_VALUE, "n_groups must be >= 1");
     if (n_groups > kMaxGroups)
@@ -770,8 +796,16 @@ bf_status bf_set_precoders(bf_plan_t p, const void *W_dev, int n_groups, void *s
             static_cast<const float *>(W_dev), n_groups, p->f, p->layout, p->Wimg);
         if ((s = launched(p, "bf_tc_build_wimg launch")) != BF_OK) return s;
         if ((s = grow(&p->wexact, &p->wexact_cap, n_groups, "precoder flags")) != BF_OK) return s;
-        bf_tc_wexact<<<n_groups, 256, 0, st>>>(p->Wimg, bftc::kp_of(p->f), p->wexact);
-        if ((s = launched(p, "bf_tc_wexact launch")) != BF_OK) return s;
+        bf_tc_wflags<<<n_groups, 256, 0, st>>>(static_cast<const float *>(W_dev), p->Wimg, p->f,
+                                              bftc::kp_of(p->f), p->wexact);
+        if ((s = launched(p, "bf_tc_wflags launch")) != BF_OK) return s;
+        // the one synchronisation of the call: AUTO's kernel choice depends on whether
+        // every group lies inside the tensor domain
+        std::vector<int32_t> flags(n_groups);
+        BF_CUDA(cudaMemcpyAsync(flags.data(), p->wexact, n_groups * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, st));
+        BF_CUDA(cudaStreamSynchronize(st));
+        p->w_in_domain = std::none_of(flags.begin(), flags.end(), [](int32_t v) { return (v & 2) != 0; });
     }
     p->n_groups = n_groups;
     return BF_OK;
@@ -804,6 +838,7 @@ static bf_status validate_apply(bf_plan_t p, const void *S, const int32_t *gidx,
 
 bf_status bf_apply(bf_plan_t p, const void *S_dev, const int32_t *group_idx_dev, void *R_dev,
                    int64_t n_blocks, void *stream) {
+    bfh::NvtxRange nvtx_("bf_apply");
     bf_status s = validate_apply(p, S_dev, group_idx_dev, R_dev, n_blocks, true);
     if (s != BF_OK || n_blocks == 0) return s;
     DeviceGuard guard(p->device);
@@ -813,6 +848,7 @@ bf_status bf_apply(bf_plan_t p, const void *S_dev, const int32_t *group_idx_dev,
 
 bf_status bf_route(bf_plan_t p, const int32_t *group_idx_dev, int64_t n_blocks, int32_t *perm_dev,
                    int32_t *offsets_dev, void *stream) {
+    bfh::NvtxRange nvtx_("bf_route");
     if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
     if (p->n_groups < 1) return fail(BF_ERR_NO_PRECODERS, "bf_set_precoders was not called");
     if (n_blocks < 0 || n_blocks >= (int64_t(1) << 31))
@@ -830,6 +866,7 @@ bf_status bf_route(bf_plan_t p, const int32_t *group_idx_dev, int64_t n_blocks, 
 
 bf_status bf_apply_routed(bf_plan_t p, const void *S_dev, const int32_t *perm_dev,
                           const int32_t *offsets_dev, void *R_dev, int64_t n_blocks, void *stream) {
+    bfh::NvtxRange nvtx_("bf_apply_routed");
     bf_status s = validate_apply(p, S_dev, perm_dev, R_dev, n_blocks, true);
     if (s != BF_OK || n_blocks == 0) return s;
     if ((perm_dev == nullptr) != (offsets_dev == nullptr))
@@ -841,6 +878,7 @@ bf_status bf_apply_routed(bf_plan_t p, const void *S_dev, const int32_t *perm_de
 }
 
 bf_status bf_apply_batch(const bf_batch_job *jobs, int n_jobs, void *stream) {
+    bfh::NvtxRange nvtx_("bf_apply_batch");
     if (n_jobs < 0 || (n_jobs > 0 && !jobs)) return fail(BF_ERR_INVALID_VALUE, "bad job list");
     if (n_jobs == 0) return BF_OK;
     const bf_plan_t p0 = jobs[0].plan;
@@ -873,10 +911,12 @@ bf_status bf_apply_batch(const bf_batch_job *jobs, int n_jobs, void *stream) {
     for (int i = 0; i <= n_jobs; ++i) {
         const bool end = i == n_jobs;
         const bf_batch_job *jb = end ? nullptr : &jobs[i];
-        // AUTO plans always join the pack (one launch for the window beats the small-f
-        // per-kernel edge of the FFMA kernel); plans set to FFMA run on their own
+        // AUTO plans join the pack (one launch for the window beats the small-f
+        // per-kernel edge of the FFMA kernel) unless their precoders lie outside the
+        // tensor domain; plans set to FFMA run on their own
         const bool tc = !end && jb->n_blocks > 0 && jb->plan->f > 0 &&
-                        jb->plan->variant != BF_VARIANT_FFMA;
+                        jb->plan->variant != BF_VARIANT_FFMA &&
+                        (jb->plan->variant == BF_VARIANT_TENSOR || jb->plan->w_in_domain);
         const int need = tc && jb->offsets_dev ? jb->plan->n_groups + 2 : 0;
         if (np > 0 && (end || !tc || np == bftc::kMaxJobs || slots + need > bftc::kOffsSlots)) {
             if ((s = launch_batch(pack, np, st)) != BF_OK) return s;
@@ -898,6 +938,7 @@ bf_status bf_apply_batch(const bf_batch_job *jobs, int n_jobs, void *stream) {
 
 bf_status bf_apply_host(bf_plan_t p, const void *S_host, const int32_t *group_idx_host,
                         void *R_host, int64_t n_blocks, void *stream) {
+    bfh::NvtxRange nvtx_("bf_apply_host");
     bf_status s = validate_apply(p, S_host, group_idx_host, R_host, n_blocks, false);
     if (s != BF_OK || n_blocks == 0) return s;
     DeviceGuard guard(p->device);

@@ -127,6 +127,7 @@ bf_status bff_plan_create(int n, bff_plan_t *out) {
 }
 
 bf_status bff_set_taps(bff_plan_t p, const void *h_dev, void *stream) {
+    bfh::NvtxRange nvtx_("bff_set_taps");
     if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
     if (!h_dev) return fail(BF_ERR_INVALID_VALUE, "h_dev is NULL");
     if (!aligned16(h_dev)) return fail(BF_ERR_MISALIGNED, "h_dev must be 16-byte aligned");
@@ -139,6 +140,7 @@ bf_status bff_set_taps(bff_plan_t p, const void *h_dev, void *stream) {
 }
 
 bf_status bff_apply(bff_plan_t p, const void *s_dev, void *y_dev, int64_t n_signals, void *stream) {
+    bfh::NvtxRange nvtx_("bff_apply");
     bf_status s = check_io(p, s_dev, y_dev, n_signals);
     if (s != BF_OK || n_signals == 0) return s;
     if (!p->have_taps) return fail(BF_ERR_NO_PRECODERS, "bff_set_taps was not called");
@@ -148,6 +150,7 @@ bf_status bff_apply(bff_plan_t p, const void *s_dev, void *y_dev, int64_t n_sign
 }
 
 bf_status bff_fft(bff_plan_t p, const void *x_dev, void *X_dev, int64_t n_signals, void *stream) {
+    bfh::NvtxRange nvtx_("bff_fft");
     bf_status s = check_io(p, x_dev, X_dev, n_signals);
     if (s != BF_OK || n_signals == 0) return s;
     DeviceGuard g(p->device);

@@ -3,6 +3,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: no-ops unless a profiler attaches
+
 #include <cstdarg>
 #include <cstdio>
 #include <string>
@@ -37,6 +39,26 @@ struct DeviceGuard {
     ~DeviceGuard() {
         if (changed) cudaSetDevice(prev);
     }
+};
+
+// NVTX range around one ABI call ("libbf" domain) so that nsys / ncu timelines show the
+// host calls (route, apply, batch, host pipeline) above the kernels they enqueue.
+struct NvtxRange {
+    static nvtxDomainHandle_t domain() {
+        static nvtxDomainHandle_t d = nvtxDomainCreateA("libbf");
+        return d;
+    }
+    explicit NvtxRange(const char *name) {
+        nvtxEventAttributes_t a{};
+        a.version = NVTX_VERSION;
+        a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+        a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+        a.message.ascii = name;
+        nvtxDomainRangePushEx(domain(), &a);
+    }
+    ~NvtxRange() { nvtxDomainRangePop(domain()); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
 };
 
 }  // namespace bfh

@@ -13,13 +13,18 @@
 //   D [m][n]   (TMEM)  = R[blk][i][j] re / im, fp32 accumulate.
 // Split precision (error-compensated, BASELINE.json north_star item 2):
 // S = S1 + S2 + S3 exactly (three tf32 terms, each rounded to 11 bits),
-// W' = W1 + W2 (+ 2^-22 residual, split once per W).  General W: the corrections
-// S2 W1 + S1 W2 as one bf16 MMA group over K'' = 2 KP, then S1 W1 in tf32; when the
-// group's W is exactly tf32 (W2 == 0: identity, selection, small integers) S2 W1 +
-// S3 W1 + S1 W1 in tf32, which makes copy-like precoders bit-exact.  The split of
-// tile t+1 rewrites each term region as soon as tile t's MMAs on it completed.
-// Dropped terms are <= ~2^-21 T; with the tensor accumulation the error stays
-// near 2e-6 T at f = 36, inside the 1e-5 T contract.
+// W' = W1 + W2 + W3 (W1, W2 tf32, |W3| <= 2^-22 |W'|, split once per W).  Every
+// product is a tf32 x tf32 product, exact in the fp32 accumulator.  General W:
+// S2 W1, S1 W2, then S1 W1 (dropped terms S3 W1 + S2 W2 + S W3 <= 3 2^-22 |s||w|);
+// when the group's W is exactly tf32 (W2 == 0: identity, selection, small integers)
+// S2 W1, S3 W1, S1 W1 = S W exactly, which makes copy-like precoders bit-exact.
+// The split of tile t+1 rewrites each term region as soon as tile t's MMAs on it
+// completed.  DESIGN.md §7 bounds the error by ~4.1e-6 T at f = 36 (complex modulus,
+// with the accumulation model measured by tools/tc_acc_probe).
+// Tensor domain: the bound needs every product term normal, so the kernel checks every
+// S value it splits (nonzero |s| in [2^-40, 2^40)) and bf_set_precoders every W entry;
+// blocks outside (incl. NaN / Inf) are recomputed at the end of the launch by the CTA
+// that owns them with the FFMA kernel's arithmetic (fix_block), bit for bit.
 //
 // One CTA (18 warps) per SM, persistent over a cost-balanced range of the
 // group-sorted block list (cta_range); tiles are 2 consecutive blocks of one group.
@@ -64,6 +69,12 @@ constexpr int kMaxStages = BFTC_MAX_STAGES;   // S ring depth (tiles), shared me
 constexpr int kSmemLimit = 232448;     // 227 KB per CTA
 constexpr int kDCol0 = 256;
 constexpr int kMinSmem = 120 * 1024;   // forces one CTA (and one TMEM owner) per SM
+#ifndef BFTC_EARLY_RELEASE
+#define BFTC_EARLY_RELEASE 0
+#endif
+// split warps release an S ring slot as soon as their values are in registers (1), or
+// after the tile's last split pass (0)
+constexpr bool kEarlyRelease = BFTC_EARLY_RELEASE != 0;
 
 __host__ __device__ constexpr int kp_of(int F) { return (2 * F + 7) / 8 * 8; }
 
@@ -74,15 +85,21 @@ __host__ __device__ constexpr int kp_of(int F) { return (2 * F + 7) / 8 * 8; }
 // for the batch kernel whose jobs carry their own f (1..36).
 constexpr int kMaxJobs = 16;
 constexpr int kOffsSlots = 1028;       // shared group-offset slots: sum over jobs of (n_groups + 2)
+constexpr int kFixCap = 64;            // out-of-domain blocks a CTA lists (more: rescan its range)
+// Tensor domain of S and W: zero, or 2^-40 <= |x| < 2^40, as fp32 bit
+// patterns without the sign.  Inside it every product of split terms is a normal fp32
+// number, so the split-precision error bound holds; NaN and Inf fall outside.
+constexpr uint32_t kDomLo = 0x2B800000u, kDomHi = 0x53800000u;
 
 struct TcJob {
     const float *Wimg;        // [n_groups][2][KP/4][16][8][4] floats (pre-split B image)
-    // Wimg per group: [W1 as tf32 core matrices (KP/4 K-chunks)] then
-    // [C = (W1 ; W2) as bf16 core matrices (2 KP bf16 of K = KP/4 chunks of 16 B)]
+    // Wimg per group: [W1 as tf32 core matrices (KP/4 K-chunks)] then [W2, same layout]
+    const float4 *Wp;         // FFMA image of the same precoders (out-of-domain fix-up)
     const float *S;
     const int32_t *perm;      // NULL = identity order
     const int32_t *offsets;   // [n_groups + 2] group starts of the sorted order, or NULL
-    const int32_t *wexact;    // [n_groups] 1 if the group's W is exactly tf32 (W2 == 0)
+    const int32_t *wexact;    // [n_groups] bit 0: W exactly tf32 (W2 == 0);
+                              //            bit 1: some |w| outside the tensor domain
     float *R;
     int64_t n_items;
     int n_groups;
@@ -109,10 +126,11 @@ template <int F>
 struct TcSmem {
     static constexpr int FS = F > 0 ? F : 36;          // sizing flow count (36 for runtime f)
     static constexpr int KP = kp_of(FS);
-    static constexpr int kWBytes = 2 * KP * 128 * 4;   // W1 tf32 image + bf16 correction image
+    static constexpr int kWBytes = 2 * KP * 128 * 4;   // W1 and W2 tf32 images
     static constexpr int kSBlock = 480 * FS;           // one block of S (slot stride)
     static constexpr int kJobBytes = kMaxJobs * 96;    // per-job context (JobCtx)
-    static constexpr int kMisc = 24 * 8 + 16 + kOffsSlots * 4 + kJobBytes;
+    static constexpr int kFixBytes = kFixCap * 8 + 16 + 2 * kMaxStages * 4;   // fix-up list
+    static constexpr int kMisc = 24 * 8 + 16 + kOffsSlots * 4 + kJobBytes + kFixBytes;
     // R staging: the epilogue writes the tile's two blocks of R into shared memory in
     // their global layout and one thread stores each block with a bulk copy (full lines,
     // no partial sectors at planar row boundaries).  Shared memory, in order of
@@ -141,8 +159,9 @@ struct TcSmem {
     static constexpr int kOffTmem = kOffBar + 24 * 8;
     static constexpr int kOffJobs = kOffTmem + 16;     // JobCtx[kMaxJobs]
     static constexpr int kOffOffs = kOffJobs + kJobBytes;   // group offsets of every job
-    static constexpr int kOffR = (kOffOffs + kOffsSlots * 4 + 127) / 128 * 128;
-    static constexpr int kBytesUsed = kStageR ? kOffR + kRStageBytes : kOffOffs + kOffsSlots * 4;
+    static constexpr int kOffFix = kOffOffs + kOffsSlots * 4;   // int2 list, n, overflow, last[]
+    static constexpr int kOffR = (kOffFix + kFixBytes + 127) / 128 * 128;
+    static constexpr int kBytesUsed = kStageR ? kOffR + kRStageBytes : kOffFix + kFixBytes;
     static constexpr int kBytes = kBytesUsed > kMinSmem ? kBytesUsed : kMinSmem;
     static_assert(kBytesUsed <= kSmemLimit, "shared memory");
 };
@@ -150,6 +169,7 @@ struct TcSmem {
 // A job as the roles see it (shared memory), with this CTA's share of it.
 struct JobCtx {
     const float *Wimg, *S;
+    const float4 *Wp;
     const int32_t *perm, *wexact;
     float *R;
     const int32_t *offs;      // shared copy of the job's offsets, or nullptr (untagged)
@@ -218,6 +238,64 @@ struct TileIter {
         return false;
     }
 };
+
+// Out-of-domain fix-up: the whole CTA recomputes block `item` of job J (group g) from
+// global memory with the FFMA kernel's per-element arithmetic (k ascending; re: +wr sr,
+// then -wi si; im: +wi sr, then +wr si; from +0), so a fixed block equals
+// bf_ffma_kernel's result bit for bit.  Only blocks (or groups) outside the tensor
+// domain get here; throughput does not matter.
+template <int LAYOUT>
+__device__ __forceinline__ void fix_block(const JobCtx &J, int64_t item, int g) {
+    const int64_t blk = block_of(J, item);
+    const int f = J.f;
+    const float *Sb = J.S + blk * (int64_t)(120 * f);
+    const float4 *Wg = J.Wp + (int64_t)g * f * 32;
+    for (int e = threadIdx.x; e < bfk::kAnt * bfk::kB; e += blockDim.x) {
+        const int i = e / bfk::kB, j = e - bfk::kB * i;
+        const int ag = i >> 3, jw = (i & 7) >> 1;
+        const bool odd = (i & 1) != 0;
+        float re = +0.0f, im = +0.0f;
+        for (int k = 0; k < f; ++k) {
+            const float4 w4 = __ldg(Wg + k * 32 + jw * 8 + ag);   // bf_relayout_w's Wp layout
+            const float wr = odd ? w4.y : w4.x, wi = odd ? w4.w : w4.z;
+            float sr, si;
+            if (LAYOUT != 1) {
+                const float2 v = __ldg(reinterpret_cast<const float2 *>(Sb) + k * bfk::kB + j);
+                sr = v.x;
+                si = v.y;
+            } else {
+                sr = __ldg(Sb + k * bfk::kB + j);
+                si = __ldg(Sb + (f + k) * bfk::kB + j);
+            }
+            re = fmaf(wr, sr, re);
+            im = fmaf(wi, sr, im);
+            re = fmaf(-wi, si, re);
+            im = fmaf(wr, si, im);
+        }
+        float *Rb = J.R + blk * (int64_t)(bfk::r_block_bytes(LAYOUT) / 4);
+        if (LAYOUT == 0) {
+            reinterpret_cast<float2 *>(Rb)[e] = make_float2(re, im);
+        } else if (LAYOUT == 1) {
+            Rb[e] = re;
+            Rb[bfk::kAnt * bfk::kB + e] = im;
+        } else if (LAYOUT == 2) {
+            reinterpret_cast<uint32_t *>(Rb)[e] = bfk::pack_half2(re, im);
+        } else {
+            reinterpret_cast<uint32_t *>(Rb)[e] = bfk::pack_i16x2(re, im, J.out_scale);
+        }
+    }
+}
+
+// Is every value of S block `blk` (480 f bytes) inside the tensor domain?  (fix-up rescan)
+__device__ __forceinline__ bool block_in_domain(const JobCtx &J, int64_t blk) {
+    const uint32_t *Sb = reinterpret_cast<const uint32_t *>(J.S) + blk * (int64_t)(120 * J.f);
+    bool ok = true;
+    for (int e = threadIdx.x; e < 120 * J.f; e += blockDim.x) {
+        const uint32_t u = __ldg(Sb + e) & 0x7FFFFFFFu;
+        ok &= u == 0u || (u >= kDomLo && u < kDomHi);
+    }
+    return __syncthreads_and(ok) != 0;
+}
 
 // Cost-balanced split of the group-sorted item list over the CTAs.  Work is
 // counted in tiles (2 blocks of one group; a group of m blocks is ceil(m / 2)
@@ -346,6 +424,12 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L::kOffTmem);
     JobCtx *jobs = reinterpret_cast<JobCtx *>(smem + L::kOffJobs);
     int32_t *soffs = reinterpret_cast<int32_t *>(smem + L::kOffOffs);
+    // fix-up list of out-of-domain blocks: (item, job << 16 | group), its length, an
+    // overflow flag, and per (S ring stage, block of the tile) the last tile listed + 1
+    int2 *fix_list = reinterpret_cast<int2 *>(smem + L::kOffFix);
+    int *fix_n = reinterpret_cast<int *>(smem + L::kOffFix + kFixCap * 8);
+    int *fix_over = fix_n + 1;
+    int *fix_last = fix_n + 4;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int kNJ = F == 0 ? kMaxJobs : 1;
@@ -359,6 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             if (p.job[i].offsets) base += p.job[i].n_groups + 2;
         JobCtx &J = jobs[threadIdx.x];
         J.Wimg = q.Wimg;
+        J.Wp = q.Wp;
         J.S = q.S;
         J.perm = q.perm;
         J.wexact = q.wexact;
@@ -394,6 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     if (!any) return;   // CTA-uniform, before any TMEM allocation
 
     if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
+    if (threadIdx.x < 4 + 2 * kMaxStages) fix_n[threadIdx.x] = 0;   // n, overflow, last[]
     if (threadIdx.x == 32) {
         for (int i = 0; i < 3; ++i) {
             bfk::mbar_init(bar_a_full + i, 32 * kSplitWarps);
@@ -428,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         const int bsel = m >= 60 ? 1 : 0, j = m - 60 * bsel;
         const uint32_t a_lane = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         int cur_g = -1, cur_j = -1;
-        bool cur_exact = false;
+        int cur_wf = 0;                                  // wexact flags of the current group
         for (int64_t t = 0; it.next(tl); ++t) {
             const JobCtx &J = jobs[tl.job];
             const int f = F > 0 ? F : J.f;
@@ -445,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             if (tl.g != cur_g || tl.job != cur_j) {
                 cur_g = tl.g;
                 cur_j = tl.job;
-                cur_exact = __ldg(J.wexact + tl.g) != 0;
+                cur_wf = __ldg(J.wexact + tl.g);
             }
             // This warp's K chunks of the thread's row of S (half of them above f = 12) are
             // read from the ring once into registers and the slot is released at once; the
@@ -454,6 +540,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             const int c_half0 = (F > 0 && F <= 12) ? KP : ((KP / 8 + 1) >> 1) * 8;
             const int c_beg0 = ks ? c_half0 : 0, c_end0 = ks ? KP : c_half0;
             float xs[kSlots * 8];
+            // tensor domain check of every value read, kept in a predicate
+            bool out_dom = false;
 #pragma unroll
             for (int i = 0; i < kSlots; ++i) {
                 const int c0 = c_beg0 + 8 * i;
@@ -473,14 +561,30 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                     }
                     xs[8 * i + 2 * q] = re;
                     xs[8 * i + 2 * q + 1] = im;
+                    const uint32_t ur = __float_as_uint(re) & 0x7FFFFFFFu, ui = __float_as_uint(im) & 0x7FFFFFFFu;
+                    out_dom |= (ur - kDomLo >= kDomHi - kDomLo && ur != 0u) |
+                               (ui - kDomLo >= kDomHi - kDomLo && ui != 0u);
                 }
             }
+            if (valid && ((cur_wf & 2) || out_dom)) {
+                // rare: list the block once per tile (the first thread to see it wins; a
+                // stage's slot is reused only after every split warp finished this tile)
+                const int key = (int)(t + 1);
+                if (atomicMax(fix_last + 2 * stage + bsel, key) < key) {
+                    const int idx = atomicAdd(fix_n, 1);
+                    if (idx < kFixCap)
+                        fix_list[idx] = make_int2((int)(it.item - tl.cnt + bsel), (it.j << 16) | cur_g);
+                    else
+                        atomicExch(fix_over, 1);
+                }
+            }
+            if (kEarlyRelease) mbar_arrive(bar_s_empty + stage);    // values are in registers
 #pragma unroll
             for (int pass = 0; pass < 3; ++pass) {
                 const int term = pass == 2 ? 0 : pass + 1;
                 bfk::mbar_wait(bar_a_free + term, par);
                 tc::fence_after_sync();
-                if (term == 2 && !cur_exact) {   // S3 is only multiplied for tf32-exact W
+                if (term == 2 && !(cur_wf & 1)) {   // S3 is only multiplied for tf32-exact W
                     tc::fence_before_sync();
                     mbar_arrive(bar_a_full + term);
                     continue;
@@ -510,22 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                         const float x3 = r1 - x2;            // exact, fits tf32
                         v[e] = __float_as_uint(term == 0 ? x1 : (term == 1 ? x2 : x3));
                     }
-                    if (term == 1 && !cur_exact) {
-                        // general W: region 1 holds the bf16 correction operand, K'' = 2 KP
-                        // elements [S2 (kk < KP) | S1 (kk >= KP)], two per column: this
-                        // chunk's 8 values of S2 go to columns c0/2.., of S1 to KP/2 + c0/2..
-                        uint32_t w2[4], w1[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            w2[e] = tc::pack_bf16x2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
-                            const float s1a = tc::tf32_round(x[2 * e]), s1b = tc::tf32_round(x[2 * e + 1]);
-                            w1[e] = tc::pack_bf16x2(s1a, s1b);
-                        }
-                        if constexpr (!(DBG & 4)) {
-                            tc::tmem_st4(a_lane + kARegion + c0 / 2, w2);
-                            tc::tmem_st4(a_lane + kARegion + KP / 2 + c0 / 2, w1);
-                        }
-                    } else if ((DBG & 32) && term == 0) {
+                    if ((DBG & 32) && term == 0) {
                         uint32_t h[4];
 #pragma unroll
                         for (int e = 0; e < 4; ++e)
@@ -539,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 tc::fence_before_sync();
                 mbar_arrive(bar_a_full + term);
             }
-            mbar_arrive(bar_s_empty + stage);             // ring slot may be refilled
+            if (!kEarlyRelease) mbar_arrive(bar_s_empty + stage);   // ring slot may be refilled
         }
     } else if (warp == kProdWarp) {
         // ------------------------------------------------------------ S producer (TMA bulk)
@@ -598,14 +687,14 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         int cur_g = -1, cur_j = -1;
         int64_t seg = -1;
         constexpr uint32_t idesc = tc::idesc_tf32(128, 128);
-        constexpr uint32_t idesc_c = tc::idesc_bf16(128, 128);
+        constexpr uint32_t idesc_c = tc::idesc_bf16(128, 128);   // DBG 16 only
         uint32_t w_base = tc::smem_u32(Wsm);
         bool exact = false;
         for (int64_t t = 0; it.next(tl); ++t) {
             const JobCtx &J = jobs[tl.job];
             const int KP = F > 0 ? L::KP : J.kp;
             if (tl.g != cur_g || tl.job != cur_j) {   // new group segment: W prefetched by the producer
-                exact = __ldg(J.wexact + tl.g) != 0;
+                exact = (__ldg(J.wexact + tl.g) & 1) != 0;
                 // the previous segment's buffer is free once every MMA issued so far completed
                 if (seg >= 0 && lane == 0) tc::mma_commit(bar_wfree + (int)(seg % L::kWBufs));
                 __syncwarp();
@@ -620,41 +709,36 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             const uint32_t u = (uint32_t)(t >> 1);
             const uint32_t d = tmem + kDCol0 + 128 * b;
             bfk::mbar_wait(bar_d_free + b, (u & 1) ^ 1);
-            // MMA groups over K, small terms first:
+            // MMA groups over K, small terms first, every one kind::tf32 (exact products):
             //   tf32-exact W (W2 == 0, e.g. identity / selection): S2 W1, S3 W1, S1 W1
-            //   in tf32 (= S W exactly up to accumulation rounding: copies are bit-exact);
-            //   general W: the two correction products S2 W1 + S1 W2 as ONE bf16 MMA
-            //   group over K'' = 2 KP ([S2 | S1] x [W1 ; W2], KP/8 instructions of K = 16),
-            //   then S1 W1 in tf32 — 2 KP/8 instead of 3 KP/8 MMAs.
+            //   (= S W exactly up to accumulation rounding: copies are bit-exact);
+            //   general W: S2 W1, S1 W2, S1 W1 (the S3 region is not used) — 3 KP/8 MMAs
+            //   (DESIGN.md §7).  The middle group of general W reads the S1 region.
             // Each split term's TMEM region is released by a commit once read.
 #pragma unroll
             for (int grp = 0; grp < 3; ++grp) {
-                const int at = grp == 0 ? 1 : (grp == 1 ? 2 : 0);   // A region: S2/corr, S3, S1
+                const int at = grp == 0 ? 1 : (grp == 1 ? 2 : 0);   // barrier: S2, S3, S1
                 bfk::mbar_wait(bar_a_full + at, (uint32_t)(t & 1));
+                const bool s1w2 = grp == 1 && !exact;
+                if (s1w2) bfk::mbar_wait(bar_a_full + 0, (uint32_t)(t & 1));
                 tc::fence_after_sync();
-                const bool run = grp != 1 || exact;
-                const bool bf16 = grp == 0 && !exact;
+                const int areg = s1w2 ? 0 : at;                     // A region read
+                const uint32_t boff = s1w2 ? (uint32_t)(KP / 4) : 0u;  // W2 image after W1
                 if (lane == 0) {
                     // DBG & 16 (energy experiment): the S1 W1 group as ceil(KP / 16)
                     // fp16-kind K = 16 MMAs on the same (reinterpreted) operands
                     const int nkb = ((DBG & 16) && grp == 2) ? (KP + 15) / 16 : KP / 8;
-                    if (run) {
 #pragma unroll
-                        for (int kb = 0; kb < nkb; ++kb) {
-                            const uint64_t desc = tc::smem_desc(
-                                w_base + (uint32_t)(((bf16 ? KP / 4 : 0) + 2 * kb) * 16 * 128),
-                                16 * 128, 128);
-                            if constexpr (!(DBG & 1)) {
-                                if ((DBG & 16) && grp == 2)
-                                    tc::mma_bf16_ts(d, tmem + at * kARegion + kb * 8, desc,
-                                                    idesc_c & ~((7u << 7) | (7u << 10)), kb != 0);
-                                else if (bf16)
-                                    tc::mma_bf16_ts(d, tmem + at * kARegion + kb * 8, desc, idesc_c,
-                                                    kb != 0);
-                                else
-                                    tc::mma_tf32_ts(d, tmem + at * kARegion + kb * 8, desc, idesc,
-                                                    (grp | kb) != 0);
-                            }
+                    for (int kb = 0; kb < nkb; ++kb) {
+                        const uint64_t desc = tc::smem_desc(
+                            w_base + (uint32_t)((boff + 2 * kb) * 16 * 128), 16 * 128, 128);
+                        if constexpr (!(DBG & 1)) {
+                            if ((DBG & 16) && grp == 2)
+                                tc::mma_bf16_ts(d, tmem + areg * kARegion + kb * 8, desc,
+                                                idesc_c & ~((7u << 7) | (7u << 10)), kb != 0);
+                            else
+                                tc::mma_tf32_ts(d, tmem + areg * kARegion + kb * 8, desc, idesc,
+                                                (grp | kb) != 0);
                         }
                     }
                     if (grp < 2) tc::mma_commit(bar_a_free + at);
@@ -745,7 +829,6 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             tc::tmem_ld_wait();
             tc::fence_before_sync();
             mbar_arrive(bar_d_free + b);                 // TMEM buffer b may be overwritten
-            const bool odd = (j & 1) != 0;
             if constexpr (!(DBG & 2) && kStageR) {
                 // staged: both blocks of the tile in their global layout in shared memory,
                 // then one bulk store per block by the first epilogue thread.  The previous
@@ -783,12 +866,37 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             }
         }
     }
-    if (kStageR && warp == kEpiWarp0 && lane == 0) bulk_wait_all();   // stage read, stores done
+    if (kStageR && warp == kEpiWarp0 && lane == 0) {
+        bulk_wait_all();                                   // stage read, stores done
+        asm volatile("fence.proxy.async.global;" ::: "memory");   // before any fix-up rewrite
+    }
     tc::fence_before_sync();
     __syncthreads();
     if (warp == 0) {
         tc::fence_after_sync();
         tc::tmem_free<512>(tmem);
+    }
+    // ---- fix-up of out-of-domain blocks (CTA-uniform; nothing to do in practice): the
+    //      listed blocks, or after an overflow every block of this CTA's ranges rechecked.
+    const int nfix = *fix_n;
+    if (nfix > 0) {
+        if (*fix_over == 0) {
+            for (int e = 0; e < nfix; ++e) {
+                const int2 en = fix_list[e];
+                fix_block<LAYOUT>(jobs[en.y >> 16], en.x, en.y & 0xFFFF);
+            }
+        } else {
+            TileIter it2{jobs, n_jobs, 0, nullptr, 0, 0, 0, 0};
+            it2.enter(0);
+            Tile t2;
+            while (it2.next(t2)) {
+                const JobCtx &J = jobs[t2.job];
+                const bool wbad = (__ldg(J.wexact + t2.g) & 2) != 0;
+                for (int b2 = 0; b2 < t2.cnt; ++b2)
+                    if (wbad || !block_in_domain(J, block_of(J, t2.item + b2)))
+                        fix_block<LAYOUT>(J, t2.item + b2, t2.g);
+            }
+        }
     }
 }
 

@@ -13,8 +13,13 @@ partition is a pure function of the tags, so every rank computes it locally.
   55 / (G * ceil(55 / G))).  Within a rank blocks keep ascending block-id order
   (bf_apply routes them again locally).
 * untagged workloads (c2, c3): contiguous, balanced block ranges.
-* c5 (4096-block chunks dealt to cells by chunk id): each chunk is split evenly
-  across ranks, so every rank sees every cell's f.
+* c5 (4096-block chunks dealt to cells by chunk id c mod 8): chunks are beamformed in
+  windows of 8 consecutive chunks (one of every cell, one bf_apply_batch launch each) and
+  whole windows are dealt round-robin to ranks (window w -> rank w mod world), so every
+  rank holds the same mix of cells' f by construction and each launch keeps whole
+  4096-block chunks (splitting every chunk would leave 512 blocks per rank at 8 GPUs,
+  ~3.5 per CTA: fill and drain would dominate).  Not c mod world: with 8 ranks that would
+  pin one cell (one f) per GPU and imbalance the load up to 36x.
 """
 from __future__ import annotations
 
@@ -40,6 +45,16 @@ def chunk_shard(chunk: int, chunk_blocks: int, rank: int, world: int) -> tuple[i
     """Global [first, first + count) of rank's share of one c5 chunk."""
     f0, c = even_range(chunk_blocks, rank, world)
     return chunk * chunk_blocks + f0, c
+
+
+def window_shard(n_chunks: int, window: int, rank: int, world: int) -> list[list[int]]:
+    """c5: the windows (lists of consecutive chunk ids, `window` per window, the last one
+    possibly shorter) that rank processes, window w -> rank w mod world, in order."""
+    if world < 1 or not (0 <= rank < world) or window < 1:
+        raise ValueError("bad rank / world / window")
+    n_win = (n_chunks + window - 1) // window
+    return [list(range(w * window, min((w + 1) * window, n_chunks)))
+            for w in range(rank, n_win, world)]
 
 
 def broadcast_precoders(W, src: int = 0):

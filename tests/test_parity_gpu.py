@@ -291,6 +291,31 @@ def test_invalid_tags_are_left_unwritten_and_checked(monkeypatch, variant):
     assert e.value.status == bf.Status.INVALID_VALUE
 
 
+@pytest.mark.parametrize("layout", [Layout.INTERLEAVED, Layout.INTERLEAVED_I16OUT])
+def test_f0_with_tags_honours_invalid_tags(monkeypatch, layout):
+    """f = 0 with tags: validly tagged blocks become +0.0, blocks with tags outside
+    [0, n_groups) are left unwritten (bf.h), and BF_CHECK=1 reports them."""
+    n, G = 77, 3
+    plan = Plan(f=0, layout=layout)
+    plan.set_precoders(torch.zeros((G, 64, 0), dtype=torch.complex64, device=DEV))
+    tags = (np.arange(n) % G).astype(np.int32)
+    tags[[4, 50]] = [G, -2]
+    td = torch.from_numpy(tags).to(DEV)
+    shape = plan.r_shape(n)
+    R = torch.full(shape, 7, dtype=plan.r_dtype, device=DEV)
+    plan.apply(torch.zeros((n, 0, 60), dtype=torch.complex64, device=DEV), td, out=R)
+    torch.cuda.synchronize()
+    Rn = R.cpu().numpy().reshape(n, -1)
+    assert (Rn[[4, 50]] == 7).all()
+    ok = np.setdiff1d(np.arange(n), [4, 50])
+    assert not Rn[ok].view(np.uint16 if Rn.dtype.itemsize == 2 else np.uint32).any()
+    monkeypatch.setenv("BF_CHECK", "1")
+    with pytest.raises(bf.BfError) as e:
+        plan.apply(torch.zeros((n, 0, 60), dtype=torch.complex64, device=DEV), td, out=R)
+    assert e.value.status == bf.Status.INVALID_VALUE
+    plan.close()
+
+
 def test_invalid_tags_with_one_group(variant):
     """One precoder group and tags: the tags are still honoured (bf.h), so a tag other than 0
     leaves its block unwritten — the single-group shortcut applies only to group_idx = NULL.
@@ -755,23 +780,26 @@ def test_non_finite_inputs_stay_local(variant):
     """A NaN or Inf in S[n][k][j] makes exactly column j of block n non-finite (for every
     antenna with W[i][k] != 0) and leaves every other element equal to the clean run
     (reading R16: IEEE propagation, no cross-talk).  Non-finite values are
-    outside the accuracy contract; the tensor path turns an Inf into NaN (its split
-    subtracts S1 from S), the FFMA path keeps IEEE infinities where they arise."""
+    outside the tensor domain: the tensor kernel recomputes those two blocks with the FFMA
+    kernel's arithmetic (its fix-up), so there they equal the clean FFMA run."""
     f = 9
     W = syn.precoders(61, 0, 1, 64, f, "unit_columns")
     S = syn.qam_symbols(61, 0, np.arange(20), f, 60, 16)
     clean = run_plan(W, S, variant=variant)
+    clean_ffma = run_plan(W, S, variant=Variant.FFMA)
     bad = S.copy()
     bad[3, 2, 7] = complex(np.nan, 0.0)
     bad[11, 8, 59] = complex(np.inf, 1.0)
     got = run_plan(W, bad, variant=variant)
+    want = clean.copy()
+    want[[3, 11]] = clean_ffma[[3, 11]]
     mask = np.zeros(got.shape, bool)
     mask[3, :, 7] = True
     mask[11, :, 59] = True
     assert not np.isfinite(got[mask].view(np.float32)).all()
     assert not np.isfinite(got[3, :, 7]).any()
-    assert_bitwise(np.where(mask, 0, got), np.where(mask, 0, clean), "unaffected elements")
-
+    assert_bitwise(np.where(mask, 0, got), np.where(mask, 0, want), "unaffected elements")
+    assert_bitwise(got[[3, 11]], run_plan(W, bad, variant=Variant.FFMA)[[3, 11]], "== FFMA kernel")
 
 
 # ---------------------------------------------------------------------------

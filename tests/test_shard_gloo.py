@@ -94,3 +94,59 @@ def test_even_range_and_chunk_shard():
     assert (first, cnt) == (7 * 4096 + 1024, 1024)
     with pytest.raises(ValueError):
         shard.even_range(10, 3, 3)
+
+
+def _window_worker(rank, world, port, n_chunks, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bf_synth as syn
+        from paper_1810_11451_b200 import shard
+        wins = shard.window_shard(n_chunks, 8, rank, world)
+        mine = [c for w in wins for c in w]
+        fc = syn.cell_flows(syn.workload("c5").seed, 8)
+        work = float(sum(int(fc[c % 8]) + 64 for c in mine))      # bytes per block ~ f + 64
+        allv = [None] * world
+        dist.all_gather_object(allv, mine)
+        q.put((rank, wins, allv, shard.max_over_ranks(work), shard.sum_over_ranks(work)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_c5_window_dealing_gloo(world):
+    """c5: whole 8-chunk windows dealt round-robin (window w -> rank w mod world): every chunk
+    exactly once, each window one chunk of every cell, every rank the same per-cell mix, so
+    the per-rank work (sum of f + 64 over its chunks) is equal."""
+    n_chunks = 2048
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_window_worker, args=(r, world, port, n_chunks, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    gathered = out[0][2]
+    assert all(o[2] == gathered for o in out)                      # every rank agrees
+    allc = np.concatenate([np.asarray(g) for g in gathered])
+    assert np.array_equal(np.sort(allc), np.arange(n_chunks))      # disjoint cover
+    for rank, wins, _, mx, tot in out:
+        for w in wins:
+            assert len(w) == 8 and sorted(c % 8 for c in w) == list(range(8))   # one per cell
+            assert w[0] // 8 % world == rank
+        cells = np.bincount(np.asarray([c for w in wins for c in w]) % 8, minlength=8)
+        assert (cells == n_chunks // 8 // world).all()              # same per-cell mix
+        assert mx * world == tot                                    # perfectly balanced
+
+
+def test_window_shard_ragged():
+    from paper_1810_11451_b200 import shard
+    for n_chunks, world in [(2048, 8), (100, 3), (5, 4), (1, 2)]:
+        got = [c for r in range(world) for w in shard.window_shard(n_chunks, 8, r, world) for c in w]
+        assert sorted(got) == list(range(n_chunks))
+    assert shard.window_shard(5, 8, 1, 4) == []
+    with pytest.raises(ValueError):
+        shard.window_shard(10, 0, 0, 1)
