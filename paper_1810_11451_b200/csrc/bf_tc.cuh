@@ -649,6 +649,22 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             const JobCtx &J = jobs[tl.job];
             const int f = F > 0 ? F : J.f;
             const int stage = (int)(t % kRing);
+            // S of this tile first: at a group change with one W buffer the producer then
+            // waits for the previous group's MMAs to drain (wfree), and the S load's HBM
+            // latency should overlap that wait and the W load instead of following them
+            bfk::mbar_wait(bar_s_empty + stage, (uint32_t)(((t / kRing) & 1) ^ 1));
+            if (DBG & 8) {
+                if (lane == 0) mbar_arrive(bar_s_full + stage);
+            } else if (lane == 0) {
+                const uint32_t sbytes = (uint32_t)(480 * f);
+                bfk::mbar_arrive_expect_tx(bar_s_full + stage, (uint32_t)tl.cnt * sbytes);
+                bfk::bulk_g2s(Ss + (stage * 2) * (L::kSBlock / 4), J.S + blk0 * (int64_t)(120 * f),
+                              sbytes, bar_s_full + stage, pol);
+                if (tl.cnt > 1)
+                    bfk::bulk_g2s(Ss + (stage * 2 + 1) * (L::kSBlock / 4),
+                                  J.S + blk1 * (int64_t)(120 * f), sbytes, bar_s_full + stage, pol);
+            }
+            __syncwarp();
             if (tl.g != cur_g || tl.job != cur_j) {
                 cur_g = tl.g;
                 cur_j = tl.job;
@@ -662,19 +678,6 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                     bfk::bulk_g2s(Wsm + wb * (L::kWBytes / 4), J.Wimg + (int64_t)tl.g * (wbytes / 4),
                                   (uint32_t)wbytes, bar_wfull + wb, bfk::policy_evict_last());
                 }
-                __syncwarp();
-            }
-            bfk::mbar_wait(bar_s_empty + stage, (uint32_t)(((t / kRing) & 1) ^ 1));
-            if (DBG & 8) {
-                if (lane == 0) mbar_arrive(bar_s_full + stage);
-            } else if (lane == 0) {
-                const uint32_t sbytes = (uint32_t)(480 * f);
-                bfk::mbar_arrive_expect_tx(bar_s_full + stage, (uint32_t)tl.cnt * sbytes);
-                bfk::bulk_g2s(Ss + (stage * 2) * (L::kSBlock / 4), J.S + blk0 * (int64_t)(120 * f),
-                              sbytes, bar_s_full + stage, pol);
-                if (tl.cnt > 1)
-                    bfk::bulk_g2s(Ss + (stage * 2 + 1) * (L::kSBlock / 4),
-                                  J.S + blk1 * (int64_t)(120 * f), sbytes, bar_s_full + stage, pol);
             }
             __syncwarp();
             tl = nx;
