@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <new>
 #include <utility>
 #include <vector>
@@ -17,8 +18,9 @@ using bfh::fail;
 
 struct bff_plan_s {
     int n = bff::kN, device = 0, num_sms = 0, ctas_per_sm = 0;
-    float2 *tw = nullptr, *H = nullptr;
-    float4 *tw3 = nullptr;
+    int ns = 2;                          // signals per CTA iteration (filter_kernel<ns>)
+    float2 *tw = nullptr, *H = nullptr;    // twiddles; DFT(h) / N
+    float4 *tw3 = nullptr;                 // pass-3 twiddle pairs
     bool have_taps = false;
     bool profiling = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
@@ -46,7 +48,10 @@ bf_status launch(bff_plan_t p, const float2 *s, float2 *y, int64_t n, int mode, 
         e1 = p->prof_events[p->prof_used].second;
         ++p->prof_used;
     }
-    bff::filter_kernel<<<grid, bff::kThreads, bff::kSmemBytes, st>>>(fp);
+    if (p->ns == 1)
+        bff::filter_kernel<1><<<grid, bff::kThreads, bff::smem_bytes(1), st>>>(fp);
+    else
+        bff::filter_kernel<2><<<grid, bff::kThreads, bff::smem_bytes(2), st>>>(fp);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "filter_kernel launch");
     ++p->launches;
@@ -94,11 +99,13 @@ bf_status bff_plan_create(int n, bff_plan_t *out) {
                     prop.minor);
     }
     p->num_sms = prop.multiProcessorCount;
-    e = cudaFuncSetAttribute(bff::filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             bff::kSmemBytes);
+    // signals per CTA iteration: kDefaultNS, or BFF_NS=1|2 (tuning experiments)
+    if (const char *env = std::getenv("BFF_NS")) p->ns = std::atoi(env) == 1 ? 1 : 2;
+    const void *kern = p->ns == 1 ? (const void *)bff::filter_kernel<1> : (const void *)bff::filter_kernel<2>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bff::smem_bytes(p->ns));
     if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaFuncSetAttribute (filter)"); }
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->ctas_per_sm, bff::filter_kernel,
-                                                      bff::kThreads, bff::kSmemBytes);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->ctas_per_sm, kern, bff::kThreads,
+                                                      bff::smem_bytes(p->ns));
     if (e != cudaSuccess) { delete p; return cuda_fail(e, "occupancy query"); }
     if (cudaMalloc(&p->tw, bff::kTwN * sizeof(float2)) != cudaSuccess ||
         cudaMalloc(&p->tw3, bff::kTw3N * sizeof(float4)) != cudaSuccess ||
