@@ -265,6 +265,7 @@ struct FParams {
     const float2 *H;     // [2048] DFT(h) / N (plan-owned)
     const float2 *tw;    // [2048] twiddle table w^m (plan-owned)
     const float4 *tw3;   // [3][128] pass-3 base twiddle pairs (plan-owned)
+    const float4 *twp;   // [5][32] pass-2 base twiddle pairs of the warp kernel (plan-owned)
     int64_t n_sig;
     int mode;            // 0: filter; 1: forward FFT only;
                          // 2: forward FFT scaled by 1/N (builds the plan's H from h)

@@ -5,10 +5,12 @@
 #include <algorithm>
 #include <cstdlib>
 #include <new>
+#include <string>
 #include <utility>
 #include <vector>
 
 #include "bf_filter.cuh"
+#include "bf_filter_warp.cuh"
 #include "bf_filter.h"
 #include "bf_host.h"
 
@@ -18,9 +20,12 @@ using bfh::fail;
 
 struct bff_plan_s {
     int n = bff::kN, device = 0, num_sms = 0, ctas_per_sm = 0;
-    int ns = 2;                          // signals per CTA iteration (filter_kernel<ns>)
+    // kernel: 3 (default) filter_warp_kernel<2> — one warp per signal, twiddle and H tables
+    // in shared memory, 2 CTAs per SM; 0 filter_warp_kernel<3> (no tables, 3 CTAs per SM);
+    // 1 / 2 the CTA-per-signal kernel filter_kernel<1 / 2> (kept for comparisons)
+    int kind = 3;
     float2 *tw = nullptr, *H = nullptr;    // twiddles; DFT(h) / N
-    float4 *tw3 = nullptr;                 // pass-3 twiddle pairs
+    float4 *tw3 = nullptr, *twp = nullptr; // pass-3 twiddle pairs; warp kernel's pass-2 bases
     bool have_taps = false;
     bool profiling = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
@@ -33,9 +38,11 @@ namespace {
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 bf_status launch(bff_plan_t p, const float2 *s, float2 *y, int64_t n, int mode, cudaStream_t st) {
-    bff::FParams fp{s, y, p->H, p->tw, p->tw3, n, mode};
+    bff::FParams fp{s, y, p->H, p->tw, p->tw3, p->twp, n, mode};
     const int64_t cap = (int64_t)p->num_sms * std::max(1, p->ctas_per_sm);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(n, cap));
+    const bool warpk = p->kind == 0 || p->kind == 3;   // 4 signals (warps) per CTA
+    const int64_t units = warpk ? (n + 3) / 4 : n;                 // warp kernel: 4 signals per CTA
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(units, cap));
     cudaEvent_t e1 = nullptr;
     if (p->profiling && mode == 0) {
         if (p->prof_used == p->prof_events.size()) {
@@ -48,7 +55,11 @@ bf_status launch(bff_plan_t p, const float2 *s, float2 *y, int64_t n, int mode, 
         e1 = p->prof_events[p->prof_used].second;
         ++p->prof_used;
     }
-    if (p->ns == 1)
+    if (p->kind == 0)
+        bff::filter_warp_kernel<3><<<grid, bff::kThreads, bff::warp_smem_bytes(false), st>>>(fp);
+    else if (p->kind == 3)
+        bff::filter_warp_kernel<2><<<grid, bff::kThreads, bff::warp_smem_bytes(true), st>>>(fp);
+    else if (p->kind == 1)
         bff::filter_kernel<1><<<grid, bff::kThreads, bff::smem_bytes(1), st>>>(fp);
     else
         bff::filter_kernel<2><<<grid, bff::kThreads, bff::smem_bytes(2), st>>>(fp);
@@ -99,36 +110,46 @@ bf_status bff_plan_create(int n, bff_plan_t *out) {
                     prop.minor);
     }
     p->num_sms = prop.multiProcessorCount;
-    // signals per CTA iteration: kDefaultNS, or BFF_NS=1|2 (tuning experiments)
-    if (const char *env = std::getenv("BFF_NS")) p->ns = std::atoi(env) == 1 ? 1 : 2;
-    const void *kern = p->ns == 1 ? (const void *)bff::filter_kernel<1> : (const void *)bff::filter_kernel<2>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bff::smem_bytes(p->ns));
+    // BFF_FILTER_KERNEL=warp_tab|warp|cta1|cta2 selects a kernel for comparison experiments
+    if (const char *env = std::getenv("BFF_FILTER_KERNEL")) {
+        const std::string k(env);
+        p->kind = k == "warp" ? 0 : k == "cta1" ? 1 : k == "cta2" ? 2 : 3;
+    }
+    const void *kern = p->kind == 0   ? (const void *)bff::filter_warp_kernel<3>
+                       : p->kind == 3 ? (const void *)bff::filter_warp_kernel<2>
+                       : p->kind == 1 ? (const void *)bff::filter_kernel<1> : (const void *)bff::filter_kernel<2>;
+    const int smem = p->kind == 0 ? bff::warp_smem_bytes(false)
+                     : p->kind == 3 ? bff::warp_smem_bytes(true) : bff::smem_bytes(p->kind);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaFuncSetAttribute (filter)"); }
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->ctas_per_sm, kern, bff::kThreads,
-                                                      bff::smem_bytes(p->ns));
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->ctas_per_sm, kern, bff::kThreads, smem);
     if (e != cudaSuccess) { delete p; return cuda_fail(e, "occupancy query"); }
     if (cudaMalloc(&p->tw, bff::kTwN * sizeof(float2)) != cudaSuccess ||
         cudaMalloc(&p->tw3, bff::kTw3N * sizeof(float4)) != cudaSuccess ||
+        cudaMalloc(&p->twp, bff::kTwpN * sizeof(float4)) != cudaSuccess ||
         cudaMalloc(&p->H, bff::kN * sizeof(float2)) != cudaSuccess) {
         cudaGetLastError();
         cudaFree(p->tw);
         cudaFree(p->tw3);
+        cudaFree(p->twp);
         cudaFree(p->H);
         delete p;
         return fail(BF_ERR_OUT_OF_MEMORY, "cudaMalloc of the filter plan tables failed");
     }
     bff::twiddle_kernel<<<(bff::kTwN + 255) / 256, 256>>>(p->tw);
     bff::twiddle3_kernel<<<(bff::kTw3N + 255) / 256, 256>>>(p->tw3);
+    bff::twiddle_warp_kernel<<<(bff::kTwpN + 255) / 256, 256>>>(p->twp);
     e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         cudaFree(p->tw);
         cudaFree(p->tw3);
+        cudaFree(p->twp);
         cudaFree(p->H);
         delete p;
         return cuda_fail(e, "twiddle table");
     }
-    p->launches += 2;
+    p->launches += 3;
     *out = p;
     return BF_OK;
 }
@@ -171,6 +192,7 @@ bf_status bff_destroy(bff_plan_t p) {
         DeviceGuard g(p->device);
         cudaFree(p->tw);
         cudaFree(p->tw3);
+        cudaFree(p->twp);
         cudaFree(p->H);
         for (auto &ev : p->prof_events) {
             cudaEventDestroy(ev.first);

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--windows", type=int, default=16)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--share", type=int, default=0)
+    ap.add_argument("--per-launch", type=int, default=8, help="chunks per bf_apply_batch launch (<= 16)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     wl = syn.workload("c5")
@@ -40,9 +41,10 @@ def main():
         plans.append(pl)
     wins = []
     nbytes = 0
-    for w in range(a.windows):
+    B = a.per_launch
+    for w in range(a.windows * 8 // B):
         jobs = {"tagged": [], "one_group": [], "untagged": []}
-        for c in range(8 * w, 8 * w + 8):
+        for c in range(B * w, B * w + B):
             f = int(fc[c % 8])
             S = torch.empty((4096, f, 60), dtype=torch.complex64, device=dev)
             sync.gen_symbols(S, wl.seed, 0, f, 60, 0, first=c * 4096)
@@ -70,7 +72,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.reps
-        print(json.dumps({"mode": mode, "windows": a.windows, "us_per_window": 1e3 * ms / a.windows,
+        print(json.dumps({"mode": mode, "per_launch": B, "windows": a.windows, "us_per_window": 1e3 * ms / a.windows,
                           "GBps": nbytes / (ms * 1e-3) / 1e9, "frac": nbytes / (ms * 1e-3) / 1e9 / hbm}),
               flush=True)
 

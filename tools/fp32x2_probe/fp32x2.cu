@@ -48,6 +48,27 @@ __global__ void __launch_bounds__(256) probe(float *out, int iters, float x) {
     }
 }
 
+// dependent-chain latency: one warp, one chain, clock64 around 4096 dependent ops
+template <int MODE>
+__global__ void lat(float *out, long long *cyc, float x) {
+    float a = x * threadIdx.x;
+    uint64_t b;
+    float2 v = make_float2(a, a + 1.f), xx = make_float2(x, x);
+    b = *reinterpret_cast<uint64_t *>(&v);
+    const uint64_t X = *reinterpret_cast<uint64_t *>(&xx);
+    const long long t0 = clock64();
+    for (int i = 0; i < 4096; ++i) {
+        if (MODE == 0) asm volatile("fma.rn.f32 %0, %0, %1, %1;" : "+f"(a) : "f"(x));
+        else if (MODE == 1) b = ffma2(b, X, X);
+        else if (MODE == 2) asm volatile("add.rn.f32 %0, %0, %1;" : "+f"(a) : "f"(x));
+        else b = fadd2(b, X);
+    }
+    const long long t1 = clock64();
+    float2 r = *reinterpret_cast<float2 *>(&b);
+    out[threadIdx.x] = a + r.x + r.y;
+    if (threadIdx.x == 0) *cyc = t1 - t0;
+}
+
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -79,5 +100,19 @@ int main() {
                 printf("{\"op\": \"%s\", \"ms\": %.3f, \"Gresults_per_s\": %.1f, \"TFLOPs\": %.2f}\n",
                        names[mode], ms, lane_ops / ms / 1e6, flops / ms / 1e9);
         }
+    long long *cyc;
+    cudaMalloc(&cyc, 8);
+    const char *ln[4] = {"FFMA", "FFMA2", "FADD", "FADD2"};
+    for (int mode = 0; mode < 4; ++mode) {
+        for (int rep = 0; rep < 2; ++rep) {
+            if (mode == 0) lat<0><<<1, 32>>>(out, cyc, 1.0001f);
+            if (mode == 1) lat<1><<<1, 32>>>(out, cyc, 1.0001f);
+            if (mode == 2) lat<2><<<1, 32>>>(out, cyc, 1.0001f);
+            if (mode == 3) lat<3><<<1, 32>>>(out, cyc, 1.0001f);
+        }
+        long long c = 0;
+        cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+        printf("{\"op\": \"%s\", \"dependent_latency_cycles\": %.2f}\n", ln[mode], c / 4096.0);
+    }
     return 0;
 }
