@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--steady-seconds", type=float, default=10.0,
                     help="after the timed burst, back-to-back steps for this long: steady-state "
                          "throughput, SM clock and power under the board's power cap (0 = off)")
+    ap.add_argument("--no-server", action="store_true",
+                    help="c2: skip the slot-server latency leg (bf_server_*)")
+    ap.add_argument("--server-slots", type=int, default=200, help="c2: timed slots of the server leg")
     ap.add_argument("--parity-stride", type=int, default=16,
                     help="check every k-th block of each rank's output against the oracle after "
                          "the timed region (c4: 65 536 of 2^20 blocks; c2: every block)")
@@ -560,6 +563,11 @@ def run_ours(args):
                         "regenerated on the host (bf_synth) and compared with the fp64 oracle")
     parity = reduce_parity(parity, dev, world)
 
+    # ---- c2: the slot server — one persistent launch serving slot after slot (bf_server_*)
+    server = None
+    if wl.name == "c2" and world == 1 and not args.no_server:
+        server = server_latency(args, plan, S, R, dev)
+
     # ---- steady state: the same step back to back for --steady-seconds (the timed burst
     #      above is ~0.2 s; the board's 1000 W cap takes ~0.3 s to bite)
     steady = None
@@ -644,7 +652,7 @@ def run_ours(args):
                        else ARITH.get(roof.get("variant"), "?")},
             "flops_per_s": total_blocks * wl.block_flops * args.steps / (elapsed_ms * 1e-3),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk, "steady": steady,
+            "clocks": clk, "steady": steady, "server": server,
         }
         if "tflops" in os.environ.get("BF_BENCH_PROBE", "tflops"):
             try:
@@ -661,6 +669,52 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return rc
+
+
+def server_latency(args, plan, S, R_ref, dev) -> dict:
+    """One slot at a time through the slot server (include/bf.h bf_server_*): submit, wait,
+    next.  16 distinct S / R buffers in rotation (16 x 37 MB > the 126 MB L2: every slot
+    reads and writes cold memory).  Device time per slot from the server's %globaltimer
+    stamps (CTA 0 sees the doorbell -> last CTA done); host round trip submit -> wait.
+    The last results are checked bit for bit against the timed bf_apply output."""
+    import statistics
+
+    import torch
+
+    import paper_1810_11451_b200 as bf
+    nbuf = 16
+    Ss = [S.clone() for _ in range(nbuf)]
+    Rs = [torch.empty_like(R_ref) for _ in range(nbuf)]
+    torch.cuda.synchronize()
+    srv = bf.Server(plan)
+    stream = torch.cuda.Stream(dev)
+    srv.start(stream)
+    dev_us, host_us = [], []
+    try:
+        for i in range(20 + args.server_slots):
+            k = i % nbuf
+            t0 = time.perf_counter()
+            tk = srv.submit(Ss[k], Rs[k])
+            srv.wait(tk, timeout_s=30)
+            t1 = time.perf_counter()
+            if i >= 20:
+                dev_us.append(srv.slot_time_us(tk))
+                host_us.append((t1 - t0) * 1e6)
+    finally:
+        srv.close()
+    torch.cuda.synchronize()
+    same = all(torch.equal(torch.view_as_real(Rs[k]), torch.view_as_real(R_ref)) for k in range(nbuf))
+    n = R_ref.shape[0]
+    med = statistics.median(dev_us)
+    q = sorted(dev_us)
+    return {"slots": len(dev_us), "blocks_per_slot": n,
+            "device_us_median": med, "device_us_p10": q[len(q) // 10], "device_us_p90": q[9 * len(q) // 10],
+            "host_roundtrip_us_median": statistics.median(host_us),
+            "REs_per_s_at_device_latency": n * 60 / (med * 1e-6),
+            "bitwise_equal_to_bf_apply": bool(same),
+            "how": f"bf_server: one persistent launch; {len(dev_us)} slots submitted one at a time "
+                   f"(submit -> wait), {nbuf} S/R buffers in rotation (cold L2); device time = "
+                   "%globaltimer from CTA 0 seeing the doorbell to the last CTA done"}
 
 
 def steady_state(args, plan, S, tags, R, local, rank, world, dev, bytes_launch, res_launch, hbm):

@@ -248,6 +248,44 @@ bf_status bf_plan_set_sm_share(bf_plan_t p, int sms);
 bf_status bf_plan_kernel_config(bf_plan_t p, int64_t n_blocks, int *grid, int *block,
                                 int *smem_bytes, int *ctas_per_sm);
 
+/* ---- slot server: latency-bound applies without a launch per slot ----------------
+ * One persistent launch of the tensor kernel (runtime-f form, one CTA per SM of the
+ * plan's SM share) stays resident and serves untagged applies ("slots", e.g. one
+ * 5G NR slot of BASELINE.json configs[1]) posted through a mailbox in mapped pinned
+ * host memory: no launch, no kernel prologue and no precoder load per slot, so a
+ * slot costs its data movement plus the pipeline's fill and drain.  Same arithmetic
+ * and results, bit for bit, as bf_apply with BF_VARIANT_TENSOR ("many
+ * products W x S" with W constant).
+ *   bf_server_create: plan with f >= 1, exactly one precoder group, precoders in the
+ *     tensor domain (else BF_ERR_UNSUPPORTED).  The plan must outlive the server and
+ *     must not be re-configured while the server runs.
+ *   bf_server_start: launches the server on `stream`.  While it runs it occupies the
+ *     SMs of the plan's SM share: work on other streams waits for those SMs (use
+ *     bf_plan_set_sm_share to leave some free).  It exits by bf_server_stop, or by
+ *     itself after 60 s without a slot.
+ *   bf_server_submit: posts R_dev = W x S_dev for n_blocks (layout of the plan,
+ *     validated as bf_apply); non-blocking, returns a ticket (1, 2, ...).  At most 4
+ *     slots are in flight: a fifth submit waits for the oldest.  S and R must stay
+ *     valid until the slot is done.
+ *   bf_server_wait: returns when slot `ticket` is done (its R written and visible to
+ *     the host and later stream work), BF_ERR_CUDA after timeout_s seconds (<= 0:
+ *     no limit) or if the server died; BF_ERR_INVALID_VALUE if a slot held S values
+ *     outside the tensor domain (the server does not run the FFMA fix-up: such data
+ *     goes through bf_apply).
+ *   bf_server_slot_time: device time of a done slot (among the last 4): from CTA 0
+ *     seeing the slot's doorbell to the last CTA finishing it, in microseconds
+ *     (%globaltimer).
+ *   bf_server_stop: posts the stop slot and synchronises the server's stream. */
+typedef struct bf_server_s *bf_server_t;
+bf_status bf_server_create(bf_plan_t p, bf_server_t *out);
+bf_status bf_server_start(bf_server_t s, void *stream);
+bf_status bf_server_submit(bf_server_t s, const void *S_dev, void *R_dev, int64_t n_blocks,
+                           uint64_t *ticket);
+bf_status bf_server_wait(bf_server_t s, uint64_t ticket, double timeout_s);
+bf_status bf_server_slot_time(bf_server_t s, uint64_t ticket, double *device_us);
+bf_status bf_server_stop(bf_server_t s);
+bf_status bf_server_destroy(bf_server_t s);
+
 const char *bf_status_string(bf_status s);
 const char *bf_last_error(void);  /* thread-local detail of the last failure */
 int bf_version(void);

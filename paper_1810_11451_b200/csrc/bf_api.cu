@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -54,6 +56,7 @@ constexpr int kAutoTensorMinF[4] = {2, 7, 4, 4};   // [layout]
 
 BfKernelTable g_table;      // FFMA kernels [f][layout]
 BfKernelTable g_table_tc;   // tcgen05 split-TF32 kernels [f][layout]
+BfKernelEntry g_server[4];  // slot-server kernels [layout]
 std::once_flag g_table_once;
 
 void init_table() {
@@ -66,6 +69,7 @@ void init_table() {
     bf_register_f25_30(g_table, g_table_tc);
     bf_register_f31_36(g_table, g_table_tc);
     bf_register_batch(g_table_tc);
+    bf_register_server(g_server);
 }
 
 // ---------------------------------------------------------------------------
@@ -1069,6 +1073,165 @@ bf_status bf_plan_set_sm_share(bf_plan_t p, int sms) {
     if (sms < 0) return fail(BF_ERR_INVALID_VALUE, "sms must be >= 0 (got %d)", sms);
     p->sm_share = sms;
     return BF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// slot server (include/bf.h bf_server_*)
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct bf_server_s {
+    bf_plan_t plan = nullptr;
+    bftc::SrvMailbox *mb = nullptr;        // mapped pinned host memory
+    bftc::SrvMailbox *mb_dev = nullptr;    // its device address
+    bftc::SrvDev *dev = nullptr;
+    cudaStream_t stream = nullptr;
+    bool running = false;
+    unsigned long long next = 0;           // last submitted slot
+};
+
+namespace {
+volatile bftc::SrvMailbox *vmb(bf_server_t s) { return s->mb; }
+bf_status server_post(bf_server_t s, const void *S, void *R, int64_t n, int stop, uint64_t *ticket) {
+    const unsigned long long k = s->next + 1;
+    // at most kSrvRing slots in flight: the descriptor entry of slot k - ring must be consumed
+    if (k > (unsigned long long)bftc::kSrvRing) {
+        const unsigned long long need = k - bftc::kSrvRing;
+        while (vmb(s)->done < need) {
+            const cudaError_t q = cudaStreamQuery(s->stream);
+            if (q != cudaErrorNotReady)
+                return q == cudaSuccess ? fail(BF_ERR_INVALID_VALUE, "the server is not running")
+                                        : cuda_fail(q, "slot server");
+        }
+    }
+    volatile bftc::SrvSlotDesc *d = &vmb(s)->desc[k % bftc::kSrvRing];
+    d->S = reinterpret_cast<unsigned long long>(S);
+    d->R = reinterpret_cast<unsigned long long>(R);
+    d->n = n;
+    d->stop = stop;
+    std::atomic_thread_fence(std::memory_order_seq_cst);   // descriptor before seq (x86: TSO)
+    vmb(s)->seq = k;
+    s->next = k;
+    if (ticket) *ticket = k;
+    return BF_OK;
+}
+}  // namespace
+
+extern "C" {
+
+bf_status bf_server_create(bf_plan_t p, bf_server_t *out) {
+    if (!p || !out) return fail(BF_ERR_INVALID_VALUE, "NULL argument");
+    if (p->f == 0) return fail(BF_ERR_UNSUPPORTED, "the slot server needs f >= 1");
+    if (p->n_groups != 1) return fail(BF_ERR_UNSUPPORTED, "the slot server serves one precoder group "
+                                                         "(untagged slots); got %d", p->n_groups);
+    if (!p->w_in_domain)
+        return fail(BF_ERR_UNSUPPORTED, "precoders outside the tensor domain: use bf_apply");
+    DeviceGuard guard(p->device);
+    bf_server_t s = new (std::nothrow) bf_server_s();
+    if (!s) return fail(BF_ERR_OUT_OF_MEMORY, "host allocation of the server failed");
+    s->plan = p;
+    if (cudaHostAlloc(reinterpret_cast<void **>(&s->mb), sizeof(bftc::SrvMailbox),
+                      cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void **>(&s->mb_dev), s->mb, 0) != cudaSuccess ||
+        cudaMalloc(&s->dev, sizeof(bftc::SrvDev)) != cudaSuccess) {
+        cudaGetLastError();
+        if (s->mb) cudaFreeHost(s->mb);
+        cudaFree(s->dev);
+        delete s;
+        return fail(BF_ERR_OUT_OF_MEMORY, "slot server mailbox allocation failed");
+    }
+    std::memset(s->mb, 0, sizeof(bftc::SrvMailbox));
+    *out = s;
+    return BF_OK;
+}
+
+bf_status bf_server_start(bf_server_t s, void *stream) {
+    bfh::NvtxRange nvtx_("bf_server_start");
+    if (!s) return fail(BF_ERR_INVALID_VALUE, "server is NULL");
+    if (s->running) return fail(BF_ERR_INVALID_VALUE, "server already running");
+    bf_plan_t p = s->plan;
+    DeviceGuard guard(p->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::memset(s->mb, 0, sizeof(bftc::SrvMailbox));
+    BF_CUDA(cudaMemsetAsync(s->dev, 0, sizeof(bftc::SrvDev), st));
+    const BfKernelEntry &kern = g_server[p->layout];
+    BF_CUDA(cudaFuncSetAttribute(kern.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kern.smem_bytes));
+    bftc::TcParams tp{};
+    tp.n_jobs = 0;
+    tp.job[0] = tc_job(p, nullptr, nullptr, nullptr, nullptr, 0);
+    tp.srv.mb = s->mb_dev;
+    tp.srv.dev = s->dev;
+    tp.srv.timeout_ns = 60ll * 1000 * 1000 * 1000;   // an abandoned server exits after 60 s idle
+    void *args[] = {&tp};
+    cudaError_t e = cudaLaunchKernel(kern.fn, dim3(sms_used(p)), dim3(bftc::kThreads), args,
+                                     (size_t)kern.smem_bytes, st);
+    if (e != cudaSuccess) return cuda_fail(e, "slot server launch");
+    ++p->launches;
+    s->stream = st;
+    s->running = true;
+    s->next = 0;
+    return BF_OK;
+}
+
+bf_status bf_server_submit(bf_server_t s, const void *S_dev, void *R_dev, int64_t n_blocks,
+                           uint64_t *ticket) {
+    if (!s) return fail(BF_ERR_INVALID_VALUE, "server is NULL");
+    if (!s->running) return fail(BF_ERR_INVALID_VALUE, "server is not running");
+    bf_status st = validate_apply(s->plan, S_dev, nullptr, R_dev, n_blocks, true);
+    if (st != BF_OK) return st;
+    return server_post(s, S_dev, R_dev, n_blocks, 0, ticket);
+}
+
+bf_status bf_server_wait(bf_server_t s, uint64_t ticket, double timeout_s) {
+    if (!s) return fail(BF_ERR_INVALID_VALUE, "server is NULL");
+    if (ticket > s->next) return fail(BF_ERR_INVALID_VALUE, "ticket %llu was not submitted",
+                                      (unsigned long long)ticket);
+    const auto t0 = std::chrono::steady_clock::now();
+    while (vmb(s)->done < ticket) {
+        const cudaError_t q = cudaStreamQuery(s->stream);
+        if (q != cudaErrorNotReady && vmb(s)->done < ticket)
+            return q == cudaSuccess ? fail(BF_ERR_CUDA, "the server exited before slot %llu",
+                                           (unsigned long long)ticket)
+                                    : cuda_fail(q, "slot server");
+        if (timeout_s > 0 && std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s)
+            return fail(BF_ERR_CUDA, "slot %llu not done after %.1f s", (unsigned long long)ticket, timeout_s);
+    }
+    if (vmb(s)->error)
+        return fail(BF_ERR_INVALID_VALUE, "a slot held S values outside the tensor domain "
+                                          "(its R is not the contract result; use bf_apply)");
+    return BF_OK;
+}
+
+bf_status bf_server_slot_time(bf_server_t s, uint64_t ticket, double *device_us) {
+    if (!s || !device_us) return fail(BF_ERR_INVALID_VALUE, "NULL argument");
+    if (ticket == 0 || vmb(s)->done < ticket || s->next >= ticket + bftc::kSrvRing)
+        return fail(BF_ERR_INVALID_VALUE, "slot %llu is not done or no longer in the ring",
+                    (unsigned long long)ticket);
+    const int e = (int)(ticket % bftc::kSrvRing);
+    *device_us = (double)(vmb(s)->t_done[e] - vmb(s)->t_seen[e]) * 1e-3;
+    return BF_OK;
+}
+
+bf_status bf_server_stop(bf_server_t s) {
+    bfh::NvtxRange nvtx_("bf_server_stop");
+    if (!s) return fail(BF_ERR_INVALID_VALUE, "server is NULL");
+    if (!s->running) return BF_OK;
+    DeviceGuard guard(s->plan->device);
+    bf_status st = server_post(s, nullptr, nullptr, 0, 1, nullptr);
+    s->running = false;
+    if (st != BF_OK) return st;
+    BF_CUDA(cudaStreamSynchronize(s->stream));
+    return BF_OK;
+}
+
+bf_status bf_server_destroy(bf_server_t s) {
+    if (!s) return fail(BF_ERR_INVALID_VALUE, "server is NULL");
+    bf_status st = s->running ? bf_server_stop(s) : BF_OK;
+    DeviceGuard guard(s->plan->device);
+    cudaFreeHost(s->mb);
+    cudaFree(s->dev);
+    delete s;
+    return st;
 }
 
 bf_status bf_plan_kernel_config(bf_plan_t p, int64_t n_blocks, int *grid, int *block,

@@ -18,3 +18,4 @@ void bf_register_f19_24(BfKernelTable &t, BfKernelTable &tc);
 void bf_register_f25_30(BfKernelTable &t, BfKernelTable &tc);
 void bf_register_f31_36(BfKernelTable &t, BfKernelTable &tc);
 void bf_register_batch(BfKernelTable &tc);   // slot [0][layout]: runtime-f batch kernel
+void bf_register_server(BfKernelEntry (&srv)[4]);   // [layout]: slot-server kernel

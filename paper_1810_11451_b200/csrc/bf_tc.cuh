@@ -112,9 +112,44 @@ struct TcJob {
 // size from the pointer, i.e. the common prefix.  The per-f kernels (bf_apply: one job)
 // take the 1-job form: 1.3 KB less parameter data per launch (~1 us of launch latency,
 // tools/launch_lat); the batch kernel (F = 0) takes all kMaxJobs.
+// Slot server (bf_server_*: one persistent launch serving a stream of untagged applies;
+// SRV kernel instantiation).  The mailbox lives in mapped pinned host memory: the host
+// writes a slot descriptor and then bumps seq; CTA 0 polls it and re-broadcasts the
+// descriptor through SrvDev (device memory) to the other CTAs; the last CTA to finish a
+// slot publishes done = seq and the device timestamps.
+constexpr int kSrvRing = 4;                // slots in flight (descriptor rings)
+struct SrvSlotDesc {
+    unsigned long long S, R;               // device pointers of the slot
+    long long n;                           // blocks
+    int stop;                              // 1: exit after the slots before this one
+    int pad;
+};
+struct SrvMailbox {
+    unsigned long long seq;                // written by the host after desc[seq % ring]
+    SrvSlotDesc desc[kSrvRing];
+    int error;                             // device: a slot held values outside the tensor domain
+    int pad;
+    unsigned long long done;               // device: last completed slot
+    unsigned long long t_seen[kSrvRing];   // device globaltimer: CTA 0 saw slot k (k % ring)
+    unsigned long long t_done[kSrvRing];   // device globaltimer: slot k complete
+};
+struct SrvDev {
+    unsigned long long seq;                // re-broadcast of the mailbox
+    unsigned long long S[kSrvRing], R[kSrvRing];
+    long long n[kSrvRing];
+    int stop[kSrvRing];
+    unsigned int done_cnt[kSrvRing];
+};
+struct SrvPtrs {
+    SrvMailbox *mb;                        // device view of the mapped mailbox
+    SrvDev *dev;
+    long long timeout_ns;                  // a poll that waits longer than this stops the server
+};
+
 template <int NJ>
 struct TcParamsN {
     int n_jobs;
+    SrvPtrs srv;                           // SRV kernels only
     TcJob job[NJ];
 };
 using TcParams = TcParamsN<kMaxJobs>;
@@ -130,7 +165,7 @@ struct TcSmem {
     static constexpr int kSBlock = 480 * FS;           // one block of S (slot stride)
     static constexpr int kJobBytes = kMaxJobs * 96;    // per-job context (JobCtx)
     static constexpr int kFixBytes = kFixCap * 8 + 16 + 2 * kMaxStages * 4;   // fix-up list
-    static constexpr int kMisc = 24 * 8 + 16 + kOffsSlots * 4 + kJobBytes + kFixBytes;
+    static constexpr int kMisc = 32 * 8 + 16 + kOffsSlots * 4 + kJobBytes + kFixBytes;
     // R staging: the epilogue writes the tile's two blocks of R into shared memory in
     // their global layout and one thread stores each block with a bulk copy (full lines,
     // no partial sectors at planar row boundaries).  Shared memory, in order of
@@ -155,8 +190,8 @@ struct TcSmem {
     static constexpr int kStages = kStagesFit < kMaxS ? kStagesFit : kMaxS;
     static_assert(kStages >= 2, "S ring needs two stages");
     static constexpr int kOffS = kWBufs * kWBytes;     // kStagesAlloc x 2 blocks
-    static constexpr int kOffBar = kOffS + kStagesAlloc * 2 * kSBlock;   // 24 mbarrier slots
-    static constexpr int kOffTmem = kOffBar + 24 * 8;
+    static constexpr int kOffBar = kOffS + kStagesAlloc * 2 * kSBlock;   // 32 mbarrier slots
+    static constexpr int kOffTmem = kOffBar + 32 * 8;
     static constexpr int kOffJobs = kOffTmem + 16;     // JobCtx[kMaxJobs]
     static constexpr int kOffOffs = kOffJobs + kJobBytes;   // group offsets of every job
     static constexpr int kOffFix = kOffOffs + kOffsSlots * 4;   // int2 list, n, overflow, last[]
@@ -389,6 +424,82 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t by
         ::"l"(dst), "r"(tc::smem_u32(src)), "r"(bytes), "l"(policy) : "memory");
 }
 
+// ---- slot server helpers -------------------------------------------------------------
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_gpu(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Producer lane 0 of every CTA: wait for slot k (1-based), fill the CTA's descriptor ring
+// entry jobs[k % ring] from the template job tmpl and publish it to the other roles
+// (slot_full).  CTA 0 polls the host mailbox and re-broadcasts through SrvDev.  A poll
+// longer than the timeout behaves as a stop.  Returns false on stop.
+__device__ __forceinline__ bool srv_fill_slot(const SrvPtrs &sp, const TcJob &tmpl, JobCtx *ring,
+                                              unsigned long long k, uint64_t *slot_full) {
+    const int e = (int)(k % kSrvRing);
+    SrvDev *dv = sp.dev;
+    const unsigned long long t0 = globaltimer();
+    bool stop = false;
+    if (blockIdx.x == 0) {
+        while (ld_acquire_sys(&sp.mb->seq) < k) {
+            if ((long long)(globaltimer() - t0) > sp.timeout_ns) { stop = true; break; }
+        }
+        volatile SrvSlotDesc *d = &sp.mb->desc[e];
+        dv->S[e] = stop ? 0ull : d->S;
+        dv->R[e] = stop ? 0ull : d->R;
+        dv->n[e] = stop ? 0ll : d->n;
+        dv->stop[e] = stop ? 1 : d->stop;
+        if (!stop) sp.mb->t_seen[e] = globaltimer();
+        st_release_gpu(&dv->seq, k);
+    } else {
+        while (ld_acquire_gpu(&dv->seq) < k) {
+            if ((long long)(globaltimer() - t0) > sp.timeout_ns) { stop = true; break; }
+        }
+    }
+    JobCtx &J = ring[e];
+    const volatile SrvDev *vd = dv;
+    stop = stop || vd->stop[e] != 0;
+    J.Wimg = tmpl.Wimg;
+    J.Wp = tmpl.Wp;
+    J.S = reinterpret_cast<const float *>(stop ? 0ull : vd->S[e]);
+    J.perm = nullptr;
+    J.wexact = tmpl.wexact;
+    J.R = reinterpret_cast<float *>(stop ? 0ull : vd->R[e]);
+    J.offs = nullptr;
+    J.n_groups = 1;
+    J.f = tmpl.f;
+    J.kp = kp_of(tmpl.f);
+    J.wbytes = 2 * J.kp * 128 * 4;
+    J.out_scale = tmpl.out_scale;
+    J.g_begin = 0;
+    const int64_t n = stop ? 0 : vd->n[e];
+    int64_t b0 = 0, e0 = 0;
+    int g0 = 0;
+    cta_range(nullptr, 1, n, 0, b0, e0, g0);
+    J.begin = b0;
+    J.end = stop ? -1 : e0;                       // end = -1: the stop marker
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(slot_full + e))
+                 : "memory");
+    return !stop;
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar))
                  : "memory");
@@ -400,8 +511,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // the split also writes S1 as packed fp16 (the instruction stream of a real fp16 main
 // product, without range handling).
 // Results are wrong with DBG != 0.
-template <int F, int LAYOUT, int DBG = 0>
+// SRV (F = 0 only): the slot server — one persistent launch; the jobs come one slot at a
+// time from the host mailbox (p.srv) instead of the parameter block, which holds the
+// plan's template job (precoders, f, output scale) in job[0].  Untagged slots, one group.
+template <int F, int LAYOUT, int DBG = 0, bool SRV = false>
 __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> p) {
+    static_assert(!SRV || F == 0, "the slot server runs the runtime-f kernel");
     using L = TcSmem<F>;
     // TMEM column stride of the three A regions: fixed across the jobs of a launch
     // (the split of a job's first tile must not overlap the previous job's regions
@@ -419,7 +534,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     // a_full[t] / a_free[t]: TMEM A region of split term t (0: S1, 1: S2, 2: S3)
     uint64_t *bar_a_full = bars + 0, *bar_a_free = bars + 3, *bar_d_full = bars + 6,
              *bar_d_free = bars + 8, *bar_wfull = bars + 10, *bar_wfree = bars + 12,
-             *bar_s_full = bars + 14, *bar_s_empty = bars + 14 + kRing;
+             *bar_s_full = bars + 14, *bar_s_empty = bars + 14 + kRing,
+             *bar_slot_full = bars + 24, *bar_slot_free = bars + 28;   // SRV: descriptor ring
     float *Ss = reinterpret_cast<float *>(smem + L::kOffS);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L::kOffTmem);
     JobCtx *jobs = reinterpret_cast<JobCtx *>(smem + L::kOffJobs);
@@ -433,10 +549,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int kNJ = F == 0 ? kMaxJobs : 1;
-    const int n_jobs = p.n_jobs < kNJ ? p.n_jobs : kNJ;
+    const int n_jobs = SRV ? 0 : (p.n_jobs < kNJ ? p.n_jobs : kNJ);
     // ---- prologue: jobs and their group offsets into shared memory, then this CTA's
     //      cost-balanced range of every job (one warp each, shuffle scans).
-    if (threadIdx.x < n_jobs) {
+    if ((int)threadIdx.x < n_jobs) {
         const TcJob &q = p.job[threadIdx.x];
         int base = 0;
         for (int i = 0; i < (int)threadIdx.x; ++i)
@@ -474,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         }
     }
     __syncthreads();
-    bool any = false;
+    bool any = SRV;
     for (int jj = 0; jj < n_jobs; ++jj) any |= jobs[jj].begin < jobs[jj].end;
     if (!any) return;   // CTA-uniform, before any TMEM allocation
 
@@ -497,6 +613,11 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             bfk::mbar_init(bar_s_full + i, 1);
             bfk::mbar_init(bar_s_empty + i, 32 * kSplitWarps);
         }
+        if (SRV)
+            for (int i = 0; i < kSrvRing; ++i) {
+                bfk::mbar_init(bar_slot_full + i, 1);
+                bfk::mbar_init(bar_slot_free + i, 1);
+            }
         bfk::mbar_fence_init();
     }
     tc::fence_before_sync();
@@ -506,6 +627,49 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     TileIter it{jobs, n_jobs, 0, nullptr, 0, 0, 0, 0};
     it.enter(0);
     Tile tl;
+    // The next tile of this role.  SRV: when the current slot is exhausted, the epilogue
+    // completes it (srv_done), the producer fills the next slot's descriptor, every role
+    // then waits for it and restarts its walk on it; false on stop.
+    enum { kRoleProd, kRoleSplit, kRoleMma, kRoleEpi };
+    unsigned long long slot = 0;
+    auto next_tile = [&](Tile &t2, int role) -> bool {
+        if constexpr (!SRV) {
+            return it.next(t2);
+        } else {
+            for (;;) {
+                if (slot > 0 && it.next(t2)) return true;
+                const unsigned long long u = slot / kSrvRing;     // use index of the next entry
+                if (role == kRoleEpi && slot > 0 && warp == kEpiWarp0 && lane == 0) {
+                    // slot done in this CTA: its R stores complete, then count it
+                    bulk_wait_all();
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    __threadfence();
+                    const int e = (int)(slot % kSrvRing);
+                    if (*fix_n > 0) atomicExch(&p.srv.mb->error, 1);
+                    const unsigned int old = atomicAdd(&p.srv.dev->done_cnt[e], 1u);
+                    if (old == (unsigned)(((slot - 1) / kSrvRing + 1) * gridDim.x) - 1u) {
+                        __threadfence_system();
+                        p.srv.mb->t_done[e] = globaltimer();
+                        st_release_sys(&p.srv.mb->done, slot);
+                    }
+                    mbar_arrive(bar_slot_free + e);
+                }
+                ++slot;
+                const int e = (int)(slot % kSrvRing);
+                if (role == kRoleProd) {
+                    if (lane == 0) {
+                        if (slot > kSrvRing) bfk::mbar_wait(bar_slot_free + e, (uint32_t)((u - 1) & 1));
+                        srv_fill_slot(p.srv, p.job[0], jobs, slot, bar_slot_full);
+                    }
+                    __syncwarp();
+                }
+                bfk::mbar_wait(bar_slot_full + e, (uint32_t)(((slot - 1) / kSrvRing) & 1));
+                if (jobs[e].end < 0) return false;
+                it = TileIter{jobs + e, 1, 0, nullptr, 0, 0, 0, 0};
+                it.enter(0);
+            }
+        }
+    };
 
     if (warp < kSplitWarps) {
         // ------------------------------------------------------------ split warps
@@ -515,8 +679,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         const uint32_t a_lane = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         int cur_g = -1, cur_j = -1;
         int cur_wf = 0;                                  // wexact flags of the current group
-        for (int64_t t = 0; it.next(tl); ++t) {
-            const JobCtx &J = jobs[tl.job];
+        for (int64_t t = 0; next_tile(tl, kRoleSplit); ++t) {
+            const JobCtx &J = it.jobs[tl.job];
             const int f = F > 0 ? F : J.f;
             const int KP = F > 0 ? L::KP : J.kp;
             const bool valid = m < 120 && bsel < tl.cnt;
@@ -638,15 +802,21 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         const uint64_t pol = bfk::policy_evict_first();
         int cur_g = -1, cur_j = -1;
         int64_t seg = -1;
-        bool have = it.next(tl);
-        int64_t blk0 = have ? block_of(jobs[tl.job], tl.item) : 0;
-        int64_t blk1 = have && tl.cnt > 1 ? block_of(jobs[tl.job], tl.item + 1) : 0;
+        // (SRV: untagged slots, block = item, and no look-ahead across a slot boundary)
+        bool have = next_tile(tl, kRoleProd);
+        int64_t blk0 = have ? block_of(it.jobs[tl.job], tl.item) : 0;
+        int64_t blk1 = have && tl.cnt > 1 ? block_of(it.jobs[tl.job], tl.item + 1) : 0;
+        const JobCtx *Jp = &it.jobs[tl.job];
         for (int64_t t = 0; have; ++t) {
             Tile nx;                       // next tile's block ids load while we wait
-            const bool have_nx = it.next(nx);
-            const int64_t nb0 = have_nx ? block_of(jobs[nx.job], nx.item) : 0;
-            const int64_t nb1 = have_nx && nx.cnt > 1 ? block_of(jobs[nx.job], nx.item + 1) : 0;
-            const JobCtx &J = jobs[tl.job];
+            bool have_nx = false;
+            int64_t nb0 = 0, nb1 = 0;
+            if constexpr (!SRV) {
+                have_nx = it.next(nx);
+                nb0 = have_nx ? block_of(jobs[nx.job], nx.item) : 0;
+                nb1 = have_nx && nx.cnt > 1 ? block_of(jobs[nx.job], nx.item + 1) : 0;
+            }
+            const JobCtx &J = *Jp;
             const int f = F > 0 ? F : J.f;
             const int stage = (int)(t % kRing);
             // S of this tile first: at a group change with one W buffer the producer then
@@ -680,10 +850,20 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 }
             }
             __syncwarp();
-            tl = nx;
-            have = have_nx;
-            blk0 = nb0;
-            blk1 = nb1;
+            if constexpr (SRV) {
+                have = next_tile(tl, kRoleProd);
+                if (have) {
+                    Jp = &it.jobs[tl.job];
+                    blk0 = tl.item;
+                    blk1 = tl.item + 1;
+                }
+            } else {
+                tl = nx;
+                have = have_nx;
+                blk0 = nb0;
+                blk1 = nb1;
+                if (have) Jp = &jobs[tl.job];
+            }
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------------------ MMA issuer
@@ -693,8 +873,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         constexpr uint32_t idesc_c = tc::idesc_bf16(128, 128);   // DBG 16 only
         uint32_t w_base = tc::smem_u32(Wsm);
         bool exact = false;
-        for (int64_t t = 0; it.next(tl); ++t) {
-            const JobCtx &J = jobs[tl.job];
+        for (int64_t t = 0; next_tile(tl, kRoleMma); ++t) {
+            const JobCtx &J = it.jobs[tl.job];
             const int KP = F > 0 ? L::KP : J.kp;
             if (tl.g != cur_g || tl.job != cur_j) {   // new group segment: W prefetched by the producer
                 exact = (__ldg(J.wexact + tl.g) & 1) != 0;
@@ -769,8 +949,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         const bool e0 = warp == kEpiWarp0 && lane == 0;  // issues the staged bulk stores
         uint64_t pol_r = 0;
         if (kStageR && e0) pol_r = bfk::policy_evict_first();
-        for (int64_t t = 0; it.next(tl); ++t) {
-            const JobCtx &J = jobs[tl.job];
+        for (int64_t t = 0; next_tile(tl, kRoleEpi); ++t) {
+            const JobCtx &J = it.jobs[tl.job];
             const int b = (int)(t & 1);
             const uint32_t u = (uint32_t)(t >> 1);
             const bool valid = m < 120 && bsel < tl.cnt;
@@ -881,7 +1061,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     }
     // ---- fix-up of out-of-domain blocks (CTA-uniform; nothing to do in practice): the
     //      listed blocks, or after an overflow every block of this CTA's ranges rechecked.
-    const int nfix = *fix_n;
+    const int nfix = SRV ? 0 : *fix_n;   // SRV: reported per slot (mailbox error) instead
     if (nfix > 0) {
         if (*fix_over == 0) {
             for (int e = 0; e < nfix; ++e) {

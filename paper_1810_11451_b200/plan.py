@@ -233,7 +233,56 @@ def plan_create_status(n_ant: int, f: int, b: int, layout: int = 0) -> Status:
     return Status(s)
 
 
-__all__ = ["Plan", "Layout", "Status", "Variant", "BfError", "plan_create_status", "N_ANT", "N_RE", "MAX_F"]
+class Server:
+    """bf_server_*: a persistent launch serving untagged applies of `plan` (one precoder
+    group) through a mapped-memory mailbox — no launch per slot (include/bf.h)."""
+
+    def __init__(self, plan: Plan):
+        self.plan = plan
+        self._h = ctypes.c_void_p()
+        check(lib().bf_server_create(plan._h, ctypes.byref(self._h)))
+        self._keep = {}
+
+    def start(self, stream=None) -> "Server":
+        check(lib().bf_server_start(self._h, _stream_handle(stream)))
+        return self
+
+    def submit(self, S: torch.Tensor, out: torch.Tensor) -> int:
+        """Post R = W x S into `out`; returns the slot's ticket (non-blocking)."""
+        n = S.shape[0]
+        self.plan._check(S, "S", self.plan.s_shape(n))
+        self.plan._check(out, "out", self.plan.r_shape(n), dtype=self.plan.r_dtype)
+        t = ctypes.c_uint64()
+        check(lib().bf_server_submit(self._h, _ptr(S), _ptr(out), n, ctypes.byref(t)))
+        self._keep[t.value % 8] = (S, out)
+        return t.value
+
+    def wait(self, ticket: int, timeout_s: float = 30.0) -> None:
+        check(lib().bf_server_wait(self._h, ctypes.c_uint64(ticket), float(timeout_s)))
+
+    def slot_time_us(self, ticket: int) -> float:
+        """Device time of a done slot (doorbell seen by CTA 0 -> last CTA done), us."""
+        v = ctypes.c_double()
+        check(lib().bf_server_slot_time(self._h, ctypes.c_uint64(ticket), ctypes.byref(v)))
+        return v.value
+
+    def stop(self) -> None:
+        check(lib().bf_server_stop(self._h))
+
+    def close(self) -> None:
+        if self._h:
+            check(lib().bf_server_destroy(self._h))
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+__all__ = ["Plan", "Server", "Layout", "Status", "Variant", "BfError", "plan_create_status", "N_ANT", "N_RE",
+           "MAX_F"]
 
 
 def apply_batch(jobs, stream=None) -> None:
