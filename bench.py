@@ -60,8 +60,9 @@ def parse():
     ap.add_argument("--parity-stride", type=int, default=16,
                     help="check every k-th block of each rank's output against the oracle after "
                          "the timed region (c4: 65 536 of 2^20 blocks; c2: every block)")
-    ap.add_argument("--c5-batch", type=int, default=8,
-                    help="c5: consecutive chunks per bf_apply_batch launch (1 = one bf_apply_routed per chunk)")
+    ap.add_argument("--c5-batch", type=int, default=16,
+                    help="c5: consecutive chunks per bf_apply_batch launch (1 = one bf_apply_routed per "
+                         "chunk; 16 = two of every cell, the kernel's job limit)")
     return ap.parse_args()
 
 
@@ -981,7 +982,7 @@ def run_c5(args, wl, world, rank, local, dev):
         plans.append(pl)
     torch.cuda.synchronize()
     t_bc = time.perf_counter() - t_bc
-    # Whole windows of B consecutive chunks (one chunk of every cell at B = 8) are dealt
+    # Whole windows of B consecutive chunks (two of every cell at the default B = 16) are dealt
     # round-robin to ranks (window w -> rank w mod world; shard.window_shard): every rank
     # sees the same per-cell f mix and each launch keeps whole 4096-block chunks.
     B = max(1, args.c5_batch)                # chunks per bf_apply_batch launch (window)

@@ -118,6 +118,9 @@ struct TcJob {
 // descriptor through SrvDev (device memory) to the other CTAs; the last CTA to finish a
 // slot publishes done = seq and the device timestamps.
 constexpr int kSrvRing = 4;                // slots in flight (descriptor rings)
+#ifndef BFTC_SRV_DIRECT
+#define BFTC_SRV_DIRECT 0   // 1: every CTA polls the host mailbox (measured 47x slower: PCIe contention)
+#endif
 struct SrvSlotDesc {
     unsigned long long S, R;               // device pointers of the slot
     long long n;                           // blocks
@@ -457,6 +460,18 @@ __device__ __forceinline__ bool srv_fill_slot(const SrvPtrs &sp, const TcJob &tm
     SrvDev *dv = sp.dev;
     const unsigned long long t0 = globaltimer();
     bool stop = false;
+#if BFTC_SRV_DIRECT
+    // every CTA polls the host mailbox itself (one PCIe round trip, no re-broadcast hop)
+    while (ld_acquire_sys(&sp.mb->seq) < k) {
+        if ((long long)(globaltimer() - t0) > sp.timeout_ns) { stop = true; break; }
+    }
+    if (blockIdx.x == 0 && !stop) sp.mb->t_seen[e] = globaltimer();
+    const volatile SrvSlotDesc *vdesc = &sp.mb->desc[e];
+    const unsigned long long dS = stop ? 0ull : vdesc->S, dR = stop ? 0ull : vdesc->R;
+    const long long dn = stop ? 0ll : vdesc->n;
+    stop = stop || vdesc->stop != 0;
+    (void)dv;
+#else
     if (blockIdx.x == 0) {
         while (ld_acquire_sys(&sp.mb->seq) < k) {
             if ((long long)(globaltimer() - t0) > sp.timeout_ns) { stop = true; break; }
@@ -473,15 +488,18 @@ __device__ __forceinline__ bool srv_fill_slot(const SrvPtrs &sp, const TcJob &tm
             if ((long long)(globaltimer() - t0) > sp.timeout_ns) { stop = true; break; }
         }
     }
-    JobCtx &J = ring[e];
     const volatile SrvDev *vd = dv;
+    const unsigned long long dS = stop ? 0ull : vd->S[e], dR = stop ? 0ull : vd->R[e];
+    const long long dn = stop ? 0ll : vd->n[e];
     stop = stop || vd->stop[e] != 0;
+#endif
+    JobCtx &J = ring[e];
     J.Wimg = tmpl.Wimg;
     J.Wp = tmpl.Wp;
-    J.S = reinterpret_cast<const float *>(stop ? 0ull : vd->S[e]);
+    J.S = reinterpret_cast<const float *>(dS);
     J.perm = nullptr;
     J.wexact = tmpl.wexact;
-    J.R = reinterpret_cast<float *>(stop ? 0ull : vd->R[e]);
+    J.R = reinterpret_cast<float *>(dR);
     J.offs = nullptr;
     J.n_groups = 1;
     J.f = tmpl.f;
@@ -489,7 +507,7 @@ __device__ __forceinline__ bool srv_fill_slot(const SrvPtrs &sp, const TcJob &tm
     J.wbytes = 2 * J.kp * 128 * 4;
     J.out_scale = tmpl.out_scale;
     J.g_begin = 0;
-    const int64_t n = stop ? 0 : vd->n[e];
+    const int64_t n = stop ? 0 : dn;
     int64_t b0 = 0, e0 = 0;
     int g0 = 0;
     cta_range(nullptr, 1, n, 0, b0, e0, g0);
