@@ -22,7 +22,7 @@ if not torch.cuda.is_available():   # pragma: no cover
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KEYS = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
         "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
-        "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks")
+        "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks", "parity")
 
 
 def _port():
@@ -58,6 +58,9 @@ def test_bench_c2_single_gpu_contract():
     assert d["config"]["workload"] == "c2"
     assert d["roofline"]["bound"] in ("hbm", "alu") and 0 < d["roofline"]["frac"] < 1.5
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
+    assert d["parity"]["ok"] and d["parity"]["blocks"] == 770          # every block vs the oracle
+    srv = d["server"]
+    assert srv["bitwise_equal_to_bf_apply"] and 0 < srv["device_us_median"] < 1000
     assert d["e2e"]["h2d_bytes_per_step"] == 770 * 480 * 36
     assert d["e2e"]["d2h_bytes_per_step"] == 770 * 30720
     assert d["gpu_launches"] >= 5
@@ -77,21 +80,36 @@ def test_bench_filter_contract():
 
 def test_bench_c4_two_ranks_share_gpu():
     """torchrun N = 2: subband sharding, W broadcast, max over ranks, whole-job value."""
-    d = _run(["--config", "c4", "--steps", "3", "--warmup", "3", "--no-e2e"], world=2)
+    d = _run(["--config", "c4", "--steps", "3", "--warmup", "3", "--no-e2e", "--steady-seconds", "0",
+              "--parity-stride", "256"], world=2)
     assert d["n_gpus"] == 2 and d["value"] > 0
     assert d["config"]["parallelism"].startswith("dp2")
+    assert d["config"]["world_size"] == 2 and d["config"]["backend"] == "gloo"
     assert d["cpu_baseline"] is None          # rank 0 at N = 1 only
     assert d["gpu_launches"] >= 2 * 3
+    par = d["parity"]                         # every rank checked its own shard
+    assert par["ok"] and len(par["per_rank"]) == 2 and all(r["ok"] and r["blocks"] > 0 for r in par["per_rank"])
 
 
 def test_bench_c5_short_stream():
     d = _run(["--config", "c5", "--steps", "3", "--warmup", "3", "--c5-chunks", "64"])
     assert d["config"]["workload"] == "c5" and d["config"]["chunks_per_step"] == 64
     assert d["config"]["launch_mode"] == "cuda_graph"
-    assert d["config"]["chunks_per_launch"] == 8 and d["config"]["launches_per_step"] == 8
+    assert d["config"]["chunks_per_launch"] == 16 and d["config"]["launches_per_step"] == 4
     assert d["config"]["apply_sms"] + d["config"]["route_sms"] \
         == torch.cuda.get_device_properties(0).multi_processor_count
     assert d["value"] > 0 and 0 < d["roofline"]["frac"] < 1.5
+
+
+def test_bench_c5_two_ranks_windows():
+    """torchrun N = 2 on c5: whole 16-chunk windows dealt to the ranks, every rank's ring
+    checked against the oracle."""
+    d = _run(["--config", "c5", "--steps", "2", "--warmup", "3", "--c5-chunks", "64"], world=2)
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["config"]["parallelism"].startswith("dp2 (whole 16-chunk windows")
+    assert d["config"]["launches_per_step"] == 2            # this rank's windows: 4 / 2
+    par = d["parity"]
+    assert par["ok"] and len(par["per_rank"]) == 2 and all(r["blocks"] > 0 for r in par["per_rank"])
 
 
 def test_bench_reference_arm():
