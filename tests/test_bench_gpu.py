@@ -117,10 +117,3 @@ def test_bench_reference_arm():
               "--cpu-seconds", "1"])
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0
-
-
-def test_bench_c5_two_ranks_share_gpu():
-    """torchrun N = 2 on c5: every chunk split across ranks, batched windows per rank."""
-    d = _run(["--config", "c5", "--steps", "3", "--warmup", "3", "--c5-chunks", "32"], world=2)
-    assert d["n_gpus"] == 2 and d["value"] > 0
-    assert d["config"]["chunks_per_step"] == 32 and d["config"]["chunks_per_launch"] == 8
