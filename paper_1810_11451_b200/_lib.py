@@ -19,7 +19,7 @@ EXPORTS = ("bf_plan_create", "bf_set_precoders", "bf_apply", "bf_apply_host", "b
            "bf_plan_set_variant", "bf_plan_get_variant", "bf_plan_set_sm_share",
            "bf_plan_set_output_exponent",
            "bf_server_create", "bf_server_start", "bf_server_submit", "bf_server_wait",
-           "bf_server_slot_time", "bf_server_stop", "bf_server_destroy",
+           "bf_server_slot_time", "bf_server_trace", "bf_server_stop", "bf_server_destroy",
            "bff_plan_create", "bff_set_taps", "bff_apply", "bff_fft", "bff_destroy",
            "bff_plan_set_profiling", "bff_plan_kernel_time", "bff_plan_launch_count",
            "bf_status_string", "bf_last_error", "bf_version")
@@ -98,6 +98,7 @@ def lib() -> ctypes.CDLL:
         "bf_server_submit": (i32, [vp, vp, vp, i64, P(ctypes.c_uint64)]),
         "bf_server_wait": (i32, [vp, ctypes.c_uint64, ctypes.c_double]),
         "bf_server_slot_time": (i32, [vp, ctypes.c_uint64, P(ctypes.c_double)]),
+        "bf_server_trace": (i32, [vp, P(ctypes.c_double), i32]),
         "bf_server_stop": (i32, [vp]),
         "bf_server_destroy": (i32, [vp]),
         "bf_status_string": (ctypes.c_char_p, [i32]),

@@ -1212,6 +1212,16 @@ bf_status bf_server_slot_time(bf_server_t s, uint64_t ticket, double *device_us)
     return BF_OK;
 }
 
+bf_status bf_server_trace(bf_server_t s, double *us, int n) {
+    if (!s || !us || n < 0) return fail(BF_ERR_INVALID_VALUE, "bad argument");
+    const unsigned long long t0 = vmb(s)->trace[0];
+    for (int i = 0; i < n && i < 8; ++i) {
+        const unsigned long long t = vmb(s)->trace[i];
+        us[i] = t ? (double)(long long)(t - t0) * 1e-3 : -1.0;
+    }
+    return BF_OK;
+}
+
 bf_status bf_server_stop(bf_server_t s) {
     bfh::NvtxRange nvtx_("bf_server_stop");
     if (!s) return fail(BF_ERR_INVALID_VALUE, "server is NULL");

@@ -121,12 +121,25 @@ constexpr int kSrvRing = 4;                // slots in flight (descriptor rings)
 #ifndef BFTC_SRV_DIRECT
 #define BFTC_SRV_DIRECT 0   // 1: every CTA polls the host mailbox (measured 47x slower: PCIe contention)
 #endif
-struct SrvSlotDesc {
+struct __align__(16) SrvSlotDesc {
     unsigned long long S, R;               // device pointers of the slot
     long long n;                           // blocks
     int stop;                              // 1: exit after the slots before this one
     int pad;
 };
+// the descriptor as two 16-byte words (one PCIe read each, issued together)
+__device__ __forceinline__ void ld_desc_sys(const SrvSlotDesc *d, unsigned long long &S,
+                                            unsigned long long &R, long long &n, int &stop) {
+    unsigned long long a0, a1, b0, b1;
+    asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%4];\n\t"
+                 "ld.relaxed.sys.global.v2.u64 {%2, %3}, [%5];"
+                 : "=l"(a0), "=l"(a1), "=l"(b0), "=l"(b1)
+                 : "l"(&d->S), "l"(&d->n) : "memory");
+    S = a0;
+    R = a1;
+    n = (long long)b0;
+    stop = (int)(b1 & 0xFFFFFFFFull);
+}
 struct SrvMailbox {
     unsigned long long seq;                // written by the host after desc[seq % ring]
     SrvSlotDesc desc[kSrvRing];
@@ -135,6 +148,7 @@ struct SrvMailbox {
     unsigned long long done;               // device: last completed slot
     unsigned long long t_seen[kSrvRing];   // device globaltimer: CTA 0 saw slot k (k % ring)
     unsigned long long t_done[kSrvRing];   // device globaltimer: slot k complete
+    unsigned long long trace[8];           // CTA 0, last slot: see srv_trace
 };
 struct SrvDev {
     unsigned long long seq;                // re-broadcast of the mailbox
@@ -433,6 +447,12 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// Timeline of CTA 0's part of the last slot (bf_server_trace), %globaltimer ns:
+// 0 doorbell seen, 1 descriptor published, 2 first S in shared memory (split), 3 first
+// D ready (epilogue), 4 last bulk store issued, 5 stores complete, 6 counted.
+__device__ __forceinline__ void srv_trace(const SrvPtrs &sp, int i) {
+    if (blockIdx.x == 0) sp.mb->trace[i] = globaltimer();
+}
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -465,7 +485,7 @@ __device__ __forceinline__ bool srv_fill_slot(const SrvPtrs &sp, const TcJob &tm
     while (ld_acquire_sys(&sp.mb->seq) < k) {
         if ((long long)(globaltimer() - t0) > sp.timeout_ns) { stop = true; break; }
     }
-    if (blockIdx.x == 0 && !stop) sp.mb->t_seen[e] = globaltimer();
+    if (blockIdx.x == 0 && !stop) sp.mb->t_seen[e] = sp.mb->trace[0] = globaltimer();
     const volatile SrvSlotDesc *vdesc = &sp.mb->desc[e];
     const unsigned long long dS = stop ? 0ull : vdesc->S, dR = stop ? 0ull : vdesc->R;
     const long long dn = stop ? 0ll : vdesc->n;
@@ -476,12 +496,15 @@ __device__ __forceinline__ bool srv_fill_slot(const SrvPtrs &sp, const TcJob &tm
         while (ld_acquire_sys(&sp.mb->seq) < k) {
             if ((long long)(globaltimer() - t0) > sp.timeout_ns) { stop = true; break; }
         }
-        volatile SrvSlotDesc *d = &sp.mb->desc[e];
-        dv->S[e] = stop ? 0ull : d->S;
-        dv->R[e] = stop ? 0ull : d->R;
-        dv->n[e] = stop ? 0ll : d->n;
-        dv->stop[e] = stop ? 1 : d->stop;
-        if (!stop) sp.mb->t_seen[e] = globaltimer();
+        unsigned long long hS = 0, hR = 0;
+        long long hn = 0;
+        int hstop = 1;
+        if (!stop) ld_desc_sys(&sp.mb->desc[e], hS, hR, hn, hstop);   // after the acquire of seq
+        dv->S[e] = hS;
+        dv->R[e] = hR;
+        dv->n[e] = hn;
+        dv->stop[e] = stop ? 1 : hstop;
+        if (!stop) sp.mb->t_seen[e] = sp.mb->trace[0] = globaltimer();
         st_release_gpu(&dv->seq, k);
     } else {
         while (ld_acquire_gpu(&dv->seq) < k) {
@@ -513,6 +536,7 @@ __device__ __forceinline__ bool srv_fill_slot(const SrvPtrs &sp, const TcJob &tm
     cta_range(nullptr, 1, n, 0, b0, e0, g0);
     J.begin = b0;
     J.end = stop ? -1 : e0;                       // end = -1: the stop marker
+    srv_trace(sp, 1);
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(slot_full + e))
                  : "memory");
     return !stop;
@@ -650,21 +674,26 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     // then waits for it and restarts its walk on it; false on stop.
     enum { kRoleProd, kRoleSplit, kRoleMma, kRoleEpi };
     unsigned long long slot = 0;
+    bool fresh = false;                   // SRV: the first tile of a slot (timeline trace)
     auto next_tile = [&](Tile &t2, int role) -> bool {
         if constexpr (!SRV) {
             return it.next(t2);
         } else {
             for (;;) {
                 if (slot > 0 && it.next(t2)) return true;
+                fresh = true;
                 const unsigned long long u = slot / kSrvRing;     // use index of the next entry
                 if (role == kRoleEpi && slot > 0 && warp == kEpiWarp0 && lane == 0) {
                     // slot done in this CTA: its R stores complete, then count it
+                    srv_trace(p.srv, 4);
                     bulk_wait_all();
+                    srv_trace(p.srv, 5);
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                     __threadfence();
                     const int e = (int)(slot % kSrvRing);
                     if (*fix_n > 0) atomicExch(&p.srv.mb->error, 1);
                     const unsigned int old = atomicAdd(&p.srv.dev->done_cnt[e], 1u);
+                    srv_trace(p.srv, 6);
                     if (old == (unsigned)(((slot - 1) / kSrvRing + 1) * gridDim.x) - 1u) {
                         __threadfence_system();
                         p.srv.mb->t_done[e] = globaltimer();
@@ -704,6 +733,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             const bool valid = m < 120 && bsel < tl.cnt;
             const int stage = (int)(t % kRing);
             bfk::mbar_wait(bar_s_full + stage, (uint32_t)((t / kRing) & 1));
+            if (SRV && fresh) {
+                if (warp == 0 && lane == 0) srv_trace(p.srv, 2);
+                fresh = false;
+            }
             const float *Sb = Ss + (stage * 2 + (valid ? bsel : 0)) * (L::kSBlock / 4);
             // Term order S2, S3, S1 mirrors the MMA order, so each region is rewritten
             // as soon as the previous tile's MMAs on it have completed and the tensor
@@ -976,6 +1009,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             float *Rb = J.R + blk * (int64_t)(bfk::r_block_bytes(LAYOUT) / 4);
             bfk::mbar_wait(bar_d_full + b, u & 1);
             tc::fence_after_sync();
+            if (SRV && fresh) {
+                if (warp == kEpiWarp0 && lane == 0) srv_trace(p.srv, 3);
+                fresh = false;
+            }
             const uint32_t d = tmem + ((uint32_t)(q * 32) << 16) + kDCol0 + 128 * b + 64 * h;
             if constexpr (!(DBG & 2) && !kStageR && (LAYOUT == 2 || LAYOUT == 3)) {
                 // 16-bit output, direct stores (int16 output at f <= 12; see kStageR), in

@@ -266,6 +266,12 @@ class Server:
         check(lib().bf_server_slot_time(self._h, ctypes.c_uint64(ticket), ctypes.byref(v)))
         return v.value
 
+    def trace_us(self) -> list:
+        """bf_server_trace: CTA 0's timeline of the last done slot (us after its doorbell)."""
+        arr = (ctypes.c_double * 8)()
+        check(lib().bf_server_trace(self._h, arr, 8))
+        return list(arr)
+
     def stop(self) -> None:
         check(lib().bf_server_stop(self._h))
 

@@ -41,16 +41,19 @@ def main():
     srv = bf.Server(plan).start(torch.cuda.Stream(dev))
     try:
         for n in sizes:
-            d = []
+            d, tr = [], []
             for i in range(10 + a.slots):
                 S, R = bufs[n][i % nbuf]
                 t = srv.submit(S, R)
                 srv.wait(t, timeout_s=30)
                 if i >= 10:
                     d.append(srv.slot_time_us(t))
+                    tr.append(srv.trace_us())
             tiles = (n + 1) // 2
             print(json.dumps({"n": n, "tiles_per_cta": tiles / 148, "device_us_median": statistics.median(d),
-                              "device_us_min": min(d), "bytes_us_at_6.5TBps": n * 48000 / 6.5e6}), flush=True)
+                              "device_us_min": min(d), "bytes_us_at_6.5TBps": n * 48000 / 6.5e6,
+                              "cta0_trace_us_median": [statistics.median(x[j] for x in tr) for j in range(7)]}),
+                  flush=True)
     finally:
         srv.close()
 
