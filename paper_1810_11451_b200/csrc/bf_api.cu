@@ -53,6 +53,9 @@ constexpr size_t kMaxProfEvents = 1 << 16;  // timed launches kept between kerne
 // kernel).  From there on
 // the tensor kernel wins, by 2.2-2.6x at f = 36.
 constexpr int kAutoTensorMinF[4] = {2, 7, 4, 4};   // [layout]
+// bf_apply_batch: 1 = one contiguous cost range of all the launch's jobs per CTA, 0 = every
+// job split over all CTAs
+constexpr int kBatchSplit = 1;
 
 BfKernelTable g_table;      // FFMA kernels [f][layout]
 BfKernelTable g_table_tc;   // tcgen05 split-TF32 kernels [f][layout]
@@ -616,6 +619,12 @@ bf_status launch_batch(const bf_batch_job *jobs, int n, cudaStream_t st) {
         tiles += (jobs[i].n_blocks + 1) / 2;
     }
     tp.n_jobs = n;
+    // how the jobs are split over the CTAs (TcParams.split): BF_BATCH_SPLIT=0|1 for experiments
+    static const int split = [] {
+        const char *e = std::getenv("BF_BATCH_SPLIT");
+        return e ? (std::atoi(e) != 0 ? 1 : 0) : kBatchSplit;
+    }();
+    tp.split = split;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, sms_used(p0)));
     bf_status s;
     cudaEvent_t e1;

@@ -166,6 +166,8 @@ struct SrvPtrs {
 template <int NJ>
 struct TcParamsN {
     int n_jobs;
+    int split;                             // batch launches: 0 every job over all CTAs;
+                                           // 1 one contiguous cost range of all jobs per CTA
     SrvPtrs srv;                           // SRV kernels only
     TcJob job[NJ];
 };
@@ -182,7 +184,7 @@ struct TcSmem {
     static constexpr int kSBlock = 480 * FS;           // one block of S (slot stride)
     static constexpr int kJobBytes = kMaxJobs * 96;    // per-job context (JobCtx)
     static constexpr int kFixBytes = kFixCap * 8 + 16 + 2 * kMaxStages * 4;   // fix-up list
-    static constexpr int kMisc = 32 * 8 + 16 + kOffsSlots * 4 + kJobBytes + kFixBytes;
+    static constexpr int kMisc = 32 * 8 + 16 + kOffsSlots * 4 + kJobBytes + kFixBytes + kMaxJobs * 8;
     // R staging: the epilogue writes the tile's two blocks of R into shared memory in
     // their global layout and one thread stores each block with a bulk copy (full lines,
     // no partial sectors at planar row boundaries).  Shared memory, in order of
@@ -212,8 +214,9 @@ struct TcSmem {
     static constexpr int kOffJobs = kOffTmem + 16;     // JobCtx[kMaxJobs]
     static constexpr int kOffOffs = kOffJobs + kJobBytes;   // group offsets of every job
     static constexpr int kOffFix = kOffOffs + kOffsSlots * 4;   // int2 list, n, overflow, last[]
-    static constexpr int kOffR = (kOffFix + kFixBytes + 127) / 128 * 128;
-    static constexpr int kBytesUsed = kStageR ? kOffR + kRStageBytes : kOffFix + kFixBytes;
+    static constexpr int kOffJCost = kOffFix + kFixBytes;        // int64 per job (split = 1)
+    static constexpr int kOffR = (kOffJCost + kMaxJobs * 8 + 127) / 128 * 128;
+    static constexpr int kBytesUsed = kStageR ? kOffR + kRStageBytes : kOffJCost + kMaxJobs * 8;
     static constexpr int kBytes = kBytesUsed > kMinSmem ? kBytesUsed : kMinSmem;
     static_assert(kBytesUsed <= kSmemLimit, "shared memory");
 };
@@ -360,41 +363,59 @@ __device__ __forceinline__ bool block_in_domain(const JobCtx &J, int64_t blk) {
 // Pure integer function of the offsets: results do not depend on it (a D row only
 // depends on its own A row), only the timing does.
 constexpr int64_t kTileCost = 4, kWCost = 2;
+// Cost model of the contiguous split of a whole batch launch over its jobs (TcParams.split
+// = 1), in units of 480 bytes: a tile of runtime f costs its two blocks' bytes, 2 (f + 64),
+// plus ~29 units of per-tile overhead (fit of the per-f kernel times, c3 sweep); a W
+// reload (group or job change) ~200 units (the ~3 us bubble of a one-buffer W change at
+// one SM's share of the HBM bandwidth; tools/batch_exp.py).
+__host__ __device__ constexpr int64_t split_tile_cost(int f) { return 2 * (f + 64) + 29; }
+constexpr int64_t kSplitWCost = 200;
 
 // item where cost position x falls inside group g (x_in = x - cost before g)
-__device__ __forceinline__ int64_t item_at(const int32_t *offs, int g, int64_t x_in) {
-    const int64_t m = offs[g + 1] - offs[g], r = x_in - kWCost;
+__device__ __forceinline__ int64_t item_at(const int32_t *offs, int g, int64_t x_in, int64_t tc,
+                                           int64_t wc) {
+    const int64_t m = offs[g + 1] - offs[g], r = x_in - wc;
     if (r <= 0) return offs[g];
-    return offs[g] + min(m, 2 * ((r + kTileCost - 1) / kTileCost));
+    return offs[g] + min(m, 2 * ((r + tc - 1) / tc));
 }
 
-// One warp computes this CTA's [begin, end) (lanes scan 32 groups at a time).
-__device__ __forceinline__ void cta_range(const int32_t *offs, int G, int64_t n, int lane,
-                                          int64_t &begin, int64_t &end, int &g_begin) {
+// Total cost of a job (warp-wide; lanes scan 32 groups at a time).
+__device__ __forceinline__ int64_t job_cost(const int32_t *offs, int G, int64_t n, int lane,
+                                            int64_t tc, int64_t wc) {
+    if (!offs) return tc * ((n + 1) / 2);
+    int64_t tot = 0;
+    for (int base = 0; base < G; base += 32) {
+        const int g = base + lane;
+        const int64_t m = g < G ? offs[g + 1] - offs[g] : 0;
+        int64_t c = m > 0 ? wc + tc * ((m + 1) / 2) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        tot += c;
+    }
+    return tot;
+}
+
+// One warp computes the items [begin, end) of the cost range [xb, xe) of a job of total
+// cost tot (to_end: the range runs to the job's end, items with invalid tags included).
+// Positions map to items monotonically, so adjacent ranges share their boundary.
+__device__ __forceinline__ void cta_range_x(const int32_t *offs, int G, int64_t n, int lane,
+                                            int64_t tc, int64_t wc, int64_t xb, int64_t xe,
+                                            bool to_end, int64_t &begin, int64_t &end,
+                                            int &g_begin) {
     g_begin = 0;
-    const int64_t bid = blockIdx.x, grid = gridDim.x;
     if (!offs) {
-        const int64_t tot = kTileCost * ((n + 1) / 2);
-        begin = min(n, 2 * ((tot * bid / grid + kTileCost - 1) / kTileCost));
-        end = bid + 1 == grid ? n : min(n, 2 * ((tot * (bid + 1) / grid + kTileCost - 1) / kTileCost));
+        begin = min(n, 2 * ((xb + tc - 1) / tc));
+        end = to_end ? n : min(n, 2 * ((xe + tc - 1) / tc));
         return;
     }
     auto cost = [&](int g) -> int64_t {
         if (g >= G) return 0;
         const int64_t m = offs[g + 1] - offs[g];
-        return m > 0 ? kWCost + kTileCost * ((m + 1) / 2) : 0;
+        return m > 0 ? wc + tc * ((m + 1) / 2) : 0;
     };
-    int64_t tot = 0;
-    for (int base = 0; base < G; base += 32) {
-        int64_t c = cost(base + lane);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        tot += c;
-    }
-    const int64_t xb = tot * bid / grid, xe = tot * (bid + 1) / grid;
     begin = n;
     end = n;
-    bool fb = false, fe = bid + 1 == grid;
+    bool fb = false, fe = to_end;
     int64_t carry = 0;
     for (int base = 0; base < G && !(fb && fe); base += 32) {
         const int g = base + lane;
@@ -409,8 +430,8 @@ __device__ __forceinline__ void cta_range(const int32_t *offs, int G, int64_t n,
         const int64_t excl = incl - c;
         const bool hb = !fb && c > 0 && xb >= excl && xb < incl;
         const bool he = !fe && c > 0 && xe >= excl && xe < incl;
-        const int64_t ib = hb ? item_at(offs, g, xb - excl) : 0;
-        const int64_t ie = he ? item_at(offs, g, xe - excl) : 0;
+        const int64_t ib = hb ? item_at(offs, g, xb - excl, tc, wc) : 0;
+        const int64_t ie = he ? item_at(offs, g, xe - excl, tc, wc) : 0;
         const unsigned mb = __ballot_sync(0xffffffffu, hb), me = __ballot_sync(0xffffffffu, he);
         if (mb) {
             begin = __shfl_sync(0xffffffffu, ib, __ffs(mb) - 1);
@@ -420,6 +441,16 @@ __device__ __forceinline__ void cta_range(const int32_t *offs, int G, int64_t n,
         if (me) { end = __shfl_sync(0xffffffffu, ie, __ffs(me) - 1); fe = true; }
         carry = __shfl_sync(0xffffffffu, incl, 31);
     }
+}
+
+// This CTA's [begin, end) of one job split over all CTAs (cost in tiles plus half a tile
+// per group segment).
+__device__ __forceinline__ void cta_range(const int32_t *offs, int G, int64_t n, int lane,
+                                          int64_t &begin, int64_t &end, int &g_begin) {
+    const int64_t bid = blockIdx.x, grid = gridDim.x;
+    const int64_t tot = job_cost(offs, G, n, lane, kTileCost, kWCost);
+    cta_range_x(offs, G, n, lane, kTileCost, kWCost, tot * bid / grid, tot * (bid + 1) / grid,
+                bid + 1 == grid, begin, end, g_begin);
 }
 
 // Named barrier 1 over the 8 epilogue warps (256 threads).
@@ -621,14 +652,47 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             for (int i = threadIdx.x; i < jobs[jj].n_groups + 2; i += blockDim.x)
                 const_cast<int32_t *>(jobs[jj].offs)[i] = p.job[jj].offsets[i];
     __syncthreads();
-    for (int jj = warp; jj < n_jobs; jj += kThreads / 32) {
-        int64_t b0, e0;
-        int g0;
-        cta_range(jobs[jj].offs, jobs[jj].n_groups, p.job[jj].n_items, lane, b0, e0, g0);
-        if (lane == 0) {
-            jobs[jj].begin = b0;
-            jobs[jj].end = e0;
-            jobs[jj].g_begin = g0;
+    if (F == 0 && p.split == 1 && n_jobs > 1) {
+        // one contiguous range of the concatenated jobs per CTA (cost: bytes + per-tile
+        // overhead + W reloads, split_tile_cost / kSplitWCost): a CTA meets ~2 jobs per launch
+        // instead of all of them, so far fewer W reloads
+        int64_t *jcost = reinterpret_cast<int64_t *>(smem + L::kOffJCost);
+        for (int jj = warp; jj < n_jobs; jj += kThreads / 32) {
+            const int64_t c = job_cost(jobs[jj].offs, jobs[jj].n_groups, p.job[jj].n_items, lane,
+                                       split_tile_cost(jobs[jj].f), kSplitWCost);
+            if (lane == 0) jcost[jj] = c;
+        }
+        __syncthreads();
+        int64_t X = 0;
+        for (int jj = 0; jj < n_jobs; ++jj) X += jcost[jj];
+        const int64_t bid = blockIdx.x, grid = gridDim.x;
+        const int64_t Xb = X * bid / grid, Xe = bid + 1 == grid ? X : X * (bid + 1) / grid;
+        for (int jj = warp; jj < n_jobs; jj += kThreads / 32) {
+            int64_t P = 0;
+            for (int i = 0; i < jj; ++i) P += jcost[i];
+            const int64_t T = jcost[jj];
+            const int64_t xb = min(max(Xb - P, (int64_t)0), T), xe = min(max(Xe - P, (int64_t)0), T);
+            int64_t b0 = p.job[jj].n_items, e0 = b0;
+            int g0 = 0;
+            if (xb < xe || (Xe >= P + T && Xb < P + T))
+                cta_range_x(jobs[jj].offs, jobs[jj].n_groups, p.job[jj].n_items, lane,
+                            split_tile_cost(jobs[jj].f), kSplitWCost, xb, xe, Xe >= P + T, b0, e0, g0);
+            if (lane == 0) {
+                jobs[jj].begin = b0;
+                jobs[jj].end = e0;
+                jobs[jj].g_begin = g0;
+            }
+        }
+    } else {
+        for (int jj = warp; jj < n_jobs; jj += kThreads / 32) {
+            int64_t b0, e0;
+            int g0;
+            cta_range(jobs[jj].offs, jobs[jj].n_groups, p.job[jj].n_items, lane, b0, e0, g0);
+            if (lane == 0) {
+                jobs[jj].begin = b0;
+                jobs[jj].end = e0;
+                jobs[jj].g_begin = g0;
+            }
         }
     }
     __syncthreads();
