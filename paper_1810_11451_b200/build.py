@@ -20,6 +20,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "-Xptxas", "-warn-spills"]   # no --use_fast_math: FFMA fusion yes, FTZ/approx no
+FLAGS += os.environ.get("BF_NVCC_EXTRA", "").split()   # experiments only (e.g. -DBF_MBAR_SUSPEND_NS=...)
 
 LIBBF = os.path.join(PKG, "libbf.so")
 LIBSYNTH = os.path.join(ROOT, "bf_synth", "libbfsynth.so")

@@ -49,6 +49,7 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "bf_ffma.cuh"
@@ -71,6 +72,15 @@ constexpr int kDCol0 = 256;
 constexpr int kMinSmem = 120 * 1024;   // forces one CTA (and one TMEM owner) per SM
 #ifndef BFTC_EARLY_RELEASE
 #define BFTC_EARLY_RELEASE 0
+#endif
+// Experiments only: the runtime-f kernel with a compile-time f in some roles
+// (BFTC_FIXF_ROLES bits: 1 split warps, 2 producer, 4 MMA issuer).  Results are wrong
+// for any other f.
+#ifndef BFTC_FIXF
+#define BFTC_FIXF 0
+#endif
+#ifndef BFTC_FIXF_ROLES
+#define BFTC_FIXF_ROLES 0
 #endif
 // split warps release an S ring slot as soon as their values are in registers (1), or
 // after the tile's last split pass (0)
@@ -792,8 +802,9 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         int cur_wf = 0;                                  // wexact flags of the current group
         for (int64_t t = 0; next_tile(tl, kRoleSplit); ++t) {
             const JobCtx &J = it.jobs[tl.job];
-            const int f = F > 0 ? F : J.f;
-            const int KP = F > 0 ? L::KP : J.kp;
+            constexpr int FXs = (BFTC_FIXF_ROLES & 1) ? BFTC_FIXF : 0;
+            const int f = F > 0 ? F : (FXs ? FXs : J.f);
+            const int KP = F > 0 ? L::KP : (FXs ? kp_of(FXs) : J.kp);
             const bool valid = m < 120 && bsel < tl.cnt;
             const int stage = (int)(t % kRing);
             bfk::mbar_wait(bar_s_full + stage, (uint32_t)((t / kRing) & 1));
@@ -812,100 +823,127 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 cur_j = tl.job;
                 cur_wf = __ldg(J.wexact + tl.g);
             }
-            // This warp's K chunks of the thread's row of S (half of them above f = 12) are
-            // read from the ring once into registers and the slot is released at once; the
-            // term passes split from registers.
-            constexpr int kSlots = (F > 0 && F <= 12) ? L::KP / 8 : ((L::KP / 8 + 1) >> 1);
-            const int c_half0 = (F > 0 && F <= 12) ? KP : ((KP / 8 + 1) >> 1) * 8;
-            const int c_beg0 = ks ? c_half0 : 0, c_end0 = ks ? KP : c_half0;
-            float xs[kSlots * 8];
-            // tensor domain check of every value read, kept in a predicate
-            bool out_dom = false;
-#pragma unroll
-            for (int i = 0; i < kSlots; ++i) {
-                const int c0 = c_beg0 + 8 * i;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int k = c0 / 2 + q;
-                    float re = 0.0f, im = 0.0f;
-                    if (c0 < c_end0 && k < f && valid) {
-                        if (LAYOUT != 1) {
-                            const float2 v = reinterpret_cast<const float2 *>(Sb)[k * 60 + j];
-                            re = v.x;
-                            im = v.y;
+            // The rest of the tile runs with a compile-time K extent: the per-f kernels pass
+            // their own, the runtime-f batch kernel dispatches on the job's KP (9 classes), so
+            // its loops and registers are sized per class instead of for f = 36.
+            auto split_tile = [&](auto kp_const) {
+                // KPc = 0: runtime K extent (register arrays sized for K = 72, halves split)
+                constexpr int KPs = decltype(kp_const)::value;
+                constexpr int KPm = KPs ? KPs : 72;
+                const int KPc = KPs ? KPs : KP;
+                // This warp's K chunks of the thread's row of S (half of them above f = 12) are
+                // read from the ring once into registers and the slot is released at once; the
+                // term passes split from registers.
+                constexpr int kSlots = KPm <= 24 ? KPm / 8 : ((KPm / 8 + 1) >> 1);
+                const int c_half0 = KPm <= 24 ? KPc : ((KPc / 8 + 1) >> 1) * 8;
+                const int c_beg0 = ks ? c_half0 : 0, c_end0 = ks ? KPc : c_half0;
+                float xs[kSlots * 8];
+                // tensor domain check of every value read, kept in a predicate
+                bool out_dom = false;
+    #pragma unroll
+                for (int i = 0; i < kSlots; ++i) {
+                    const int c0 = c_beg0 + 8 * i;
+    #pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int k = c0 / 2 + q;
+                        float re = 0.0f, im = 0.0f;
+                        // (with a compile-time K extent only the last chunk can pass f)
+                        if (c0 < c_end0 && ((KPs > 0 && c0 + 8 < KPs) || k < f) && valid) {
+                            if (LAYOUT != 1) {
+                                const float2 v = reinterpret_cast<const float2 *>(Sb)[k * 60 + j];
+                                re = v.x;
+                                im = v.y;
+                            } else {
+                                re = Sb[k * 60 + j];
+                                im = Sb[f * 60 + k * 60 + j];
+                            }
+                        }
+                        xs[8 * i + 2 * q] = re;
+                        xs[8 * i + 2 * q + 1] = im;
+                        const uint32_t ur = __float_as_uint(re) & 0x7FFFFFFFu, ui = __float_as_uint(im) & 0x7FFFFFFFu;
+                        out_dom |= (ur - kDomLo >= kDomHi - kDomLo && ur != 0u) |
+                                   (ui - kDomLo >= kDomHi - kDomLo && ui != 0u);
+                    }
+                }
+                if (valid && ((cur_wf & 2) || out_dom)) {
+                    // rare: list the block once per tile (the first thread to see it wins; a
+                    // stage's slot is reused only after every split warp finished this tile)
+                    const int key = (int)(t + 1);
+                    if (atomicMax(fix_last + 2 * stage + bsel, key) < key) {
+                        const int idx = atomicAdd(fix_n, 1);
+                        if (idx < kFixCap)
+                            fix_list[idx] = make_int2((int)(it.item - tl.cnt + bsel), (it.j << 16) | cur_g);
+                        else
+                            atomicExch(fix_over, 1);
+                    }
+                }
+                if (kEarlyRelease) mbar_arrive(bar_s_empty + stage);    // values are in registers
+    #pragma unroll
+                for (int pass = 0; pass < 3; ++pass) {
+                    const int term = pass == 2 ? 0 : pass + 1;
+                    bfk::mbar_wait(bar_a_free + term, par);
+                    tc::fence_after_sync();
+                    if (term == 2 && !(cur_wf & 1)) {   // S3 is only multiplied for tf32-exact W
+                        tc::fence_before_sync();
+                        mbar_arrive(bar_a_full + term);
+                        continue;
+                    }
+                    // DBG 32: S1 as fp16 pairs over K rounded up to 16 (one more chunk at f = 36)
+                    const int kend = ((DBG & 32) && term == 0) ? (KPc + 15) / 16 * 16 : KPc;
+                    // this warp's K chunks; at f <= 12 (<= 3 chunks) the second warp of each
+                    // quarter only keeps the barrier counts (splitting measured slower there)
+                    const int c_half = KPm <= 24 ? kend : ((kend / 8 + 1) >> 1) * 8;
+                    const int c_beg = ks ? c_half : 0, c_end = ks ? kend : c_half;
+    #pragma unroll
+                    for (int i = 0; i < kSlots; ++i) {
+                        const int c0 = c_beg + 8 * i;
+                        if (c0 >= c_end) break;
+                        float x[8];
+    #pragma unroll
+                        for (int e = 0; e < 8; ++e) x[e] = xs[8 * i + e];
+                        uint32_t v[8];
+    #pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            // exact 3-term split, each term rounded to 11 significant
+                            // bits (integer add + mask, 2 ops): x = x1 + x2 + x3 exactly,
+                            // |x - x1| <= 2^-11 |x|, |x3| <= 2^-22 |x|.
+                            const float x1 = tc::tf32_round(x[e]);
+                            const float r1 = x[e] - x1;          // exact
+                            const float x2 = tc::tf32_round(r1);
+                            const float x3 = r1 - x2;            // exact, fits tf32
+                            v[e] = __float_as_uint(term == 0 ? x1 : (term == 1 ? x2 : x3));
+                        }
+                        if ((DBG & 32) && term == 0) {
+                            uint32_t h[4];
+    #pragma unroll
+                            for (int e = 0; e < 4; ++e)
+                                h[e] = bfk::pack_half2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+                            if constexpr (!(DBG & 4)) tc::tmem_st4(a_lane + c0 / 2, h);
                         } else {
-                            re = Sb[k * 60 + j];
-                            im = Sb[f * 60 + k * 60 + j];
+                            if constexpr (!(DBG & 4)) tc::tmem_st8(a_lane + term * kARegion + c0, v);
                         }
                     }
-                    xs[8 * i + 2 * q] = re;
-                    xs[8 * i + 2 * q + 1] = im;
-                    const uint32_t ur = __float_as_uint(re) & 0x7FFFFFFFu, ui = __float_as_uint(im) & 0x7FFFFFFFu;
-                    out_dom |= (ur - kDomLo >= kDomHi - kDomLo && ur != 0u) |
-                               (ui - kDomLo >= kDomHi - kDomLo && ui != 0u);
-                }
-            }
-            if (valid && ((cur_wf & 2) || out_dom)) {
-                // rare: list the block once per tile (the first thread to see it wins; a
-                // stage's slot is reused only after every split warp finished this tile)
-                const int key = (int)(t + 1);
-                if (atomicMax(fix_last + 2 * stage + bsel, key) < key) {
-                    const int idx = atomicAdd(fix_n, 1);
-                    if (idx < kFixCap)
-                        fix_list[idx] = make_int2((int)(it.item - tl.cnt + bsel), (it.j << 16) | cur_g);
-                    else
-                        atomicExch(fix_over, 1);
-                }
-            }
-            if (kEarlyRelease) mbar_arrive(bar_s_empty + stage);    // values are in registers
-#pragma unroll
-            for (int pass = 0; pass < 3; ++pass) {
-                const int term = pass == 2 ? 0 : pass + 1;
-                bfk::mbar_wait(bar_a_free + term, par);
-                tc::fence_after_sync();
-                if (term == 2 && !(cur_wf & 1)) {   // S3 is only multiplied for tf32-exact W
+                    tc::tmem_st_wait();
                     tc::fence_before_sync();
                     mbar_arrive(bar_a_full + term);
-                    continue;
                 }
-                // DBG 32: S1 as fp16 pairs over K rounded up to 16 (one more chunk at f = 36)
-                const int kend = ((DBG & 32) && term == 0) ? (KP + 15) / 16 * 16 : KP;
-                // this warp's K chunks; at f <= 12 (<= 3 chunks) the second warp of each
-                // quarter only keeps the barrier counts (splitting measured slower there)
-                const int c_half = (F > 0 && F <= 12) ? kend : ((kend / 8 + 1) >> 1) * 8;
-                const int c_beg = ks ? c_half : 0, c_end = ks ? kend : c_half;
-#pragma unroll
-                for (int i = 0; i < kSlots; ++i) {
-                    const int c0 = c_beg + 8 * i;
-                    if (c0 >= c_end) break;
-                    float x[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) x[e] = xs[8 * i + e];
-                    uint32_t v[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        // exact 3-term split, each term rounded to 11 significant
-                        // bits (integer add + mask, 2 ops): x = x1 + x2 + x3 exactly,
-                        // |x - x1| <= 2^-11 |x|, |x3| <= 2^-22 |x|.
-                        const float x1 = tc::tf32_round(x[e]);
-                        const float r1 = x[e] - x1;          // exact
-                        const float x2 = tc::tf32_round(r1);
-                        const float x3 = r1 - x2;            // exact, fits tf32
-                        v[e] = __float_as_uint(term == 0 ? x1 : (term == 1 ? x2 : x3));
-                    }
-                    if ((DBG & 32) && term == 0) {
-                        uint32_t h[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e)
-                            h[e] = bfk::pack_half2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
-                        if constexpr (!(DBG & 4)) tc::tmem_st4(a_lane + c0 / 2, h);
-                    } else {
-                        if constexpr (!(DBG & 4)) tc::tmem_st8(a_lane + term * kARegion + c0, v);
-                    }
+            };
+            if constexpr (F > 0) {
+                split_tile(std::integral_constant<int, L::KP>{});
+            } else if constexpr (FXs > 0) {
+                split_tile(std::integral_constant<int, kp_of(FXs)>{});
+            } else {
+                switch (KP) {
+                    case 8: split_tile(std::integral_constant<int, 8>{}); break;
+                    case 16: split_tile(std::integral_constant<int, 16>{}); break;
+                    case 24: split_tile(std::integral_constant<int, 24>{}); break;
+                    case 32: split_tile(std::integral_constant<int, 32>{}); break;
+                    case 40: split_tile(std::integral_constant<int, 40>{}); break;
+                    case 48: split_tile(std::integral_constant<int, 48>{}); break;
+                    case 56: split_tile(std::integral_constant<int, 56>{}); break;
+                    case 64: split_tile(std::integral_constant<int, 64>{}); break;
+                    default: split_tile(std::integral_constant<int, 72>{}); break;
                 }
-                tc::tmem_st_wait();
-                tc::fence_before_sync();
-                mbar_arrive(bar_a_full + term);
             }
             if (!kEarlyRelease) mbar_arrive(bar_s_empty + stage);   // ring slot may be refilled
         }
@@ -932,7 +970,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 nb1 = have_nx && nx.cnt > 1 ? block_of(jobs[nx.job], nx.item + 1) : 0;
             }
             const JobCtx &J = *Jp;
-            const int f = F > 0 ? F : J.f;
+            constexpr int FXp = (BFTC_FIXF_ROLES & 2) ? BFTC_FIXF : 0;
+            const int f = F > 0 ? F : (FXp ? FXp : J.f);
             const int stage = (int)(t % kRing);
             // S of this tile first: at a group change with one W buffer the producer then
             // waits for the previous group's MMAs to drain (wfree), and the S load's HBM
@@ -990,7 +1029,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         bool exact = false;
         for (int64_t t = 0; next_tile(tl, kRoleMma); ++t) {
             const JobCtx &J = it.jobs[tl.job];
-            const int KP = F > 0 ? L::KP : J.kp;
+            constexpr int FXm = (BFTC_FIXF_ROLES & 4) ? BFTC_FIXF : 0;
+            const int KP = F > 0 ? L::KP : (FXm ? kp_of(FXm) : J.kp);
             if (tl.g != cur_g || tl.job != cur_j) {   // new group segment: W prefetched by the producer
                 exact = (__ldg(J.wexact + tl.g) & 1) != 0;
                 // the previous segment's buffer is free once every MMA issued so far completed
@@ -1013,35 +1053,58 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             //   general W: S2 W1, S1 W2, S1 W1 (the S3 region is not used) — 3 KP/8 MMAs
             //   (DESIGN.md §7).  The middle group of general W reads the S1 region.
             // Each split term's TMEM region is released by a commit once read.
-#pragma unroll
-            for (int grp = 0; grp < 3; ++grp) {
-                const int at = grp == 0 ? 1 : (grp == 1 ? 2 : 0);   // barrier: S2, S3, S1
-                bfk::mbar_wait(bar_a_full + at, (uint32_t)(t & 1));
-                const bool s1w2 = grp == 1 && !exact;
-                if (s1w2) bfk::mbar_wait(bar_a_full + 0, (uint32_t)(t & 1));
-                tc::fence_after_sync();
-                const int areg = s1w2 ? 0 : at;                     // A region read
-                const uint32_t boff = s1w2 ? (uint32_t)(KP / 4) : 0u;  // W2 image after W1
-                if (lane == 0) {
-                    // DBG & 16 (energy experiment): the S1 W1 group as ceil(KP / 16)
-                    // fp16-kind K = 16 MMAs on the same (reinterpreted) operands
-                    const int nkb = ((DBG & 16) && grp == 2) ? (KP + 15) / 16 : KP / 8;
-#pragma unroll
-                    for (int kb = 0; kb < nkb; ++kb) {
-                        const uint64_t desc = tc::smem_desc(
-                            w_base + (uint32_t)((boff + 2 * kb) * 16 * 128), 16 * 128, 128);
-                        if constexpr (!(DBG & 1)) {
-                            if ((DBG & 16) && grp == 2)
-                                tc::mma_bf16_ts(d, tmem + areg * kARegion + kb * 8, desc,
-                                                idesc_c & ~((7u << 7) | (7u << 10)), kb != 0);
-                            else
-                                tc::mma_tf32_ts(d, tmem + areg * kARegion + kb * 8, desc, idesc,
-                                                (grp | kb) != 0);
+            // The K extent is a compile-time constant in the issue loop (the runtime-f
+            // kernel dispatches on the job's KP): descriptors then come precomputed and an
+            // MMA issues in ~10 instructions instead of ~16 (runtime loop: -8 % at f = 35).
+            auto mma_groups = [&](auto kp_const) {
+                constexpr int KPc = decltype(kp_const)::value;
+    #pragma unroll
+                for (int grp = 0; grp < 3; ++grp) {
+                    const int at = grp == 0 ? 1 : (grp == 1 ? 2 : 0);   // barrier: S2, S3, S1
+                    bfk::mbar_wait(bar_a_full + at, (uint32_t)(t & 1));
+                    const bool s1w2 = grp == 1 && !exact;
+                    if (s1w2) bfk::mbar_wait(bar_a_full + 0, (uint32_t)(t & 1));
+                    tc::fence_after_sync();
+                    const int areg = s1w2 ? 0 : at;                     // A region read
+                    const uint32_t boff = s1w2 ? (uint32_t)(KPc / 4) : 0u;  // W2 image after W1
+                    if (lane == 0) {
+                        // DBG & 16 (energy experiment): the S1 W1 group as ceil(KP / 16)
+                        // fp16-kind K = 16 MMAs on the same (reinterpreted) operands
+                        const int nkb = ((DBG & 16) && grp == 2) ? (KPc + 15) / 16 : KPc / 8;
+    #pragma unroll
+                        for (int kb = 0; kb < nkb; ++kb) {
+                            const uint64_t desc = tc::smem_desc(
+                                w_base + (uint32_t)((boff + 2 * kb) * 16 * 128), 16 * 128, 128);
+                            if constexpr (!(DBG & 1)) {
+                                if ((DBG & 16) && grp == 2)
+                                    tc::mma_bf16_ts(d, tmem + areg * kARegion + kb * 8, desc,
+                                                    idesc_c & ~((7u << 7) | (7u << 10)), kb != 0);
+                                else
+                                    tc::mma_tf32_ts(d, tmem + areg * kARegion + kb * 8, desc, idesc,
+                                                    (grp | kb) != 0);
+                            }
                         }
+                        if (grp < 2) tc::mma_commit(bar_a_free + at);
                     }
-                    if (grp < 2) tc::mma_commit(bar_a_free + at);
+                    __syncwarp();
                 }
-                __syncwarp();
+            };
+            if constexpr (F > 0) {
+                mma_groups(std::integral_constant<int, L::KP>{});
+            } else if constexpr (FXm > 0) {
+                mma_groups(std::integral_constant<int, kp_of(FXm)>{});
+            } else {
+                switch (KP) {
+                    case 8: mma_groups(std::integral_constant<int, 8>{}); break;
+                    case 16: mma_groups(std::integral_constant<int, 16>{}); break;
+                    case 24: mma_groups(std::integral_constant<int, 24>{}); break;
+                    case 32: mma_groups(std::integral_constant<int, 32>{}); break;
+                    case 40: mma_groups(std::integral_constant<int, 40>{}); break;
+                    case 48: mma_groups(std::integral_constant<int, 48>{}); break;
+                    case 56: mma_groups(std::integral_constant<int, 56>{}); break;
+                    case 64: mma_groups(std::integral_constant<int, 64>{}); break;
+                    default: mma_groups(std::integral_constant<int, 72>{}); break;
+                }
             }
             if (lane == 0) {
                 tc::mma_commit(bar_a_free + 0);

@@ -27,6 +27,7 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():   # pragma: no cover
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
+import paper_1810_11451_b200 as bf  # noqa: E402
 from paper_1810_11451_b200 import Layout, Plan, Variant  # noqa: E402
 
 DEV = torch.device("cuda", 0)
@@ -272,3 +273,32 @@ def test_out_of_domain_precoders(value):
     if np.isfinite(value):
         R_ref, T, _ = oracle.beamform(W, S, tags, n_threads=NT)
         assert_parity(Rt, R_ref, T, what="out-of-domain precoders")
+
+
+def test_out_of_domain_blocks_in_a_batch():
+    """bf_apply_batch over jobs of different f, some holding out-of-domain blocks: each job's
+    result equals its own FFMA-variant apply bitwise on the fixed-up blocks and its own
+    tensor apply elsewhere (the batch kernel's fix-up uses the job's own precoders)."""
+    jobs, refs = [], []
+    for i, f in enumerate((3, 17, 36)):
+        n, G = 257 + 31 * i, 3
+        S, bad = extreme_blocks(f, n, 40 + f)
+        W = syn.precoders(50 + i, f, G, 64, f, "unit_columns")
+        tags = syn.subband_tags(50 + i, np.arange(n), G)
+        p = Plan(f=f, variant=Variant.TENSOR)
+        p.set_precoders(torch.from_numpy(W).to(DEV))
+        Sd = torch.from_numpy(np.ascontiguousarray(S)).to(DEV)
+        perm, offs = p.route(torch.from_numpy(tags).to(DEV))
+        R = torch.empty(p.r_shape(n), dtype=p.r_dtype, device=DEV)
+        jobs.append((p, Sd, perm, offs, R))
+        Rf, _ = run(W, S, tags, Variant.FFMA)
+        Rt, _ = run(W, S, tags, Variant.TENSOR)
+        refs.append((Rf, Rt, np.array(sorted(bad))))
+    bf.apply_batch(jobs)
+    torch.cuda.synchronize()
+    for (p, Sd, perm, offs, R), (Rf, Rt, badi) in zip(jobs, refs):
+        got = R.cpu().numpy()
+        assert_bitwise(got[badi], Rf[badi], f"f={p.f}: fixed-up blocks == FFMA kernel")
+        good = np.setdiff1d(np.arange(len(got)), badi)
+        assert_bitwise(got[good], Rt[good], f"f={p.f}: other blocks == tensor apply")
+        p.close()

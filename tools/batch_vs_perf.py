@@ -18,10 +18,17 @@ import paper_1810_11451_b200 as bf  # noqa: E402
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--f", type=int, nargs="*", default=[5, 7, 15, 19, 24, 32, 35])
+    ap.add_argument("--modes", nargs="*", default=["per_f", "batch"])
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--repeat", type=int, default=1, help="timings per mode (noise check)")
+    a = ap.parse_args()
     dev = torch.device("cuda", 0)
     hbm = benchkit.measured_peaks()["hbm_gbs"]
     n = 65536
-    for f in (5, 7, 15, 19, 24, 32, 35):
+    for f in a.f:
         W = syn.precoders(1, f, 1, 64, f, "none")
         p = bf.Plan(f=f, variant=bf.Variant.TENSOR)
         p.set_precoders(torch.from_numpy(W).to(dev))
@@ -29,7 +36,7 @@ def main():
         sync.gen_symbols(S, 1, 0, f, 60, 64, first=0)
         R = torch.empty((n, 64, 60), dtype=torch.complex64, device=dev)
         res = {"f": f}
-        for mode in ("per_f", "batch"):
+        for mode in [m for _ in range(a.repeat) for m in a.modes]:
             run = (lambda: p.apply(S, out=R)) if mode == "per_f" else \
                 (lambda: bf.apply_batch([(p, S, None, None, R)]))
             for _ in range(3):
@@ -37,12 +44,16 @@ def main():
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            for _ in range(20):
+            for _ in range(a.reps):
                 run()
             e1.record()
             torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / 20
-            res[mode + "_frac"] = n * 480 * (f + 64) / (ms * 1e-3) / 1e9 / hbm
+            ms = e0.elapsed_time(e1) / a.reps
+            frac = n * 480 * (f + 64) / (ms * 1e-3) / 1e9 / hbm
+            if a.repeat > 1:
+                res.setdefault(mode + "_frac", []).append(round(frac, 4))
+            else:
+                res[mode + "_frac"] = frac
         print(json.dumps(res), flush=True)
         p.close()
 
