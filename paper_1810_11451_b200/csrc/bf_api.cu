@@ -5,6 +5,7 @@
 // instantiation (a4+a5+a7), the f = 0 path (a8), and the host-buffer pipeline
 // used for end-to-end measurement.  PAPER.md:84-86 defines the operation.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -106,64 +107,70 @@ __global__ void bf_relayout_w(const float *__restrict__ W, int n_groups, int F, 
 
 // Builds the pre-split B image of one or more groups (bf_set_precoders):
 // img[g][t][kc][ng][r][e] = term t of B'[n = 8 ng + r][kk = 4 kc + e], t = 0: W1, 1: W2.
-__global__ void bf_tc_build_wimg(const float *__restrict__ W, int n_groups, int F, int layout,
-                                 float *__restrict__ img) {
-    // Per group: [W1 tf32 core matrices: KP/4 K-chunks x 16 row groups x 8 rows x 4]
-    //            [W2, the same layout]
-    // with B'[n][kk] the real embedding (n = 2i + c_out, kk = 2k + c_in),
-    // W1 = tf32(B'), W2 = tf32(B' - W1) (both round to nearest; B' = W1 + W2 + W3 with
-    // |W3| <= 2^-22 |B'|).
+__global__ void bf_tc_build_wimg(const float *__restrict__ W, int F, int layout,
+                                 uint32_t *__restrict__ img, int32_t *__restrict__ wflags) {
+    // One CTA per group.  Image: [W1 fp16 core matrices: KP/8 K-chunks x 16 row groups x
+    // 8 rows x 8 halves] then [W2, the same layout], with B'[n][kk] the real embedding
+    // (n = 2i + c_out, kk = 2k + c_in) of W scaled by 2^tau, tau placing the group's largest
+    // component in [2^14, 2^15); W1 = tf32(B'), W2 = tf32(B' - W1) (round to nearest, ties
+    // away), each rounded to fp16 (exact in fp16's normal range; B' = W1 + W2 + W3 with
+    // |W3| <= 2^-22 |B'|).  Flags: bit 0 = the group is exact in one fp16
+    // term (W2 == 0 and W1 exact: identity, selection, small integers — the kernel then
+    // multiplies S3 instead of W2); bit 1 = outside the tensor domain (an entry not 0 and
+    // not in [2^-40, 2^40), NaN, Inf, or a nonzero element, max(|re|, |im|), more than
+    // kRelRange binades below the largest component); bits 8-15 = tau + 128.
+    const int g = blockIdx.x;
     const int KP = bftc::kp_of(F);
-    const int64_t half = (int64_t)KP * 128;            // 32-bit words per part
-    const int64_t per_group = 2 * half;
-    const int64_t total = (int64_t)n_groups * per_group;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t g = idx / per_group;
-        const int rem = (int)(idx - g * per_group);
-        const int part = rem < half ? 0 : 1;
-        const int w = rem - part * (int)half;
-        const int kc = w / 512, r2 = w % 512;
-        const int ng = r2 / 32, r = (r2 / 4) % 8, e = r2 % 4;
-        const int n = ng * 8 + r, kk = kc * 4 + e;
-        const int i = n >> 1, cout = n & 1, k = kk >> 1, cin = kk & 1;
-        float v = 0.0f;
-        if (k < F) {
-            float wr, wi;
-            if (layout != BF_LAYOUT_PLANAR) {
-                wr = W[((g * 64 + i) * F + k) * 2];
-                wi = W[((g * 64 + i) * F + k) * 2 + 1];
-            } else {
-                wr = W[(g * 2 + 0) * 64 * F + i * F + k];
-                wi = W[(g * 2 + 1) * 64 * F + i * F + k];
-            }
-            // B'[2i][2k] = wr, B'[2i][2k+1] = -wi, B'[2i+1][2k] = wi, B'[2i+1][2k+1] = wr
-            v = cout == 0 ? (cin == 0 ? wr : -wi) : (cin == 0 ? wi : wr);
-        }
-        const float w1 = tc::to_tf32(v);
-        img[idx] = part == 0 ? w1 : tc::to_tf32(v - w1);
+    __shared__ int s_emax;
+    if (threadIdx.x == 0) s_emax = 0;
+    __syncthreads();
+    const uint32_t *wg = reinterpret_cast<const uint32_t *>(W) + (int64_t)g * 128 * F;
+    auto comp = [&](int i, int k, int c) -> uint32_t {   // bits of Wr (c = 0) / Wi (c = 1)
+        return layout != BF_LAYOUT_PLANAR ? wg[(i * F + k) * 2 + c] : wg[c * 64 * F + i * F + k];
+    };
+    int emax = 0, bad = 0;
+    for (int e = threadIdx.x; e < 64 * F; e += blockDim.x) {
+        const uint32_t ur = comp(e / F, e % F, 0) & 0x7FFFFFFFu, ui = comp(e / F, e % F, 1) & 0x7FFFFFFFu;
+        bad |= !(ur == 0u || (ur >= bftc::kDomLo && ur < bftc::kDomHi));
+        bad |= !(ui == 0u || (ui >= bftc::kDomLo && ui < bftc::kDomHi));
+        emax = max(emax, (int)(max(ur, ui) >> 23));
     }
-}
-
-// Per-group flags (one CTA per group): bit 0 = W exactly tf32 (its W2 image is all zero:
-// the tensor kernel then multiplies S3 instead of W2 and copy-like W is bit-exact);
-// bit 1 = some entry outside the tensor domain (nonzero |w| < 2^-40, |w| >= 2^40, NaN,
-// Inf): those groups' blocks are recomputed by the kernel's fix-up.
-__global__ void bf_tc_wflags(const float *__restrict__ W, const float *__restrict__ img, int F,
-                             int KP, int32_t *__restrict__ wflags) {
-    const int64_t per_group = 2LL * KP * 128;
-    const float *w2 = img + blockIdx.x * per_group + per_group / 2;
-    int nz = 0, bad = 0;
-    for (int i = threadIdx.x; i < KP * 128; i += blockDim.x)
-        nz |= (__float_as_uint(w2[i]) & 0x7FFFFFFFu) != 0u;
-    const uint32_t *wg = reinterpret_cast<const uint32_t *>(W) + (int64_t)blockIdx.x * 128 * F;
-    for (int i = threadIdx.x; i < 128 * F; i += blockDim.x) {   // the group's 64 x F complex
-        const uint32_t u = wg[i] & 0x7FFFFFFFu;
-        bad |= !(u == 0u || (u >= bftc::kDomLo && u < bftc::kDomHi));
+    atomicMax(&s_emax, emax);
+    __syncthreads();
+    emax = s_emax;
+    const uint32_t lo = (uint32_t)(emax - bftc::kRelRange) << 23;
+    for (int e = threadIdx.x; e < 64 * F; e += blockDim.x) {
+        const uint32_t ur = comp(e / F, e % F, 0) & 0x7FFFFFFFu, ui = comp(e / F, e % F, 1) & 0x7FFFFFFFu;
+        bad |= emax != 0 && max(ur, ui) - 1u < lo - 1u;
     }
-    nz = __syncthreads_or(nz);
     bad = __syncthreads_or(bad);
-    if (threadIdx.x == 0) wflags[blockIdx.x] = (nz ? 0 : 1) | (bad ? 2 : 0);
+    const int tau = emax != 0 && !bad ? 141 - emax : 0;
+    const float sc = __uint_as_float((uint32_t)(127 + tau) << 23);
+    const int half_words = KP * 64;                       // 32-bit words per part
+    uint32_t *out = img + (int64_t)g * 2 * half_words;
+    int inexact = 0;
+    for (int w = threadIdx.x; w < half_words; w += blockDim.x) {
+        const int kc = w / 512, r2 = w % 512;
+        const int ng = r2 / 32, r = (r2 / 4) % 8, e2 = r2 % 4;
+        const int n = ng * 8 + r, i = n >> 1, cout = n & 1;
+        float t1[2], t2[2];
+        for (int h = 0; h < 2; ++h) {
+            const int kk = kc * 8 + 2 * e2 + h, k = kk >> 1, cin = kk & 1;
+            float v = 0.0f;
+            if (k < F && !bad) {
+                const float wr = __uint_as_float(comp(i, k, 0)), wi = __uint_as_float(comp(i, k, 1));
+                // B'[2i][2k] = wr, B'[2i][2k+1] = -wi, B'[2i+1][2k] = wi, B'[2i+1][2k+1] = wr
+                v = (cout == 0 ? (cin == 0 ? wr : -wi) : (cin == 0 ? wi : wr)) * sc;
+            }
+            t1[h] = tc::to_tf32(v);
+            t2[h] = tc::to_tf32(v - t1[h]);
+            inexact |= t2[h] != 0.0f || __half2float(__float2half_rn(t1[h])) != t1[h];
+        }
+        out[w] = tc::pack_f16x2(t1[0], t1[1]);
+        out[half_words + w] = tc::pack_f16x2(t2[0], t2[1]);
+    }
+    inexact = __syncthreads_or(inexact);
+    if (threadIdx.x == 0) wflags[g] = (inexact ? 0 : 1) | (bad ? 2 : 0) | ((tau + 128) << 8);
 }
 
 // a8 with tags (f = 0): +0.0 for every block whose tag is in [0, G); blocks with other
@@ -803,15 +810,12 @@ bf_status bf_set_precoders(bf_plan_t p, const void *W_dev, int n_groups, void *s
         bf_relayout_w<<<blocks, 256, 0, st>>>(static_cast<const float *>(W_dev), n_groups, p->f,
                                               p->layout, p->Wp);
         if ((s = launched(p, "bf_relayout_w launch")) != BF_OK) return s;
-        const int64_t img = (int64_t)n_groups * 2 * bftc::kp_of(p->f) * 128;
+        const int64_t img = (int64_t)n_groups * bftc::kp_of(p->f) * 128;   // 32-bit words
         if ((s = grow(&p->Wimg, &p->Wimg_cap, img, "tensor-core precoders")) != BF_OK) return s;
-        bf_tc_build_wimg<<<(int)std::min<int64_t>((img + 255) / 256, 4096), 256, 0, st>>>(
-            static_cast<const float *>(W_dev), n_groups, p->f, p->layout, p->Wimg);
-        if ((s = launched(p, "bf_tc_build_wimg launch")) != BF_OK) return s;
         if ((s = grow(&p->wexact, &p->wexact_cap, n_groups, "precoder flags")) != BF_OK) return s;
-        bf_tc_wflags<<<n_groups, 256, 0, st>>>(static_cast<const float *>(W_dev), p->Wimg, p->f,
-                                              bftc::kp_of(p->f), p->wexact);
-        if ((s = launched(p, "bf_tc_wflags launch")) != BF_OK) return s;
+        bf_tc_build_wimg<<<n_groups, 256, 0, st>>>(static_cast<const float *>(W_dev), p->f, p->layout,
+                                                  reinterpret_cast<uint32_t *>(p->Wimg), p->wexact);
+        if ((s = launched(p, "bf_tc_build_wimg launch")) != BF_OK) return s;
         // the one synchronisation of the call: AUTO's kernel choice depends on whether
         // every group lies inside the tensor domain
         std::vector<int32_t> flags(n_groups);

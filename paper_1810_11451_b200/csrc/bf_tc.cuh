@@ -86,7 +86,13 @@ constexpr int kMinSmem = 120 * 1024;   // forces one CTA (and one TMEM owner) pe
 // after the tile's last split pass (0)
 constexpr bool kEarlyRelease = BFTC_EARLY_RELEASE != 0;
 
-__host__ __device__ constexpr int kp_of(int F) { return (2 * F + 7) / 8 * 8; }
+// K extent of the real embedding (2F), padded to the K = 16 of a kind::f16 MMA.
+__host__ __device__ constexpr int kp_of(int F) { return (2 * F + 15) / 16 * 16; }
+// Relative range of the f16 path: the operands of a row of S (a group of
+// W) are scaled by 2^e so their largest component lies in [2^14, 2^15); every nonzero
+// element (the larger of |re|, |im|) must then be >= 1, i.e. within 2^14 of the largest
+// (exponent fields: e(elem) >= e(max) - kRelRange).
+constexpr int kRelRange = 14;
 
 // One apply of a plan: blocks [0, n_items) of S -> R with the plan's precoders.
 // A launch processes a list of jobs (bf_apply: one; bf_apply_batch: up to
@@ -102,14 +108,16 @@ constexpr int kFixCap = 64;            // out-of-domain blocks a CTA lists (more
 constexpr uint32_t kDomLo = 0x2B800000u, kDomHi = 0x53800000u;
 
 struct TcJob {
-    const float *Wimg;        // [n_groups][2][KP/4][16][8][4] floats (pre-split B image)
-    // Wimg per group: [W1 as tf32 core matrices (KP/4 K-chunks)] then [W2, same layout]
+    const float *Wimg;        // [n_groups][2][KP/8][16][8][8] fp16 (pre-split B image)
+    // Wimg per group: [W1 as fp16 core matrices (KP/8 K-chunks of 8)] then [W2, same
+    // layout], both of W scaled by 2^tau (tau in wexact bits 8-15)
     const float4 *Wp;         // FFMA image of the same precoders (out-of-domain fix-up)
     const float *S;
     const int32_t *perm;      // NULL = identity order
     const int32_t *offsets;   // [n_groups + 2] group starts of the sorted order, or NULL
-    const int32_t *wexact;    // [n_groups] bit 0: W exactly tf32 (W2 == 0);
-                              //            bit 1: some |w| outside the tensor domain
+    const int32_t *wexact;    // [n_groups] bit 0: W exact in one fp16 term (W2 == 0);
+                              //            bit 1: W outside the tensor domain;
+                              //            bits 8-15: tau + 128 (the group's scale 2^tau)
     float *R;
     int64_t n_items;
     int n_groups;
@@ -190,11 +198,15 @@ template <int F>
 struct TcSmem {
     static constexpr int FS = F > 0 ? F : 36;          // sizing flow count (36 for runtime f)
     static constexpr int KP = kp_of(FS);
-    static constexpr int kWBytes = 2 * KP * 128 * 4;   // W1 and W2 tf32 images
+    static constexpr int kWBytes = 2 * KP * 128 * 2;   // W1 and W2 fp16 images
     static constexpr int kSBlock = 480 * FS;           // one block of S (slot stride)
     static constexpr int kJobBytes = kMaxJobs * 96;    // per-job context (JobCtx)
     static constexpr int kFixBytes = kFixCap * 8 + 16 + 2 * kMaxStages * 4;   // fix-up list
-    static constexpr int kMisc = 32 * 8 + 16 + kOffsSlots * 4 + kJobBytes + kFixBytes + kMaxJobs * 8;
+    static constexpr int kBars = 40;                    // mbarrier slots
+    static constexpr int kSigBytes = 2 * 128 * 4;       // per-row scale exponents, 2 tiles
+    static constexpr int kXchBytes = 2 * 8 * 32 * 4;    // split warps' row-range exchange
+    static constexpr int kMisc = kBars * 8 + 16 + kOffsSlots * 4 + kJobBytes + kFixBytes + kMaxJobs * 8 +
+                                 kSigBytes + kXchBytes;
     // R staging: the epilogue writes the tile's two blocks of R into shared memory in
     // their global layout and one thread stores each block with a bulk copy (full lines,
     // no partial sectors at planar row boundaries).  Shared memory, in order of
@@ -219,14 +231,16 @@ struct TcSmem {
     static constexpr int kStages = kStagesFit < kMaxS ? kStagesFit : kMaxS;
     static_assert(kStages >= 2, "S ring needs two stages");
     static constexpr int kOffS = kWBufs * kWBytes;     // kStagesAlloc x 2 blocks
-    static constexpr int kOffBar = kOffS + kStagesAlloc * 2 * kSBlock;   // 32 mbarrier slots
-    static constexpr int kOffTmem = kOffBar + 32 * 8;
+    static constexpr int kOffBar = kOffS + kStagesAlloc * 2 * kSBlock;   // kBars mbarrier slots
+    static constexpr int kOffTmem = kOffBar + kBars * 8;
     static constexpr int kOffJobs = kOffTmem + 16;     // JobCtx[kMaxJobs]
     static constexpr int kOffOffs = kOffJobs + kJobBytes;   // group offsets of every job
     static constexpr int kOffFix = kOffOffs + kOffsSlots * 4;   // int2 list, n, overflow, last[]
     static constexpr int kOffJCost = kOffFix + kFixBytes;        // int64 per job (split = 1)
-    static constexpr int kOffR = (kOffJCost + kMaxJobs * 8 + 127) / 128 * 128;
-    static constexpr int kBytesUsed = kStageR ? kOffR + kRStageBytes : kOffJCost + kMaxJobs * 8;
+    static constexpr int kOffSig = kOffJCost + kMaxJobs * 8;       // int32 [2][128]
+    static constexpr int kOffXch = kOffSig + kSigBytes;            // uint32 [2][8][32]
+    static constexpr int kOffR = (kOffXch + kXchBytes + 127) / 128 * 128;
+    static constexpr int kBytesUsed = kStageR ? kOffR + kRStageBytes : kOffXch + kXchBytes;
     static constexpr int kBytes = kBytesUsed > kMinSmem ? kBytesUsed : kMinSmem;
     static_assert(kBytesUsed <= kSmemLimit, "shared memory");
 };
@@ -351,13 +365,27 @@ __device__ __forceinline__ void fix_block(const JobCtx &J, int64_t item, int g) 
     }
 }
 
-// Is every value of S block `blk` (480 f bytes) inside the tensor domain?  (fix-up rescan)
-__device__ __forceinline__ bool block_in_domain(const JobCtx &J, int64_t blk) {
+// Is S block `blk` inside the tensor domain (fix-up rescan; the split warps' test)?  Every
+// value 0 or in [2^-40, 2^40); per row (RE j) every nonzero element within kRelRange
+// binades of the row's largest component (element = max(|re|, |im|)); for exact W also
+// every nonzero component.
+template <int LAYOUT>
+__device__ __forceinline__ bool block_in_domain(const JobCtx &J, int64_t blk, bool exact_w) {
     const uint32_t *Sb = reinterpret_cast<const uint32_t *>(J.S) + blk * (int64_t)(120 * J.f);
     bool ok = true;
-    for (int e = threadIdx.x; e < 120 * J.f; e += blockDim.x) {
-        const uint32_t u = __ldg(Sb + e) & 0x7FFFFFFFu;
-        ok &= u == 0u || (u >= kDomLo && u < kDomHi);
+    for (int jj = threadIdx.x; jj < 60; jj += blockDim.x) {
+        int emax = 0, emin = 255, cmin = 255;
+        for (int k = 0; k < J.f; ++k) {
+            const uint32_t ur = __ldg(Sb + (LAYOUT != 1 ? 2 * (k * 60 + jj) : k * 60 + jj)) & 0x7FFFFFFFu;
+            const uint32_t ui = __ldg(Sb + (LAYOUT != 1 ? 2 * (k * 60 + jj) + 1 : (J.f + k) * 60 + jj)) &
+                                0x7FFFFFFFu;
+            ok &= (ur == 0u || (ur >= kDomLo && ur < kDomHi)) && (ui == 0u || (ui >= kDomLo && ui < kDomHi));
+            const int e = (int)(max(ur, ui) >> 23);
+            if (ur | ui) { emax = max(emax, e); emin = min(emin, e); }
+            if (ur) cmin = min(cmin, (int)(ur >> 23));
+            if (ui) cmin = min(cmin, (int)(ui >> 23));
+        }
+        ok &= emax == 0 || (emin >= emax - kRelRange && (!exact_w || cmin >= emax - kRelRange));
     }
     return __syncthreads_and(ok) != 0;
 }
@@ -568,7 +596,7 @@ __device__ __forceinline__ bool srv_fill_slot(const SrvPtrs &sp, const TcJob &tm
     J.n_groups = 1;
     J.f = tmpl.f;
     J.kp = kp_of(tmpl.f);
-    J.wbytes = 2 * J.kp * 128 * 4;
+    J.wbytes = 2 * J.kp * 128 * 2;
     J.out_scale = tmpl.out_scale;
     J.g_begin = 0;
     const int64_t n = stop ? 0 : dn;
@@ -604,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     // TMEM column stride of the three A regions: fixed across the jobs of a launch
     // (the split of a job's first tile must not overlap the previous job's regions
     // that its last MMAs may still read).
-    constexpr int kARegion = L::KP;
+    constexpr int kARegion = L::KP / 2;      // fp16 pairs: KP / 2 columns per term
     // staged R (see TcSmem::kStageR); int16 output at f <= 12 measured faster with the
     // warps storing independently (0.41 vs 0.50 ms per 10^5 blocks; staged wins above:
     // f = 36 0.70 vs 0.84 — tools/sweep_f.py, profiles/r01_sweep_i16_v6.txt)
@@ -618,7 +646,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     uint64_t *bar_a_full = bars + 0, *bar_a_free = bars + 3, *bar_d_full = bars + 6,
              *bar_d_free = bars + 8, *bar_wfull = bars + 10, *bar_wfree = bars + 12,
              *bar_s_full = bars + 14, *bar_s_empty = bars + 14 + kRing,
-             *bar_slot_full = bars + 24, *bar_slot_free = bars + 28;   // SRV: descriptor ring
+             *bar_slot_full = bars + 24, *bar_slot_free = bars + 28,   // SRV: descriptor ring
+             *bar_sig_full = bars + 32, *bar_sig_free = bars + 34;     // row scales, per D buffer
     float *Ss = reinterpret_cast<float *>(smem + L::kOffS);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + L::kOffTmem);
     JobCtx *jobs = reinterpret_cast<JobCtx *>(smem + L::kOffJobs);
@@ -651,7 +680,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         J.n_groups = q.n_groups;
         J.f = F > 0 ? F : q.f;
         J.kp = kp_of(J.f);
-        J.wbytes = 2 * J.kp * 128 * 4;
+        J.wbytes = 2 * J.kp * 128 * 2;
         J.out_scale = q.out_scale;
         J.begin = J.end = 0;
         J.g_begin = 0;
@@ -729,6 +758,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             bfk::mbar_init(bar_s_full + i, 1);
             bfk::mbar_init(bar_s_empty + i, 32 * kSplitWarps);
         }
+        for (int i = 0; i < 2; ++i) {
+            bfk::mbar_init(bar_sig_full + i, 32 * kSplitWarps / 2);   // the K-half-0 warps write
+            bfk::mbar_init(bar_sig_free + i, 32 * kEpiWarps);
+        }
         if (SRV)
             for (int i = 0; i < kSrvRing; ++i) {
                 bfk::mbar_init(bar_slot_full + i, 1);
@@ -798,8 +831,11 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         const int ks = warp >> 2;                        // K half: chunks [0, h) or [h, end)
         const int bsel = m >= 60 ? 1 : 0, j = m - 60 * bsel;
         const uint32_t a_lane = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        uint32_t *xch = reinterpret_cast<uint32_t *>(smem + L::kOffXch);   // [2][8 warps][32]
+        int32_t *sig = reinterpret_cast<int32_t *>(smem + L::kOffSig);     // [2][128]
         int cur_g = -1, cur_j = -1;
         int cur_wf = 0;                                  // wexact flags of the current group
+        const int32_t *cur_wk = nullptr;                // (SRV: its entry, kept across slots)
         for (int64_t t = 0; next_tile(tl, kRoleSplit); ++t) {
             const JobCtx &J = it.jobs[tl.job];
             constexpr int FXs = (BFTC_FIXF_ROLES & 1) ? BFTC_FIXF : 0;
@@ -821,25 +857,26 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             if (tl.g != cur_g || tl.job != cur_j) {
                 cur_g = tl.g;
                 cur_j = tl.job;
-                cur_wf = __ldg(J.wexact + tl.g);
+                if (!SRV || J.wexact + tl.g != cur_wk) cur_wf = __ldg(J.wexact + tl.g);
+                cur_wk = J.wexact + tl.g;
             }
             // The rest of the tile runs with a compile-time K extent: the per-f kernels pass
-            // their own, the runtime-f batch kernel dispatches on the job's KP (9 classes), so
+            // their own, the runtime-f batch kernel dispatches on the job's KP (5 classes), so
             // its loops and registers are sized per class instead of for f = 36.
             auto split_tile = [&](auto kp_const) {
-                // KPc = 0: runtime K extent (register arrays sized for K = 72, halves split)
-                constexpr int KPs = decltype(kp_const)::value;
-                constexpr int KPm = KPs ? KPs : 72;
-                const int KPc = KPs ? KPs : KP;
-                // This warp's K chunks of the thread's row of S (half of them above f = 12) are
+                constexpr int KPc = decltype(kp_const)::value;
+                // This warp's K chunks of the thread's row of S (half of them above f = 16) are
                 // read from the ring once into registers and the slot is released at once; the
                 // term passes split from registers.
-                constexpr int kSlots = KPm <= 24 ? KPm / 8 : ((KPm / 8 + 1) >> 1);
-                const int c_half0 = KPm <= 24 ? KPc : ((KPc / 8 + 1) >> 1) * 8;
+                constexpr int kSlots = KPc <= 32 ? KPc / 8 : ((KPc / 8 + 1) >> 1);
+                constexpr int c_half0 = KPc <= 32 ? KPc : ((KPc / 8 + 1) >> 1) * 8;
                 const int c_beg0 = ks ? c_half0 : 0, c_end0 = ks ? KPc : c_half0;
                 float xs[kSlots * 8];
-                // tensor domain check of every value read, kept in a predicate
-                bool out_dom = false;
+                // tensor domain of the row: its largest element (max(|re|, |im|))
+                // in [2^-40, 2^40), every nonzero element within kRelRange binades of it, no
+                // NaN (the fma chain below turns any NaN into a NaN; Inf fails the range)
+                float emx = 0.0f, nan_chk = 0.0f;
+                uint32_t emn1 = 0xFFFFFFFFu;                 // smallest nonzero element bits - 1
     #pragma unroll
                 for (int i = 0; i < kSlots; ++i) {
                     const int c0 = c_beg0 + 8 * i;
@@ -847,8 +884,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                     for (int q = 0; q < 4; ++q) {
                         const int k = c0 / 2 + q;
                         float re = 0.0f, im = 0.0f;
-                        // (with a compile-time K extent only the last chunk can pass f)
-                        if (c0 < c_end0 && ((KPs > 0 && c0 + 8 < KPs) || k < f) && valid) {
+                        // (only the last chunk of a K class can pass f: fmin = KPc / 2 - 7)
+                        if (c0 < c_end0 && (c0 + 8 <= KPc - 14 || k < f) && valid) {
                             if (LAYOUT != 1) {
                                 const float2 v = reinterpret_cast<const float2 *>(Sb)[k * 60 + j];
                                 re = v.x;
@@ -860,11 +897,87 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                         }
                         xs[8 * i + 2 * q] = re;
                         xs[8 * i + 2 * q + 1] = im;
-                        const uint32_t ur = __float_as_uint(re) & 0x7FFFFFFFu, ui = __float_as_uint(im) & 0x7FFFFFFFu;
-                        out_dom |= (ur - kDomLo >= kDomHi - kDomLo && ur != 0u) |
-                                   (ui - kDomLo >= kDomHi - kDomLo && ui != 0u);
+                        const float el = fmaxf(fabsf(re), fabsf(im));
+                        emx = fmaxf(emx, el);
+                        emn1 = min(emn1, __float_as_uint(el) - 1u);
+                        nan_chk = fmaf(re, im, nan_chk);
                     }
                 }
+                // the row's other K half lives in the partner warp (warp ^ 4): exchange maxima
+                {
+                    float *xw = reinterpret_cast<float *>(xch) + (t & 1) * 256;
+                    xw[warp * 32 + lane] = emx;
+                    asm volatile("bar.sync %0, 64;" ::"r"(2 + (warp & 3)) : "memory");
+                    emx = fmaxf(emx, xw[(warp ^ 4) * 32 + lane]);
+                }
+                const int emax = (int)(__float_as_uint(emx) >> 23);     // 0: all-zero row
+                bool out_dom = nan_chk != nan_chk || emax >= (int)(kDomHi >> 23) ||
+                               (emax != 0 && (emax < (int)(kDomLo >> 23) ||
+                                              (emn1 != 0xFFFFFFFFu &&
+                                               (int)((emn1 + 1u) >> 23) < emax - kRelRange)));
+                // row scale 2^sg: the largest component lands in [2^14, 2^15); the epilogue
+                // undoes sg + tau (the group's W scale) with one exact multiply
+                const int sg = emax != 0 && !out_dom ? 141 - emax : 0;
+                const float sc = __uint_as_float((uint32_t)(127 + sg) << 23);
+    #pragma unroll
+                for (int i = 0; i < kSlots * 4; ++i) {
+                    float2 x2 = make_float2(xs[2 * i], xs[2 * i + 1]);
+                    x2 = tc::mul2f(x2, make_float2(sc, sc));
+                    xs[2 * i] = x2.x;
+                    xs[2 * i + 1] = x2.y;
+                }
+                if (ks == 0) {
+                    bfk::mbar_wait(bar_sig_free + (int)(t & 1), (uint32_t)(((t >> 1) & 1) ^ 1));
+                    sig[(t & 1) * 128 + m] = sg + ((cur_wf >> 8) & 255) - 128;
+                    mbar_arrive(bar_sig_full + (int)(t & 1));
+                }
+                if (kEarlyRelease) mbar_arrive(bar_s_empty + stage);    // values are in registers
+                uint32_t tiny = 0xFFFFFFFFu;   // exact W: smallest nonzero scaled component - 1
+    #pragma unroll
+                for (int pass = 0; pass < 3; ++pass) {
+                    const int term = pass == 2 ? 0 : pass + 1;
+                    bfk::mbar_wait(bar_a_free + term, par);
+                    tc::fence_after_sync();
+                    if (term == 2 && !(cur_wf & 1)) {   // S3 is only multiplied for exact W
+                        tc::fence_before_sync();
+                        mbar_arrive(bar_a_full + term);
+                        continue;
+                    }
+                    // this warp's K chunks; up to f = 16 (<= 4 chunks) the second warp of each
+                    // quarter only keeps the barrier counts
+    #pragma unroll
+                    for (int i = 0; i < kSlots; ++i) {
+                        const int c0 = c_beg0 + 8 * i;
+                        if (c0 >= c_end0) break;
+                        uint32_t h[4];
+    #pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            // exact 3-term split of the scaled values, each term rounded to
+                            // 11 significant bits (integer add + mask, 2 ops): x = x1 + x2 +
+                            // x3 exactly, |x - x1| <= 2^-11 |x|, |x3| <= 2^-22 |x|; packed
+                            // as fp16 pairs (exact in fp16's normal range)
+                            float y[2];
+    #pragma unroll
+                            for (int c = 0; c < 2; ++c) {
+                                const float x = xs[8 * i + 2 * e + c];
+                                const float x1 = tc::tf32_round(x);
+                                const float r1 = x - x1;          // exact
+                                const float x2 = tc::tf32_round(r1);
+                                y[c] = term == 0 ? x1 : (term == 1 ? x2 : r1 - x2);
+                                // exact W: all three terms exact in fp16 needs every nonzero
+                                // scaled component >= 2^-1 (else the block is fixed up)
+                                if (term == 2)
+                                    tiny = min(tiny, (__float_as_uint(x) & 0x7FFFFFFFu) - 1u);
+                            }
+                            h[e] = tc::pack_f16x2(y[0], y[1]);
+                        }
+                        if constexpr (!(DBG & 4)) tc::tmem_st4(a_lane + term * kARegion + c0 / 2, h);
+                    }
+                    tc::tmem_st_wait();
+                    tc::fence_before_sync();
+                    mbar_arrive(bar_a_full + term);
+                }
+                out_dom |= tiny < 0x3EFFFFFFu;   // a nonzero scaled component below 2^-1
                 if (valid && ((cur_wf & 2) || out_dom)) {
                     // rare: list the block once per tile (the first thread to see it wins; a
                     // stage's slot is reused only after every split warp finished this tile)
@@ -872,60 +985,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                     if (atomicMax(fix_last + 2 * stage + bsel, key) < key) {
                         const int idx = atomicAdd(fix_n, 1);
                         if (idx < kFixCap)
-                            fix_list[idx] = make_int2((int)(it.item - tl.cnt + bsel), (it.j << 16) | cur_g);
+                            fix_list[idx] = make_int2((int)(it.item - tl.cnt + bsel), (it.j << 16) | tl.g);
                         else
                             atomicExch(fix_over, 1);
                     }
-                }
-                if (kEarlyRelease) mbar_arrive(bar_s_empty + stage);    // values are in registers
-    #pragma unroll
-                for (int pass = 0; pass < 3; ++pass) {
-                    const int term = pass == 2 ? 0 : pass + 1;
-                    bfk::mbar_wait(bar_a_free + term, par);
-                    tc::fence_after_sync();
-                    if (term == 2 && !(cur_wf & 1)) {   // S3 is only multiplied for tf32-exact W
-                        tc::fence_before_sync();
-                        mbar_arrive(bar_a_full + term);
-                        continue;
-                    }
-                    // DBG 32: S1 as fp16 pairs over K rounded up to 16 (one more chunk at f = 36)
-                    const int kend = ((DBG & 32) && term == 0) ? (KPc + 15) / 16 * 16 : KPc;
-                    // this warp's K chunks; at f <= 12 (<= 3 chunks) the second warp of each
-                    // quarter only keeps the barrier counts (splitting measured slower there)
-                    const int c_half = KPm <= 24 ? kend : ((kend / 8 + 1) >> 1) * 8;
-                    const int c_beg = ks ? c_half : 0, c_end = ks ? kend : c_half;
-    #pragma unroll
-                    for (int i = 0; i < kSlots; ++i) {
-                        const int c0 = c_beg + 8 * i;
-                        if (c0 >= c_end) break;
-                        float x[8];
-    #pragma unroll
-                        for (int e = 0; e < 8; ++e) x[e] = xs[8 * i + e];
-                        uint32_t v[8];
-    #pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            // exact 3-term split, each term rounded to 11 significant
-                            // bits (integer add + mask, 2 ops): x = x1 + x2 + x3 exactly,
-                            // |x - x1| <= 2^-11 |x|, |x3| <= 2^-22 |x|.
-                            const float x1 = tc::tf32_round(x[e]);
-                            const float r1 = x[e] - x1;          // exact
-                            const float x2 = tc::tf32_round(r1);
-                            const float x3 = r1 - x2;            // exact, fits tf32
-                            v[e] = __float_as_uint(term == 0 ? x1 : (term == 1 ? x2 : x3));
-                        }
-                        if ((DBG & 32) && term == 0) {
-                            uint32_t h[4];
-    #pragma unroll
-                            for (int e = 0; e < 4; ++e)
-                                h[e] = bfk::pack_half2(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
-                            if constexpr (!(DBG & 4)) tc::tmem_st4(a_lane + c0 / 2, h);
-                        } else {
-                            if constexpr (!(DBG & 4)) tc::tmem_st8(a_lane + term * kARegion + c0, v);
-                        }
-                    }
-                    tc::tmem_st_wait();
-                    tc::fence_before_sync();
-                    mbar_arrive(bar_a_full + term);
                 }
             };
             if constexpr (F > 0) {
@@ -934,15 +997,11 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 split_tile(std::integral_constant<int, kp_of(FXs)>{});
             } else {
                 switch (KP) {
-                    case 8: split_tile(std::integral_constant<int, 8>{}); break;
                     case 16: split_tile(std::integral_constant<int, 16>{}); break;
-                    case 24: split_tile(std::integral_constant<int, 24>{}); break;
                     case 32: split_tile(std::integral_constant<int, 32>{}); break;
-                    case 40: split_tile(std::integral_constant<int, 40>{}); break;
                     case 48: split_tile(std::integral_constant<int, 48>{}); break;
-                    case 56: split_tile(std::integral_constant<int, 56>{}); break;
                     case 64: split_tile(std::integral_constant<int, 64>{}); break;
-                    default: split_tile(std::integral_constant<int, 72>{}); break;
+                    default: split_tile(std::integral_constant<int, 80>{}); break;
                 }
             }
             if (!kEarlyRelease) mbar_arrive(bar_s_empty + stage);   // ring slot may be refilled
@@ -989,7 +1048,9 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                                   J.S + blk1 * (int64_t)(120 * f), sbytes, bar_s_full + stage, pol);
             }
             __syncwarp();
-            if (tl.g != cur_g || tl.job != cur_j) {
+            // A new W segment at every group or job change; the slot server keeps the image
+            // across slots (one plan and group; applied to batches this measured ~1 % slower).
+            if ((tl.g != cur_g || tl.job != cur_j) && !(SRV && seg >= 0)) {
                 cur_g = tl.g;
                 cur_j = tl.job;
                 ++seg;
@@ -1023,15 +1084,14 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         // ------------------------------------------------------------ MMA issuer
         int cur_g = -1, cur_j = -1;
         int64_t seg = -1;
-        constexpr uint32_t idesc = tc::idesc_tf32(128, 128);
-        constexpr uint32_t idesc_c = tc::idesc_bf16(128, 128);   // DBG 16 only
+        constexpr uint32_t idesc = tc::idesc_f16(128, 128);
         uint32_t w_base = tc::smem_u32(Wsm);
         bool exact = false;
         for (int64_t t = 0; next_tile(tl, kRoleMma); ++t) {
             const JobCtx &J = it.jobs[tl.job];
             constexpr int FXm = (BFTC_FIXF_ROLES & 4) ? BFTC_FIXF : 0;
             const int KP = F > 0 ? L::KP : (FXm ? kp_of(FXm) : J.kp);
-            if (tl.g != cur_g || tl.job != cur_j) {   // new group segment: W prefetched by the producer
+            if ((tl.g != cur_g || tl.job != cur_j) && !(SRV && seg >= 0)) {   // new W segment (producer's rule)
                 exact = (__ldg(J.wexact + tl.g) & 1) != 0;
                 // the previous segment's buffer is free once every MMA issued so far completed
                 if (seg >= 0 && lane == 0) tc::mma_commit(bar_wfree + (int)(seg % L::kWBufs));
@@ -1047,10 +1107,11 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             const uint32_t u = (uint32_t)(t >> 1);
             const uint32_t d = tmem + kDCol0 + 128 * b;
             bfk::mbar_wait(bar_d_free + b, (u & 1) ^ 1);
-            // MMA groups over K, small terms first, every one kind::tf32 (exact products):
-            //   tf32-exact W (W2 == 0, e.g. identity / selection): S2 W1, S3 W1, S1 W1
+            // MMA groups over K, small terms first, every one kind::f16 on fp16 terms of the
+            // scaled operands (exact 11-bit x 11-bit products, fp32 accumulate):
+            //   exact W (W2 == 0, e.g. identity / selection): S2 W1, S3 W1, S1 W1
             //   (= S W exactly up to accumulation rounding: copies are bit-exact);
-            //   general W: S2 W1, S1 W2, S1 W1 (the S3 region is not used) — 3 KP/8 MMAs
+            //   general W: S2 W1, S1 W2, S1 W1 (the S3 region is not used) — 3 KP/16 MMAs
             //   (DESIGN.md §7).  The middle group of general W reads the S1 region.
             // Each split term's TMEM region is released by a commit once read.
             // The K extent is a compile-time constant in the issue loop (the runtime-f
@@ -1066,23 +1127,17 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                     if (s1w2) bfk::mbar_wait(bar_a_full + 0, (uint32_t)(t & 1));
                     tc::fence_after_sync();
                     const int areg = s1w2 ? 0 : at;                     // A region read
-                    const uint32_t boff = s1w2 ? (uint32_t)(KPc / 4) : 0u;  // W2 image after W1
+                    const uint32_t boff = s1w2 ? (uint32_t)(KPc / 8) : 0u;  // W2 image after W1
                     if (lane == 0) {
-                        // DBG & 16 (energy experiment): the S1 W1 group as ceil(KP / 16)
-                        // fp16-kind K = 16 MMAs on the same (reinterpreted) operands
-                        const int nkb = ((DBG & 16) && grp == 2) ? (KPc + 15) / 16 : KPc / 8;
+                        // K = 16 per MMA: 8 TMEM columns of fp16 pairs of A, two 16-byte K
+                        // chunks (2 x 2048 bytes) of the B image
     #pragma unroll
-                        for (int kb = 0; kb < nkb; ++kb) {
+                        for (int kb = 0; kb < KPc / 16; ++kb) {
                             const uint64_t desc = tc::smem_desc(
                                 w_base + (uint32_t)((boff + 2 * kb) * 16 * 128), 16 * 128, 128);
-                            if constexpr (!(DBG & 1)) {
-                                if ((DBG & 16) && grp == 2)
-                                    tc::mma_bf16_ts(d, tmem + areg * kARegion + kb * 8, desc,
-                                                    idesc_c & ~((7u << 7) | (7u << 10)), kb != 0);
-                                else
-                                    tc::mma_tf32_ts(d, tmem + areg * kARegion + kb * 8, desc, idesc,
-                                                    (grp | kb) != 0);
-                            }
+                            if constexpr (!(DBG & 1))
+                                tc::mma_f16_ts(d, tmem + areg * kARegion + kb * 8, desc, idesc,
+                                               (grp | kb) != 0);
                         }
                         if (grp < 2) tc::mma_commit(bar_a_free + at);
                     }
@@ -1095,15 +1150,11 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 mma_groups(std::integral_constant<int, kp_of(FXm)>{});
             } else {
                 switch (KP) {
-                    case 8: mma_groups(std::integral_constant<int, 8>{}); break;
                     case 16: mma_groups(std::integral_constant<int, 16>{}); break;
-                    case 24: mma_groups(std::integral_constant<int, 24>{}); break;
                     case 32: mma_groups(std::integral_constant<int, 32>{}); break;
-                    case 40: mma_groups(std::integral_constant<int, 40>{}); break;
                     case 48: mma_groups(std::integral_constant<int, 48>{}); break;
-                    case 56: mma_groups(std::integral_constant<int, 56>{}); break;
                     case 64: mma_groups(std::integral_constant<int, 64>{}); break;
-                    default: mma_groups(std::integral_constant<int, 72>{}); break;
+                    default: mma_groups(std::integral_constant<int, 80>{}); break;
                 }
             }
             if (lane == 0) {
@@ -1125,6 +1176,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         const int m = q * 32 + lane;
         const int bsel = m >= 60 ? 1 : 0, j = m - 60 * bsel;
         const bool e0 = warp == kEpiWarp0 && lane == 0;  // issues the staged bulk stores
+        const int32_t *sig = reinterpret_cast<const int32_t *>(smem + L::kOffSig);   // [2][128]
         uint64_t pol_r = 0;
         if (kStageR && e0) pol_r = bfk::policy_evict_first();
         for (int64_t t = 0; next_tile(tl, kRoleEpi); ++t) {
@@ -1140,6 +1192,11 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 if (warp == kEpiWarp0 && lane == 0) srv_trace(p.srv, 3);
                 fresh = false;
             }
+            // the row's scale 2^-(sg + tau) from the split warps: one exact multiply (exact
+            // unless the result is subnormal)
+            bfk::mbar_wait(bar_sig_full + b, u & 1);
+            const float us = __uint_as_float((uint32_t)(127 - sig[b * 128 + m]) << 23);
+            mbar_arrive(bar_sig_free + b);
             const uint32_t d = tmem + ((uint32_t)(q * 32) << 16) + kDCol0 + 128 * b + 64 * h;
             if constexpr (!(DBG & 2) && !kStageR && (LAYOUT == 2 || LAYOUT == 3)) {
                 // 16-bit output, direct stores (int16 output at f <= 12; see kStageR), in
@@ -1165,8 +1222,11 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int aa = 2 * i;            // antenna pair within the half
-                        const float re0 = __uint_as_float(v[2 * aa]), im0 = __uint_as_float(v[2 * aa + 1]);
-                        const float re1 = __uint_as_float(v[2 * aa + 2]), im1 = __uint_as_float(v[2 * aa + 3]);
+                        const float2 z0 = tc::mul2f(make_float2(__uint_as_float(v[2 * aa]), __uint_as_float(v[2 * aa + 1])),
+                                                    make_float2(us, us));
+                        const float2 z1 = tc::mul2f(make_float2(__uint_as_float(v[2 * aa + 2]),
+                                                                __uint_as_float(v[2 * aa + 3])), make_float2(us, us));
+                        const float re0 = z0.x, im0 = z0.y, re1 = z1.x, im1 = z1.y;
                         const float gr = __shfl_xor_sync(0xffffffffu, odd ? re0 : re1, 1);
                         const float gi = __shfl_xor_sync(0xffffffffu, odd ? im0 : im1, 1);
                         // even lane: antenna a, REs j, j+1; odd lane: antenna a+1, REs j-1, j
@@ -1208,7 +1268,9 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
 #pragma unroll
                     for (int aa = 0; aa < 32; ++aa) {
                         const int a = 32 * h + aa;
-                        const float re = __uint_as_float(v[2 * aa]), im = __uint_as_float(v[2 * aa + 1]);
+                        const float2 z = tc::mul2f(make_float2(__uint_as_float(v[2 * aa]), __uint_as_float(v[2 * aa + 1])),
+                                                   make_float2(us, us));
+                        const float re = z.x, im = z.y;
                         if (LAYOUT == 0)
                             *reinterpret_cast<float2 *>(Rt + 2 * (a * 60 + j)) = make_float2(re, im);
                         else if (LAYOUT == 1) {
@@ -1258,7 +1320,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 const JobCtx &J = jobs[t2.job];
                 const bool wbad = (__ldg(J.wexact + t2.g) & 2) != 0;
                 for (int b2 = 0; b2 < t2.cnt; ++b2)
-                    if (wbad || !block_in_domain(J, block_of(J, t2.item + b2)))
+                    if (wbad || !block_in_domain<LAYOUT>(J, block_of(J, t2.item + b2),
+                                                         (__ldg(J.wexact + t2.g) & 1) != 0))
                         fix_block<LAYOUT>(J, t2.item + b2, t2.g);
             }
         }

@@ -93,8 +93,23 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
            ((uint32_t)(M >> 4) << 24);
 }
 
-// D[tmem] (+)= A[tmem] x B[smem desc], bf16 inputs (A: two bf16 per 32-bit TMEM
-// column, even K element in the low half); one thread issues.
+// Instruction descriptor for kind::f16 with fp16 A/B ([7,10) a_format = 0 (F16),
+// [10,13) b_format = 0), fp32 accumulate, K-major; K = 16 per instruction.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// Two fp32 values rounded (RN-even) to fp16 and packed, the first in the low half
+// (the even K element of an A / B pair).
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+// D[tmem] (+)= A[tmem] x B[smem desc], kind::f16 (fp16 or bf16 inputs by the
+// descriptor; A: two 16-bit values per 32-bit TMEM column, even K element in the low
+// half); one thread issues.
 __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
                                             uint32_t idesc, uint32_t accumulate) {
     asm volatile(
@@ -102,6 +117,11 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
         ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
+}
+
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+    mma_bf16_ts(d_tmem, a_tmem, b_desc, idesc, accumulate);
 }
 
 // Two fp32 values rounded (RN-even) to bf16 and packed, the first in the low half.
@@ -127,6 +147,14 @@ __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile(
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
         ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Packed fp32x2 multiply (FMUL2: two IEEE fp32 products, round to nearest, one instruction).
+__device__ __forceinline__ float2 mul2f(float2 a, float2 b) {
+    unsigned long long ra = *reinterpret_cast<const unsigned long long *>(&a);
+    unsigned long long rb = *reinterpret_cast<const unsigned long long *>(&b), r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(ra), "l"(rb));
+    return *reinterpret_cast<const float2 *>(&r);
 }
 
 // fp32 -> tf32 (round to nearest, ties away), returned as an fp32 bit pattern

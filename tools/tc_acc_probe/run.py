@@ -25,7 +25,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 def lib():
     L = ctypes.CDLL(os.path.join(HERE, "libtcacc.so"))
     L.acc_run.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int] * 3
+    L.acc_run_kind.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int] * 4
     return L
+
+
+def h16(x):
+    """fp16-exact values (round to nearest fp16), as fp32."""
+    return np.asarray(x, np.float64).astype(np.float16).astype(np.float32)
 
 
 def tf32(x):
@@ -34,22 +40,23 @@ def tf32(x):
     return b.astype(np.uint32).view(np.float32)
 
 
-def run(L, A, B, C, c_mode=1):
+def run(L, A, B, C, c_mode=1, kind=0):
     npb, nmma = A.shape[0], A.shape[1]
     A = np.ascontiguousarray(A, np.float32)
     B = np.ascontiguousarray(B, np.float32)
     C = np.ascontiguousarray(C, np.float32)
     D = np.empty((npb, 128, 128), np.float32)
-    rc = L.acc_run(A.ctypes.data, B.ctypes.data, C.ctypes.data, D.ctypes.data, npb, nmma, c_mode)
+    rc = L.acc_run_kind(A.ctypes.data, B.ctypes.data, C.ctypes.data, D.ctypes.data, npb, nmma, c_mode,
+                        kind)
     assert rc == 0, rc
     return D
 
 
 def exact(A, B, C, c_mode=1):
     """Exact D (extended precision): terms [np][128][128][nmma*8 (+1)], summed by magnitude."""
-    npb, nmma = A.shape[:2]
-    A64 = A.astype(np.float64).transpose(0, 2, 1, 3).reshape(npb, 128, nmma * 8)
-    B64 = B.astype(np.float64).transpose(0, 2, 1, 3).reshape(npb, 128, nmma * 8)
+    npb, nmma, K = A.shape[0], A.shape[1], A.shape[3]
+    A64 = A.astype(np.float64).transpose(0, 2, 1, 3).reshape(npb, 128, nmma * K)
+    B64 = B.astype(np.float64).transpose(0, 2, 1, 3).reshape(npb, 128, nmma * K)
     out = np.empty((npb, 128, 128), np.longdouble)
     absum = np.empty((npb, 128, 128), np.float64)
     amax = np.empty((npb, 128, 128), np.float64)
@@ -124,6 +131,55 @@ def chain_cases(rng, npb):
         yield name, A, B, np.zeros((npb, 128, 128)), 0
 
 
+def cases16(rng, npb):
+    """kind::f16 (fp16 operands, K = 16): the same families within fp16's range."""
+    g = lambda *s: rng.standard_normal(s)  # noqa: E731
+    sh = (npb, 1, 128, 16)
+    yield "f16_gauss_c0", h16(g(*sh)), h16(g(*sh)), np.zeros((npb, 128, 128)), 0
+    u = rng.integers(-20, 21, (npb, 128, 128))
+    yield "f16_gauss_c_scaled", h16(g(*sh)), h16(g(*sh)), g(npb, 128, 128) * 2.0 ** u, 1
+    yield ("f16_positive", h16(rng.uniform(0.5, 1, sh)), h16(rng.uniform(0.5, 1, sh)),
+           rng.uniform(0.5, 1, (npb, 128, 128)) * 2.0 ** rng.integers(-3, 4, (npb, 128, 128)), 1)
+    v = rng.integers(-12, 13, sh)
+    w = rng.integers(-12, 13, sh)
+    yield "f16_spread_exponents", h16(g(*sh) * 2.0 ** v), h16(g(*sh) * 2.0 ** w), g(npb, 128, 128), 1
+    a = h16(rng.uniform(1, 2, sh) * 2.0 ** rng.integers(-14, -4, sh))
+    b = h16(rng.uniform(1, 2, sh) * 2.0 ** rng.integers(-14, -4, sh))
+    yield "f16_trunc_below_acc_pos", a, b, np.ones((npb, 128, 128)) * rng.uniform(1, 2, (npb, 128, 128)), 1
+    yield "f16_trunc_below_acc_neg", -a, b, np.ones((npb, 128, 128)) * rng.uniform(1, 2, (npb, 128, 128)), 1
+    a2 = h16(g(*sh) * 2.0 ** rng.integers(-14, -2, sh))
+    a2[..., 0] = h16(rng.uniform(1, 2, (npb, 1, 128)) * 2.0 ** 10)
+    yield "f16_one_large_product", a2, h16(g(*sh)), g(npb, 128, 128) * 2.0 ** -2, 1
+    A3, B3 = h16(g(*sh) * 64), h16(g(*sh) * 64)
+    s = np.einsum("pmik,pmjk->pij", A3.astype(np.float64), B3.astype(np.float64))
+    yield "f16_cancellation", A3, B3, (-s).astype(np.float32) * (1 + 2.0 ** -20 * g(npb, 128, 128)), 1
+    a4 = h16(np.ones(sh) * rng.uniform(1, 2, sh))
+    a4[..., 1::2] *= -1
+    yield "f16_alternating", a4, h16(rng.uniform(1, 2, sh)), rng.uniform(1, 2, (npb, 128, 128)) * 16, 1
+    # fp16 subnormal operands (exact in fp16) and products near fp16's range ends
+    sub = h16(rng.integers(1, 1024, sh) * 2.0 ** -24)
+    yield "f16_subnormal_operands", sub, h16(g(*sh) * 2.0 ** 14), g(npb, 128, 128), 1
+    yield "f16_large", h16(rng.uniform(1, 2, sh) * 2.0 ** 15), h16(rng.uniform(-2, 2, sh) * 2.0 ** 15), \
+        g(npb, 128, 128) * 2.0 ** 30, 1
+
+
+def chain_cases16(rng, npb):
+    """The f16 kernel's chain at f = 36 (K padded to 80: 5 MMAs per group), operands scaled
+    so the row / group maximum sits in [2^14, 2^15): S2 W1, S1 W2, then S1 W1."""
+    sh = (npb, 5, 128, 16)
+    for name, gen in (("f16_kernel_chain_gauss", lambda: rng.standard_normal(sh)),
+                      ("f16_kernel_chain_positive", lambda: rng.uniform(0.5, 1.0, sh))):
+        s, w = gen().astype(np.float32) * 2.0 ** 12, gen().astype(np.float32) * 2.0 ** 12
+        s[:, 4, :, 8:] = 0                       # K = 72 of 80
+        w[:, 4, :, 8:] = 0
+        s1, w1 = tf32(s), tf32(w)
+        s2, w2 = h16(tf32(s - s1)), h16(tf32(w - w1))
+        s1, w1 = h16(s1), h16(w1)
+        A = np.concatenate([s2, s1, s1], axis=1)
+        B = np.concatenate([w1, w2, w1], axis=1)
+        yield name, A, B, np.zeros((npb, 128, 128)), 0
+
+
 def subnormal_checks(L):
     out = {}
     A = np.zeros((1, 1, 128, 8), np.float32)
@@ -166,23 +222,28 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--out", default="")
     ap.add_argument("--save", default="", help="npz of every case's A, B, C, D (model fitting)")
+    ap.add_argument("--kind", default="tf32", choices=["tf32", "f16"])
     args = ap.parse_args()
     L = lib()
     rng = np.random.default_rng(args.seed)
     res = {}
     raw = {}
-    for name, A, B, C, cm in list(cases(rng, args.np)) + list(chain_cases(rng, max(4, args.np // 4))):
-        A, B = tf32(A), tf32(B)
+    kind = 1 if args.kind == "f16" else 0
+    gen = (list(cases16(rng, args.np)) + list(chain_cases16(rng, max(4, args.np // 4)))) if kind else \
+        (list(cases(rng, args.np)) + list(chain_cases(rng, max(4, args.np // 4))))
+    for name, A, B, C, cm in gen:
+        A, B = (h16(A), h16(B)) if kind else (tf32(A), tf32(B))
         C = np.asarray(C, np.float32)
-        D = run(L, A, B, C, cm)
+        D = run(L, A, B, C, cm, kind)
         if args.save:
             raw.update({f"{name}/A": A, f"{name}/B": B, f"{name}/C": C, f"{name}/D": D,
                         f"{name}/cmode": np.int32(cm)})
         ex, absum, amax = exact(A, B, C, cm)
         res[name] = stats(D, ex, absum, amax, A.shape[1])
         print(name, json.dumps(res[name]), flush=True)
-    res["subnormals"] = subnormal_checks(L)
-    print("subnormals", json.dumps(res["subnormals"]))
+    if not kind:
+        res["subnormals"] = subnormal_checks(L)
+        print("subnormals", json.dumps(res["subnormals"]))
     if args.out:
         with open(args.out, "w") as fh:
             json.dump(res, fh, indent=1)

@@ -1,4 +1,5 @@
-// Accumulation-error probe for tcgen05.mma kind::tf32 (fp32 accumulate in TMEM).
+// Accumulation-error probe for tcgen05.mma kind::tf32 and kind::f16 (fp16 inputs; fp32
+// accumulate in TMEM).
 //
 // DESIGN.md §7 bounds the tensor path's error with a model of how one MMA adds
 // its K = 8 exact products to the accumulator.  This probe measures that model:
@@ -16,20 +17,32 @@
 
 constexpr int kMaxMma = 32;
 
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+// KIND 0: kind::tf32, K = 8 per MMA; KIND 1: kind::f16 with fp16 A/B, K = 16 per MMA (the
+// host passes fp16-exact values as fp32; two per 32-bit word, even K element low).
+template <int KIND>
 __global__ void __launch_bounds__(128, 1)
 acc_probe(const float *A, const float *B, const float *C, float *D, int nmma, int c_mode) {
+    constexpr int KK = KIND ? 16 : 8;
     __shared__ uint32_t tmem_base;
     __shared__ __align__(8) uint64_t bar;
     extern __shared__ __align__(1024) float Bs[];   // nmma x [2 K-chunks][16][8][4]
     const int tid = threadIdx.x, warp = tid / 32;
     const int64_t p = blockIdx.x;
-    const float *Ap = A + p * nmma * 128 * 8, *Bp = B + p * nmma * 128 * 8;
+    const float *Ap = A + p * nmma * 128 * KK, *Bp = B + p * nmma * 128 * KK;
     if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
     if (tid == 0) { bfk::mbar_init(&bar, 1); bfk::mbar_fence_init(); }
-    for (int idx = tid; idx < nmma * 128 * 8; idx += 128) {
-        const int m = idx / 1024, rem = idx % 1024, n = rem / 8, k = rem % 8;
-        const int kc = k / 4, ng = n / 8, r = n % 8, e = k % 4;
-        Bs[m * 1024 + ((kc * 16 + ng) * 8 + r) * 4 + e] = Bp[idx];
+    for (int idx = tid; idx < nmma * 128 * 8; idx += 128) {   // one 32-bit word each
+        const int m = idx / 1024, rem = idx % 1024, n = rem / 8, w = rem % 8;
+        const int kc = w / 4, ng = n / 8, r = n % 8, e = w % 4;
+        const float *src = Bp + (m * 128 + n) * KK;
+        Bs[m * 1024 + ((kc * 16 + ng) * 8 + r) * 4 + e] =
+            KIND ? __uint_as_float(pack_f16x2(src[2 * w], src[2 * w + 1])) : src[w];
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc::fence_before_sync();
@@ -46,7 +59,9 @@ acc_probe(const float *A, const float *B, const float *C, float *D, int nmma, in
     // A_m -> columns [256 + 8 m, 256 + 8 m + 8)
     for (int m = 0; m < nmma; ++m) {
         uint32_t v[8];
-        for (int i = 0; i < 8; ++i) v[i] = __float_as_uint(Ap[(m * 128 + tid) * 8 + i]);
+        const float *src = Ap + (m * 128 + tid) * KK;
+        for (int i = 0; i < 8; ++i)
+            v[i] = KIND ? pack_f16x2(src[2 * i], src[2 * i + 1]) : __float_as_uint(src[i]);
         tc::tmem_st8(base + lane_base + 256 + 8 * m, v);
     }
     tc::tmem_st_wait();
@@ -54,10 +69,14 @@ acc_probe(const float *A, const float *B, const float *C, float *D, int nmma, in
     __syncthreads();
     tc::fence_after_sync();
     if (tid == 0) {
-        const uint32_t idesc = tc::idesc_tf32(128, 128);
+        const uint32_t idesc = KIND ? (tc::idesc_bf16(128, 128) & ~((7u << 7) | (7u << 10)))
+                                    : tc::idesc_tf32(128, 128);
         for (int m = 0; m < nmma; ++m) {
             const uint64_t desc = tc::smem_desc(tc::smem_u32(Bs + m * 1024), 16 * 128, 128);
-            tc::mma_tf32_ts(base, base + 256 + 8 * m, desc, idesc, (c_mode != 0 || m > 0) ? 1u : 0u);
+            if (KIND)
+                tc::mma_bf16_ts(base, base + 256 + 8 * m, desc, idesc, (c_mode != 0 || m > 0) ? 1u : 0u);
+            else
+                tc::mma_tf32_ts(base, base + 256 + 8 * m, desc, idesc, (c_mode != 0 || m > 0) ? 1u : 0u);
         }
         tc::mma_commit(&bar);
     }
@@ -74,22 +93,34 @@ acc_probe(const float *A, const float *B, const float *C, float *D, int nmma, in
     if (warp == 0) tc::tmem_free<512>(base);
 }
 
-// A, B: [np][nmma][128][8] fp32 (tf32 bit patterns); C, D: [np][128][128].
-extern "C" int acc_run(const float *A, const float *B, const float *C, float *D, int np, int nmma,
-                       int c_mode) {
+// A, B: [np][nmma][128][K] fp32 (tf32 or fp16-exact values; K = 8 or 16 by kind);
+// C, D: [np][128][128].
+extern "C" int acc_run_kind(const float *A, const float *B, const float *C, float *D, int np,
+                            int nmma, int c_mode, int kind) {
     if (nmma < 1 || nmma > kMaxMma || np < 1) return -1;
-    const size_t ab = (size_t)np * nmma * 128 * 8 * 4, cd = (size_t)np * 128 * 128 * 4;
+    const int KK = kind ? 16 : 8;
+    const size_t ab = (size_t)np * nmma * 128 * KK * 4, cd = (size_t)np * 128 * 128 * 4;
     float *dA, *dB, *dC, *dD;
     cudaMalloc(&dA, ab); cudaMalloc(&dB, ab); cudaMalloc(&dC, cd); cudaMalloc(&dD, cd);
     cudaMemcpy(dA, A, ab, cudaMemcpyHostToDevice);
     cudaMemcpy(dB, B, ab, cudaMemcpyHostToDevice);
     cudaMemcpy(dC, C, cd, cudaMemcpyHostToDevice);
     const int smem = nmma * 1024 * 4;
-    cudaFuncSetAttribute(acc_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    acc_probe<<<np, 128, smem>>>(dA, dB, dC, dD, nmma, c_mode);
+    if (kind) {
+        cudaFuncSetAttribute(acc_probe<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        acc_probe<1><<<np, 128, smem>>>(dA, dB, dC, dD, nmma, c_mode);
+    } else {
+        cudaFuncSetAttribute(acc_probe<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        acc_probe<0><<<np, 128, smem>>>(dA, dB, dC, dD, nmma, c_mode);
+    }
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("acc_probe: %s\n", cudaGetErrorString(e)); return (int)e; }
     cudaMemcpy(D, dD, cd, cudaMemcpyDeviceToHost);
     cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dD);
     return 0;
+}
+
+extern "C" int acc_run(const float *A, const float *B, const float *C, float *D, int np, int nmma,
+                       int c_mode) {
+    return acc_run_kind(A, B, C, D, np, nmma, c_mode, 0);
 }

@@ -92,6 +92,8 @@ extern "C" float tcx_run(int dbg, const float *S, float *R, const float *Wimg, l
         case 15: return run<15>(S, R, Wimg, n, reps);
         case 16: return run<16>(S, R, Wimg, n, reps);
         case 48: return run<48>(S, R, Wimg, n, reps);
+        case 64: return run<64>(S, R, Wimg, n, reps);
+        case 240: return run<240>(S, R, Wimg, n, reps);
     }
     return -2;
 }
