@@ -73,6 +73,9 @@ constexpr int kMinSmem = 120 * 1024;   // forces one CTA (and one TMEM owner) pe
 #ifndef BFTC_EARLY_RELEASE
 #define BFTC_EARLY_RELEASE 0
 #endif
+#ifndef BFTC_ABUFS
+#define BFTC_ABUFS 2      // TMEM A-region buffers (2 where they fit)
+#endif
 // Experiments only: the runtime-f kernel with a compile-time f in some roles
 // (BFTC_FIXF_ROLES bits: 1 split warps, 2 producer, 4 MMA issuer).  Results are wrong
 // for any other f.
@@ -202,7 +205,7 @@ struct TcSmem {
     static constexpr int kSBlock = 480 * FS;           // one block of S (slot stride)
     static constexpr int kJobBytes = kMaxJobs * 96;    // per-job context (JobCtx)
     static constexpr int kFixBytes = kFixCap * 8 + 16 + 2 * kMaxStages * 4;   // fix-up list
-    static constexpr int kBars = 40;                    // mbarrier slots
+    static constexpr int kBars = 48;                    // mbarrier slots
     static constexpr int kSigBytes = 2 * 128 * 4;       // per-row scale exponents, 2 tiles
     static constexpr int kXchBytes = 2 * 8 * 32 * 4;    // split warps' row-range exchange
     static constexpr int kMisc = kBars * 8 + 16 + kOffsSlots * 4 + kJobBytes + kFixBytes + kMaxJobs * 8 +
@@ -633,6 +636,9 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     // (the split of a job's first tile must not overlap the previous job's regions
     // that its last MMAs may still read).
     constexpr int kARegion = L::KP / 2;      // fp16 pairs: KP / 2 columns per term
+    // A regions double-buffered (the split of tile t + 1 overlaps tile t's MMAs) when both
+    // sets of three terms fit below the D buffers
+    constexpr int kABufs = (2 * 3 * kARegion <= kDCol0) ? BFTC_ABUFS : 1;
     // staged R (see TcSmem::kStageR); int16 output at f <= 12 measured faster with the
     // warps storing independently (0.41 vs 0.50 ms per 10^5 blocks; staged wins above:
     // f = 36 0.70 vs 0.84 — tools/sweep_f.py, profiles/r01_sweep_i16_v6.txt)
@@ -643,6 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     float *Wsm = reinterpret_cast<float *>(smem);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::kOffBar);
     // a_full[t] / a_free[t]: TMEM A region of split term t (0: S1, 1: S2, 2: S3)
+    // a_full / a_free of A buffer 0 at bars + 0 / + 3, of A buffer 1 at bars + 36 / + 39
     uint64_t *bar_a_full = bars + 0, *bar_a_free = bars + 3, *bar_d_full = bars + 6,
              *bar_d_free = bars + 8, *bar_wfull = bars + 10, *bar_wfree = bars + 12,
              *bar_s_full = bars + 14, *bar_s_empty = bars + 14 + kRing,
@@ -745,6 +752,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
         for (int i = 0; i < 3; ++i) {
             bfk::mbar_init(bar_a_full + i, 32 * kSplitWarps);
             bfk::mbar_init(bar_a_free + i, 1);
+            bfk::mbar_init(bar_a_full + 36 + i, 32 * kSplitWarps);
+            bfk::mbar_init(bar_a_free + 36 + i, 1);
         }
         bfk::mbar_init(bar_d_full + 0, 1);
         bfk::mbar_init(bar_d_full + 1, 1);
@@ -853,7 +862,11 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             // as soon as the previous tile's MMAs on it have completed and the tensor
             // pipe keeps running on the other terms meanwhile.
             // tcgen05.st is warp-collective: every lane stores (invalid rows store 0).
-            const uint32_t par = (uint32_t)((t & 1) ^ 1);
+            // A buffer of this tile, its barriers and the parity of its a_free wait
+            const int ab = kABufs == 2 ? (int)(t & 1) : 0;
+            uint64_t *a_full = bar_a_full + 36 * ab, *a_free = bar_a_free + 36 * ab;
+            const uint32_t par = kABufs == 2 ? (uint32_t)(((t >> 1) & 1) ^ 1) : (uint32_t)((t & 1) ^ 1);
+            const uint32_t a_base = a_lane + (uint32_t)(ab * 3 * kARegion);
             if (tl.g != cur_g || tl.job != cur_j) {
                 cur_g = tl.g;
                 cur_j = tl.job;
@@ -936,11 +949,11 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     #pragma unroll
                 for (int pass = 0; pass < 3; ++pass) {
                     const int term = pass == 2 ? 0 : pass + 1;
-                    bfk::mbar_wait(bar_a_free + term, par);
+                    bfk::mbar_wait(a_free + term, par);
                     tc::fence_after_sync();
                     if (term == 2 && !(cur_wf & 1)) {   // S3 is only multiplied for exact W
                         tc::fence_before_sync();
-                        mbar_arrive(bar_a_full + term);
+                        mbar_arrive(a_full + term);
                         continue;
                     }
                     // this warp's K chunks; up to f = 16 (<= 4 chunks) the second warp of each
@@ -971,11 +984,11 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                             }
                             h[e] = tc::pack_f16x2(y[0], y[1]);
                         }
-                        if constexpr (!(DBG & 4)) tc::tmem_st4(a_lane + term * kARegion + c0 / 2, h);
+                        if constexpr (!(DBG & 4)) tc::tmem_st4(a_base + term * kARegion + c0 / 2, h);
                     }
                     tc::tmem_st_wait();
                     tc::fence_before_sync();
-                    mbar_arrive(bar_a_full + term);
+                    mbar_arrive(a_full + term);
                 }
                 out_dom |= tiny < 0x3EFFFFFFu;   // a nonzero scaled component below 2^-1
                 if (valid && ((cur_wf & 2) || out_dom)) {
@@ -1107,6 +1120,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             const uint32_t u = (uint32_t)(t >> 1);
             const uint32_t d = tmem + kDCol0 + 128 * b;
             bfk::mbar_wait(bar_d_free + b, (u & 1) ^ 1);
+            const int ab = kABufs == 2 ? b : 0;            // A buffer of this tile (split's rule)
+            uint64_t *a_full = bar_a_full + 36 * ab, *a_free = bar_a_free + 36 * ab;
+            const uint32_t apar = kABufs == 2 ? (uint32_t)(u & 1) : (uint32_t)(t & 1);
+            const uint32_t a_tm = tmem + (uint32_t)(ab * 3 * kARegion);
             // MMA groups over K, small terms first, every one kind::f16 on fp16 terms of the
             // scaled operands (exact 11-bit x 11-bit products, fp32 accumulate):
             //   exact W (W2 == 0, e.g. identity / selection): S2 W1, S3 W1, S1 W1
@@ -1122,9 +1139,9 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     #pragma unroll
                 for (int grp = 0; grp < 3; ++grp) {
                     const int at = grp == 0 ? 1 : (grp == 1 ? 2 : 0);   // barrier: S2, S3, S1
-                    bfk::mbar_wait(bar_a_full + at, (uint32_t)(t & 1));
+                    bfk::mbar_wait(a_full + at, apar);
                     const bool s1w2 = grp == 1 && !exact;
-                    if (s1w2) bfk::mbar_wait(bar_a_full + 0, (uint32_t)(t & 1));
+                    if (s1w2) bfk::mbar_wait(a_full + 0, apar);
                     tc::fence_after_sync();
                     const int areg = s1w2 ? 0 : at;                     // A region read
                     const uint32_t boff = s1w2 ? (uint32_t)(KPc / 8) : 0u;  // W2 image after W1
@@ -1136,10 +1153,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                             const uint64_t desc = tc::smem_desc(
                                 w_base + (uint32_t)((boff + 2 * kb) * 16 * 128), 16 * 128, 128);
                             if constexpr (!(DBG & 1))
-                                tc::mma_f16_ts(d, tmem + areg * kARegion + kb * 8, desc, idesc,
+                                tc::mma_f16_ts(d, a_tm + areg * kARegion + kb * 8, desc, idesc,
                                                (grp | kb) != 0);
                         }
-                        if (grp < 2) tc::mma_commit(bar_a_free + at);
+                        if (grp < 2) tc::mma_commit(a_free + at);
                     }
                     __syncwarp();
                 }
@@ -1158,7 +1175,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 }
             }
             if (lane == 0) {
-                tc::mma_commit(bar_a_free + 0);
+                tc::mma_commit(a_free + 0);
                 tc::mma_commit(bar_d_full + b);
             }
             __syncwarp();
