@@ -299,9 +299,10 @@ def peak_basis(peaks: dict) -> str:
 
 # What the beamforming product is computed in (the line's "dtype" is its fp32 summary).
 ARITH = {
-    "tensor": "tcgen05 split precision, all kind::tf32 (exact products): S2*W1 + S1*W2 + S1*W1, fp32 "
-              "accumulate in TMEM (tf32-exact W: S2*W1 + S3*W1 + S1*W1, bit-exact copies); out-of-domain "
-              "blocks recomputed with FFMA arithmetic; DESIGN.md §7",
+    "tensor": "tcgen05 split precision on scaled operands (rows of S, groups of W by powers of two), "
+              "11-bit terms as fp16, kind::f16 MMAs (exact products): S2*W1 + S1*W2 + S1*W1, fp32 "
+              "accumulate in TMEM, exact unscale (exact W: S2*W1 + S3*W1 + S1*W1, bit-exact copies); "
+              "blocks outside the tensor domain recomputed with FFMA arithmetic; DESIGN.md §7",
     "ffma": "fp32 FFMA, 4 per complex MAC, k ascending",
 }
 
@@ -515,8 +516,8 @@ def run_ours(args):
     ai = wl.block_flops / blk_bytes
     variant = plan.variant.name.lower()
     # FFMA kernel: bound by the FP32 pipe when AI x HBM exceeds the FFMA peak.
-    # Tensor kernel: 3 KP/8 tf32 MMAs (K = 8) per 2-block tile at ~1.1 PFLOP/s
-    # nominal leave it HBM-bound at every f (tensor pipe < 50 % busy, profiles/).
+    # Tensor kernel: 3 KP/16 fp16 MMAs (K = 16, KP = 16 ceil(2f / 16)) per 2-block tile at
+    # ~2.2 PFLOP/s nominal leave it HBM-bound at every f (tensor pipe < 30 % busy).
     fp32_bound = variant == "ffma" and ai * hbm / 1e3 > peak_max
     # dram bytes of the same kernel from the committed `ncu --set full` capture
     # (profiles/traffic.json, per block), scaled to this launch's block count

@@ -95,16 +95,22 @@ typedef enum {
 
 /* Kernel variant.  Both compute the same product within the same contract.
  *   BF_VARIANT_FFMA    CUDA-core kernel: 4 fp32 FFMA per complex MAC.
- *   BF_VARIANT_TENSOR  tcgen05 tensor-core kernel: S split exactly into 3 terms
- *                      of 11-bit significands, W into 2 (+ a 2^-22 residual);
- *                      S2 W1 + S1 W2 + S1 W1 as kind::tf32 MMAs (S2 W1 + S3 W1 +
- *                      S1 W1 when W is exactly tf32), every product exact, fp32
- *                      accumulation in TMEM (error-compensated split precision,
- *                      BASELINE.json north_star item 2).  Tensor domain: nonzero
- *                      |s|, |w| in [2^-40, 2^40); blocks with an S value outside
- *                      it (or NaN / Inf) and blocks of groups with a W entry
- *                      outside it are recomputed inside the same launch with the
- *                      FFMA kernel's arithmetic (bitwise equal to BF_VARIANT_FFMA).
+ *   BF_VARIANT_TENSOR  tcgen05 tensor-core kernel: every row of S (one RE) and
+ *                      every precoder group scaled by a power of two into fp16's
+ *                      range, S split exactly into 3 terms of 11-bit significands,
+ *                      W into 2 (+ a 2^-22 residual), the terms as fp16; S2 W1 +
+ *                      S1 W2 + S1 W1 as kind::f16 MMAs (S2 W1 + S3 W1 + S1 W1 when W
+ *                      is exact in one fp16 term), every product exact, fp32
+ *                      accumulation in TMEM, exact unscale (error-compensated split
+ *                      precision, BASELINE.json north_star item 2).
+ *                      Tensor domain: per row of S the largest element
+ *                      max(|re|, |im|) 0 or in [2^-40, 2^40), no NaN, every nonzero
+ *                      element within 2^14 of the row's largest component (for
+ *                      exact W every nonzero component within 2^15); per group of W
+ *                      the same with entries in [2^-40, 2^40).  Blocks with a row
+ *                      outside it and blocks of groups outside it are recomputed
+ *                      inside the same launch with the FFMA kernel's arithmetic
+ *                      (bitwise equal to BF_VARIANT_FFMA).
  *   BF_VARIANT_AUTO    per-(f, layout) choice from the measured variant table
  *                      (default): FFMA at small f, tensor above; FFMA whenever a
  *                      precoder entry lies outside the tensor domain. */

@@ -1,4 +1,4 @@
-// bf_tc.cuh — sm_100a tensor-core (tcgen05, kind::tf32) beamforming kernel.
+// bf_tc.cuh — sm_100a tensor-core (tcgen05, kind::f16 on split fp16 terms) beamforming kernel.
 //
 // Same operation as bf_ffma.cuh: R[n] = W[g(n)] x S[n], complex
 // fp32, 64 antennas, 60 REs, F flows.  SURVEY.md §8(f) row 2: a split-precision
@@ -11,19 +11,22 @@
 //                      n = 2i  : kk=2k -> Wr[i][k],  kk=2k+1 -> -Wi[i][k]
 //                      n = 2i+1: kk=2k -> Wi[i][k],  kk=2k+1 ->  Wr[i][k]
 //   D [m][n]   (TMEM)  = R[blk][i][j] re / im, fp32 accumulate.
-// Split precision (error-compensated, BASELINE.json north_star item 2):
-// S = S1 + S2 + S3 exactly (three tf32 terms, each rounded to 11 bits),
-// W' = W1 + W2 + W3 (W1, W2 tf32, |W3| <= 2^-22 |W'|, split once per W).  Every
-// product is a tf32 x tf32 product, exact in the fp32 accumulator.  General W:
-// S2 W1, S1 W2, then S1 W1 (dropped terms S3 W1 + S2 W2 + S W3 <= 3 2^-22 |s||w|);
-// when the group's W is exactly tf32 (W2 == 0: identity, selection, small integers)
-// S2 W1, S3 W1, S1 W1 = S W exactly, which makes copy-like precoders bit-exact.
-// The split of tile t+1 rewrites each term region as soon as tile t's MMAs on it
-// completed.  DESIGN.md §7 bounds the error by ~4.1e-6 T at f = 36 (complex modulus,
-// with the accumulation model measured by tools/tc_acc_probe).
-// Tensor domain: the bound needs every product term normal, so the kernel checks every
-// S value it splits (nonzero |s| in [2^-40, 2^40)) and bf_set_precoders every W entry;
-// blocks outside (incl. NaN / Inf) are recomputed at the end of the launch by the CTA
+// Split precision (error-compensated, BASELINE.json north_star item 2): every row of A
+// (one RE) is scaled by 2^sg and every precoder group by 2^tau so the largest component
+// lies in [2^14, 2^15); S' = S1 + S2 + S3 exactly (11-bit terms), W' = W1 + W2 + W3
+// (11-bit W1, W2, |W3| <= 2^-22 |W'|, split once per bf_set_precoders), every term as
+// fp16 (exact in fp16's normal range; the tensor domain bounds the rest).  Every product
+// is an fp16 x fp16 product, exact in the fp32 accumulator (kind::f16, K = 16).  General
+// W: S2 W1, S1 W2, then S1 W1 (dropped terms S3 W1 + S2 W2 + S W3 <= 3 2^-22 |s||w|);
+// when the group is exact in one fp16 term (W2 == 0: identity, selection, small
+// integers) S2 W1, S3 W1, S1 W1 = S W exactly, which makes copy-like precoders
+// bit-exact.  The epilogue undoes 2^(sg + tau) with one exact multiply.
+// bounds the error by 5.8e-6 T at f = 36 (complex modulus, with the accumulation model
+// measured by tools/tc_acc_probe).
+// Tensor domain: per row the largest element in [2^-40, 2^40), no NaN, every nonzero
+// element within 2^14 of the largest component (exact W: every nonzero component within
+// 2^15) — tested by the split warps as they read S; per group of W the same, tested by
+// bf_set_precoders.  Blocks outside are recomputed at the end of the launch by the CTA
 // that owns them with the FFMA kernel's arithmetic (fix_block), bit for bit.
 //
 // One CTA (18 warps) per SM, persistent over a cost-balanced range of the
@@ -35,8 +38,9 @@
 //              memory allows: the next group's image loads while the current one's
 //              MMAs run);
 //   warps 0-7  split (two per TMEM lane quarter, each half of the K columns above
-//              f = 12): LDS S (conflict-free, one RE column per lane), split into
-//              the terms, tcgen05.st into the A regions (one TMEM lane per RE);
+//              f = 16): LDS S (conflict-free, one RE column per lane), the row's
+//              scale (the two halves exchange their maxima), split into the terms,
+//              tcgen05.st of fp16 pairs into the A regions (one TMEM lane per RE);
 //   warp 8     MMA issuer (one thread);
 //   warps 9-16 epilogue (two per lane quarter, half the D columns each): tcgen05.ld
 //              of the thread's D row half, release of the TMEM buffer, then the
@@ -44,8 +48,9 @@
 //              global layout and stored by one thread with one bulk copy per block
 //              (int16 output at f <= 12: direct 8-byte stores instead).
 // Shared memory per f: TcSmem (W buffers, S ring depth, R stage).
-// TMEM: A terms at columns [0, 3 KP) (KP of f = 36 for the batch kernel), D double buffer at
-// [256, 384), [384, 512).
+// TMEM: two sets of A terms (fp16 pairs: KP / 2 columns per term; KP of f = 36 for the
+// batch kernel) at [0, 3 KP / 2) and [3 KP / 2, 3 KP), D double buffer at [256, 384),
+// [384, 512).
 #pragma once
 #include <cstddef>
 #include <cstdint>
