@@ -290,10 +290,12 @@ bf_status bf_server_submit(bf_server_t s, const void *S_dev, void *R_dev, int64_
 bf_status bf_server_wait(bf_server_t s, uint64_t ticket, double timeout_s);
 bf_status bf_server_slot_time(bf_server_t s, uint64_t ticket, double *device_us);
 bf_status bf_server_stop(bf_server_t s);
-/* Instrumentation: the timeline of CTA 0's part of the last done slot, microseconds after
- * CTA 0 saw its doorbell: [0] 0, [1] descriptor published to the CTA, [2] first S block in
- * shared memory, [3] first D tile ready, [4] last R store issued, [5] R stores complete,
- * [6] slot counted (-1: not reached).  us[0..min(n, 8)). */
+/* Instrumentation (library built with -DBFTC_SRV_TRACE=1; otherwise -1 entries): the
+ * timeline of CTA 0's part of the last done slot, microseconds after CTA 0 saw its
+ * doorbell: [0] 0, [1] descriptor published to the CTA, [2] first S block in shared
+ * memory, [3] first D tile ready, [4] last R store issued, [5] R stores complete, [6] slot
+ * counted (-1: not reached); then [8 + c] CTA c's slot start and [168 + c] its count
+ * (c < 160).  us[0..min(n, 328)). */
 bf_status bf_server_trace(bf_server_t s, double *us, int n);
 bf_status bf_server_destroy(bf_server_t s);
 

@@ -1117,13 +1117,18 @@ bf_status server_post(bf_server_t s, const void *S, void *R, int64_t n, int stop
                                         : cuda_fail(q, "slot server");
         }
     }
-    volatile bftc::SrvSlotDesc *d = &vmb(s)->desc[k % bftc::kSrvRing];
-    d->S = reinterpret_cast<unsigned long long>(S);
-    d->R = reinterpret_cast<unsigned long long>(R);
-    d->n = n;
-    d->stop = stop;
-    std::atomic_thread_fence(std::memory_order_seq_cst);   // descriptor before seq (x86: TSO)
-    vmb(s)->seq = k;
+    // the descriptor as LL words (8-byte stores: data | slot number << 32), in any order:
+    // the server takes it once every word carries k (bf_tc.cuh kDescWords)
+    volatile unsigned long long *d = vmb(s)->desc[k % bftc::kSrvRing];
+    const unsigned long long pS = reinterpret_cast<unsigned long long>(S);
+    const unsigned long long pR = reinterpret_cast<unsigned long long>(R);
+    d[0] = bftc::ll_word((unsigned int)pS, k);
+    d[1] = bftc::ll_word((unsigned int)(pS >> 32), k);
+    d[2] = bftc::ll_word((unsigned int)pR, k);
+    d[3] = bftc::ll_word((unsigned int)(pR >> 32), k);
+    d[4] = bftc::ll_word((unsigned int)n, k);
+    d[5] = bftc::ll_word((unsigned int)stop, k);
+    std::atomic_thread_fence(std::memory_order_seq_cst);
     s->next = k;
     if (ticket) *ticket = k;
     return BF_OK;
@@ -1228,8 +1233,9 @@ bf_status bf_server_slot_time(bf_server_t s, uint64_t ticket, double *device_us)
 bf_status bf_server_trace(bf_server_t s, double *us, int n) {
     if (!s || !us || n < 0) return fail(BF_ERR_INVALID_VALUE, "bad argument");
     const unsigned long long t0 = vmb(s)->trace[0];
-    for (int i = 0; i < n && i < 8; ++i) {
-        const unsigned long long t = vmb(s)->trace[i];
+    for (int i = 0; i < n && i < 8 + 2 * 160; ++i) {   // trace, then per-CTA seen / done
+        const unsigned long long t = i < 8 ? vmb(s)->trace[i]
+                                           : (i < 168 ? vmb(s)->cta_seen[i - 8] : vmb(s)->cta_done[i - 168]);
         us[i] = t ? (double)(long long)(t - t0) * 1e-3 : -1.0;
     }
     return BF_OK;

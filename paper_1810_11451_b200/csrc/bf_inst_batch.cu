@@ -13,8 +13,8 @@ void bf_register_batch(BfKernelTable &tc) {
 
 // The slot-server instantiations (bf_server_*): the same kernel, jobs from the mailbox.
 void bf_register_server(BfKernelEntry (&srv)[4]) {
-    srv[0] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<0, 0, 0, true>), bftc::TcSmem<0>::kBytes};
-    srv[1] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<0, 1, 0, true>), bftc::TcSmem<0>::kBytes};
-    srv[2] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<0, 2, 0, true>), bftc::TcSmem<0>::kBytes};
-    srv[3] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<0, 3, 0, true>), bftc::TcSmem<0>::kBytes};
+    srv[0] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<0, 0, 0, true>), bftc::TcSmem<0, true>::kBytes};
+    srv[1] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<0, 1, 0, true>), bftc::TcSmem<0, true>::kBytes};
+    srv[2] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<0, 2, 0, true>), bftc::TcSmem<0, true>::kBytes};
+    srv[3] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<0, 3, 0, true>), bftc::TcSmem<0, true>::kBytes};
 }

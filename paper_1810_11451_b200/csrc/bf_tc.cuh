@@ -107,8 +107,11 @@ constexpr int kRelRange = 14;
 // kMaxJobs, e.g. consecutive streaming chunks of different cells), each split
 // over all CTAs; the kernel template's F is the flow count of every job, or 0
 // for the batch kernel whose jobs carry their own f (1..36).
-constexpr int kMaxJobs = 16;
-constexpr int kOffsSlots = 1028;       // shared group-offset slots: sum over jobs of (n_groups + 2)
+#ifndef BFTC_MAX_JOBS
+#define BFTC_MAX_JOBS 16
+#endif
+constexpr int kMaxJobs = BFTC_MAX_JOBS;
+constexpr int kOffsSlots = kMaxJobs <= 16 ? 1028 : 2052;   // shared group-offset slots: sum over jobs of (n_groups + 2)
 constexpr int kFixCap = 64;            // out-of-domain blocks a CTA lists (more: rescan its range)
 // Tensor domain of S and W: zero, or 2^-40 <= |x| < 2^40, as fp32 bit
 // patterns without the sign.  Inside it every product of split terms is a normal fp32
@@ -147,40 +150,50 @@ constexpr int kSrvRing = 4;                // slots in flight (descriptor rings)
 #ifndef BFTC_SRV_DIRECT
 #define BFTC_SRV_DIRECT 0   // 1: every CTA polls the host mailbox (measured 47x slower: PCIe contention)
 #endif
-struct __align__(16) SrvSlotDesc {
-    unsigned long long S, R;               // device pointers of the slot
-    long long n;                           // blocks
-    int stop;                              // 1: exit after the slots before this one
-    int pad;
-};
-// the descriptor as two 16-byte words (one PCIe read each, issued together)
-__device__ __forceinline__ void ld_desc_sys(const SrvSlotDesc *d, unsigned long long &S,
-                                            unsigned long long &R, long long &n, int &stop) {
-    unsigned long long a0, a1, b0, b1;
-    asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%4];\n\t"
-                 "ld.relaxed.sys.global.v2.u64 {%2, %3}, [%5];"
-                 : "=l"(a0), "=l"(a1), "=l"(b0), "=l"(b1)
-                 : "l"(&d->S), "l"(&d->n) : "memory");
-    S = a0;
-    R = a1;
-    n = (long long)b0;
-    stop = (int)(b1 & 0xFFFFFFFFull);
+// Slot descriptors travel as LL words (the NCCL "LL" idea): each 8-byte word carries 32
+// bits of data and the 32-bit slot number, and 8-byte aligned stores are single-copy
+// atomic, so a reader that sees the expected slot number in every word holds the whole
+// descriptor — no fence between data and flag on either hop (host -> CTA 0 over PCIe,
+// CTA 0 -> the other CTAs through L2).
+constexpr int kDescWords = 6;              // S lo, S hi, R lo, R hi, n, stop
+__host__ __device__ inline unsigned long long ll_word(unsigned int data, unsigned long long k) {
+    return ((unsigned long long)(unsigned int)k << 32) | data;
+}
+// the six words of one descriptor, three 16-byte loads issued together
+template <bool SYS>
+__device__ __forceinline__ void ld_ll6(const unsigned long long *w, unsigned long long (&v)[kDescWords]) {
+    if (SYS)
+        asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%6];\n\t"
+                     "ld.relaxed.sys.global.v2.u64 {%2, %3}, [%6+16];\n\t"
+                     "ld.relaxed.sys.global.v2.u64 {%4, %5}, [%6+32];"
+                     : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]), "=l"(v[4]), "=l"(v[5])
+                     : "l"(w) : "memory");
+    else
+        asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%6];\n\t"
+                     "ld.relaxed.gpu.global.v2.u64 {%2, %3}, [%6+16];\n\t"
+                     "ld.relaxed.gpu.global.v2.u64 {%4, %5}, [%6+32];"
+                     : "=l"(v[0]), "=l"(v[1]), "=l"(v[2]), "=l"(v[3]), "=l"(v[4]), "=l"(v[5])
+                     : "l"(w) : "memory");
+}
+__device__ __forceinline__ bool ll_complete(const unsigned long long (&v)[kDescWords], unsigned long long k) {
+    bool ok = true;
+#pragma unroll
+    for (int i = 0; i < kDescWords; ++i) ok &= (unsigned int)(v[i] >> 32) == (unsigned int)k;
+    return ok;
 }
 struct SrvMailbox {
-    unsigned long long seq;                // written by the host after desc[seq % ring]
-    SrvSlotDesc desc[kSrvRing];
+    __align__(16) unsigned long long desc[kSrvRing][kDescWords];   // host-written LL words
     int error;                             // device: a slot held values outside the tensor domain
     int pad;
     unsigned long long done;               // device: last completed slot
     unsigned long long t_seen[kSrvRing];   // device globaltimer: CTA 0 saw slot k (k % ring)
     unsigned long long t_done[kSrvRing];   // device globaltimer: slot k complete
     unsigned long long trace[8];           // CTA 0, last slot: see srv_trace
+    unsigned long long cta_seen[160];      // BFTC_SRV_TRACE builds: every CTA, last slot
+    unsigned long long cta_done[160];
 };
 struct SrvDev {
-    unsigned long long seq;                // re-broadcast of the mailbox
-    unsigned long long S[kSrvRing], R[kSrvRing];
-    long long n[kSrvRing];
-    int stop[kSrvRing];
+    __align__(16) unsigned long long desc[kSrvRing][kDescWords];   // CTA 0's re-broadcast
     unsigned int done_cnt[kSrvRing];
 };
 struct SrvPtrs {
@@ -202,7 +215,7 @@ template <int F>
 using TcParamsOf = TcParamsN<F == 0 ? kMaxJobs : 1>;
 static_assert(offsetof(TcParamsN<1>, job) == offsetof(TcParams, job), "TcParams prefix layout");
 
-template <int F>
+template <int F, bool SRV = false>
 struct TcSmem {
     static constexpr int FS = F > 0 ? F : 36;          // sizing flow count (36 for runtime f)
     static constexpr int KP = kp_of(FS);
@@ -227,14 +240,17 @@ struct TcSmem {
     static constexpr int kFitA = (kSmemLimit - 2 * kWBytes - kMisc - kRStageBytes - 128) / (2 * kSBlock);
     static constexpr int kFitB = (kSmemLimit - kWBytes - kMisc - kRStageBytes - 128) / (2 * kSBlock);
     static constexpr bool kStageR = kFitA >= 2 || kFitB >= 2;
-    static constexpr int kWBufs = (kFitA < 2 && kFitB >= 2) ? 1 : 2;
+    // (the slot server keeps one group's image for good: one W buffer, the space to S)
+    static constexpr int kWBufs = SRV || (kFitA < 2 && kFitB >= 2) ? 1 : 2;
     static constexpr int kFixed = kWBufs * kWBytes + kMisc + (kStageR ? kRStageBytes + 128 : 0);
     static constexpr int kStagesFit = (kSmemLimit - kFixed) / (2 * kSBlock);
     // S ring depth: with the staged epilogue a deeper ring measured slower above f = 12
     // (e.g. f = 20: 0.87 of the copy bandwidth with 4 stages, 0.94 with 2; f <= 12 gains
     // from 4 — tools/sweep_f.py, BFTC_MAX_STAGES builds, profiles/r01_sweep_stages_v5.txt)
     // (fp16 output, whose stores are half the bytes, keeps the deepest ring that fits)
-    static constexpr int kMaxS = (F > 0 && F <= 12) ? kMaxStages : (kMaxStages < 2 ? kMaxStages : 2);
+    // (slot server: latency, not bandwidth — every stage that fits, so a CTA's few tiles of a
+    // small slot all load at once)
+    static constexpr int kMaxS = (SRV || (F > 0 && F <= 12)) ? kMaxStages : (kMaxStages < 2 ? kMaxStages : 2);
     static constexpr int kStagesAlloc = kStagesFit < kMaxStages ? kStagesFit : kMaxStages;
     static constexpr int kStages = kStagesFit < kMaxS ? kStagesFit : kMaxS;
     static_assert(kStages >= 2, "S ring needs two stages");
@@ -527,8 +543,13 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // Timeline of CTA 0's part of the last slot (bf_server_trace), %globaltimer ns:
 // 0 doorbell seen, 1 descriptor published, 2 first S in shared memory (split), 3 first
 // D ready (epilogue), 4 last bulk store issued, 5 stores complete, 6 counted.
+#ifndef BFTC_SRV_TRACE
+#define BFTC_SRV_TRACE 0   // 1: CTA 0 timeline of the last slot (tools/server_exp.py)
+#endif
 __device__ __forceinline__ void srv_trace(const SrvPtrs &sp, int i) {
-    if (blockIdx.x == 0) sp.mb->trace[i] = globaltimer();
+    // (host-memory writes: a later fence in the same thread waits for them, so they stay
+    // out of the product build)
+    if (BFTC_SRV_TRACE && blockIdx.x == 0) sp.mb->trace[i] = globaltimer();
 }
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
     unsigned long long v;
@@ -557,42 +578,49 @@ __device__ __forceinline__ bool srv_fill_slot(const SrvPtrs &sp, const TcJob &tm
     SrvDev *dv = sp.dev;
     const unsigned long long t0 = globaltimer();
     bool stop = false;
+    unsigned long long v[kDescWords];
 #if BFTC_SRV_DIRECT
     // every CTA polls the host mailbox itself (one PCIe round trip, no re-broadcast hop)
-    while (ld_acquire_sys(&sp.mb->seq) < k) {
+    for (;;) {
+        ld_ll6<true>(sp.mb->desc[e], v);
+        if (ll_complete(v, k)) break;
         if ((long long)(globaltimer() - t0) > sp.timeout_ns) { stop = true; break; }
     }
-    if (blockIdx.x == 0 && !stop) sp.mb->t_seen[e] = sp.mb->trace[0] = globaltimer();
-    const volatile SrvSlotDesc *vdesc = &sp.mb->desc[e];
-    const unsigned long long dS = stop ? 0ull : vdesc->S, dR = stop ? 0ull : vdesc->R;
-    const long long dn = stop ? 0ll : vdesc->n;
-    stop = stop || vdesc->stop != 0;
+    if (blockIdx.x == 0 && !stop) sp.mb->t_seen[e] = globaltimer();
     (void)dv;
 #else
     if (blockIdx.x == 0) {
-        while (ld_acquire_sys(&sp.mb->seq) < k) {
+        for (;;) {
+            ld_ll6<true>(sp.mb->desc[e], v);
+            if (ll_complete(v, k)) break;
             if ((long long)(globaltimer() - t0) > sp.timeout_ns) { stop = true; break; }
         }
-        unsigned long long hS = 0, hR = 0;
-        long long hn = 0;
-        int hstop = 1;
-        if (!stop) ld_desc_sys(&sp.mb->desc[e], hS, hR, hn, hstop);   // after the acquire of seq
-        dv->S[e] = hS;
-        dv->R[e] = hR;
-        dv->n[e] = hn;
-        dv->stop[e] = stop ? 1 : hstop;
-        if (!stop) sp.mb->t_seen[e] = sp.mb->trace[0] = globaltimer();
-        st_release_gpu(&dv->seq, k);
+        const unsigned long long t_seen = globaltimer();
+        if (stop)
+            for (int i = 0; i < kDescWords; ++i) v[i] = ll_word(i == 5 ? 1u : 0u, k);
+        // re-broadcast: relaxed 8-byte stores, the slot number in every word
+        asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};\n\t"
+                     "st.relaxed.gpu.global.v2.u64 [%0+16], {%3, %4};\n\t"
+                     "st.relaxed.gpu.global.v2.u64 [%0+32], {%5, %6};"
+                     ::"l"(dv->desc[e]), "l"(v[0]), "l"(v[1]), "l"(v[2]), "l"(v[3]), "l"(v[4]), "l"(v[5])
+                     : "memory");
+        if (!stop) {
+            sp.mb->t_seen[e] = t_seen;
+            if (BFTC_SRV_TRACE) sp.mb->trace[0] = t_seen;
+        }
     } else {
-        while (ld_acquire_gpu(&dv->seq) < k) {
+        for (;;) {
+            ld_ll6<false>(dv->desc[e], v);
+            if (ll_complete(v, k)) break;
             if ((long long)(globaltimer() - t0) > sp.timeout_ns) { stop = true; break; }
         }
     }
-    const volatile SrvDev *vd = dv;
-    const unsigned long long dS = stop ? 0ull : vd->S[e], dR = stop ? 0ull : vd->R[e];
-    const long long dn = stop ? 0ll : vd->n[e];
-    stop = stop || vd->stop[e] != 0;
 #endif
+    if (BFTC_SRV_TRACE && !stop && blockIdx.x < 160) sp.mb->cta_seen[blockIdx.x] = globaltimer();
+    const unsigned long long dS = stop ? 0ull : ((v[0] & 0xFFFFFFFFull) | (v[1] << 32));
+    const unsigned long long dR = stop ? 0ull : ((v[2] & 0xFFFFFFFFull) | (v[3] << 32));
+    const long long dn = stop ? 0ll : (long long)(unsigned int)v[4];
+    stop = stop || (unsigned int)v[5] != 0u;
     JobCtx &J = ring[e];
     J.Wimg = tmpl.Wimg;
     J.Wp = tmpl.Wp;
@@ -636,7 +664,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 template <int F, int LAYOUT, int DBG = 0, bool SRV = false>
 __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> p) {
     static_assert(!SRV || F == 0, "the slot server runs the runtime-f kernel");
-    using L = TcSmem<F>;
+    using L = TcSmem<F, SRV>;
     // TMEM column stride of the three A regions: fixed across the jobs of a launch
     // (the split of a job's first tile must not overlap the previous job's regions
     // that its last MMAs may still read).
@@ -810,13 +838,18 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                     bulk_wait_all();
                     srv_trace(p.srv, 5);
                     asm volatile("fence.proxy.async.global;" ::: "memory");
-                    __threadfence();
                     const int e = (int)(slot % kSrvRing);
                     if (*fix_n > 0) atomicExch(&p.srv.mb->error, 1);
-                    const unsigned int old = atomicAdd(&p.srv.dev->done_cnt[e], 1u);
+                    // count the CTA (acq_rel: its R before the count; the last one sees all)
+                    unsigned int old;
+                    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                                 : "=r"(old) : "l"(&p.srv.dev->done_cnt[e]) : "memory");
                     srv_trace(p.srv, 6);
+                    if (BFTC_SRV_TRACE && blockIdx.x < 160) p.srv.mb->cta_done[blockIdx.x] = globaltimer();
                     if (old == (unsigned)(((slot - 1) / kSrvRing + 1) * gridDim.x) - 1u) {
-                        __threadfence_system();
+                        // the last CTA: every CTA's R is ordered before its count (acq_rel), and
+                        // the system-scope release of `done` makes them visible to the host
+                        // (cumulativity) — no separate system fence
                         p.srv.mb->t_done[e] = globaltimer();
                         st_release_sys(&p.srv.mb->done, slot);
                     }

@@ -266,10 +266,12 @@ class Server:
         check(lib().bf_server_slot_time(self._h, ctypes.c_uint64(ticket), ctypes.byref(v)))
         return v.value
 
-    def trace_us(self) -> list:
-        """bf_server_trace: CTA 0's timeline of the last done slot (us after its doorbell)."""
-        arr = (ctypes.c_double * 8)()
-        check(lib().bf_server_trace(self._h, arr, 8))
+    def trace_us(self, per_cta: bool = False) -> list:
+        """bf_server_trace: CTA 0's timeline of the last done slot (us after its doorbell);
+        per_cta: then every CTA's slot start and count (BFTC_SRV_TRACE builds only)."""
+        n = 8 + (320 if per_cta else 0)
+        arr = (ctypes.c_double * n)()
+        check(lib().bf_server_trace(self._h, arr, n))
         return list(arr)
 
     def stop(self) -> None:

@@ -25,6 +25,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--slots", type=int, default=100)
     ap.add_argument("--f", type=int, default=36)
+    ap.add_argument("--per-cta", action="store_true", help="per-CTA start / count (BFTC_SRV_TRACE build)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     f = a.f
@@ -48,8 +49,13 @@ def main():
                 srv.wait(t, timeout_s=30)
                 if i >= 10:
                     d.append(srv.slot_time_us(t))
-                    tr.append(srv.trace_us())
+                    tr.append(srv.trace_us(per_cta=a.per_cta))
             tiles = (n + 1) // 2
+            if a.per_cta:
+                seen = [statistics.median(x[8 + c] for x in tr) for c in range(148)]
+                done = [statistics.median(x[168 + c] for x in tr) for c in range(148)]
+                print(json.dumps({"n": n, "cta_seen_us": [round(v, 2) for v in seen],
+                                  "cta_done_us": [round(v, 2) for v in done]}), flush=True)
             print(json.dumps({"n": n, "tiles_per_cta": tiles / 148, "device_us_median": statistics.median(d),
                               "device_us_min": min(d), "bytes_us_at_6.5TBps": n * 48000 / 6.5e6,
                               "cta0_trace_us_median": [statistics.median(x[j] for x in tr) for j in range(7)]}),
