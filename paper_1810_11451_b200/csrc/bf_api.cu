@@ -52,8 +52,11 @@ constexpr size_t kMaxProfEvents = 1 << 16;  // timed launches kept between kerne
 // planar f <= 6 (within +-4 %), fp16 output f <= 3 (FFMA 5-16 % ahead), int16 output
 // f <= 3 (FFMA 0.32 vs 0.43 ms at f = 1; profiles/r01_sweep_auto_v7.jsonl, 18-warp tensor
 // kernel).  From there on
-// the tensor kernel wins, by 2.2-2.6x at f = 36.
-constexpr int kAutoTensorMinF[4] = {2, 7, 4, 4};   // [layout]
+// the tensor kernel wins, by 2.2-2.6x at f = 36.  Round 2 (fp16-term tensor kernel,
+// profiles/r02_sweep_auto_f16.txt): interleaved f = 1 FFMA 0.553 vs 0.560 ms, planar
+// within +-3 % up to f = 6, fp16 and int16 output FFMA ahead up to f = 4 (0.36 vs 0.37,
+// 0.45 vs 0.47 ms), the tensor kernel from f = 5.
+constexpr int kAutoTensorMinF[4] = {2, 7, 5, 5};   // [layout]
 // bf_apply_batch: 1 = one contiguous cost range of all the launch's jobs per CTA, 0 = every
 // job split over all CTAs
 constexpr int kBatchSplit = 1;
