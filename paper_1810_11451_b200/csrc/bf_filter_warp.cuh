@@ -222,8 +222,18 @@ __global__ void __launch_bounds__(kThreads, MINC) filter_warp_kernel(const FPara
             }
         }
         float2 *dst = p.y + sig * kN;
+        if (p.mode == 0) {
+            // the conj of the conj trick as a sign flip on the integer pipe (LOP3), not an
+            // FMUL2 on the FMA pipe the transforms keep ~2/3 busy
 #pragma unroll
-        for (int s = 0; s < 64; ++s) __stcs(dst + l + 32 * s, up(mul2(a[s], oscale)));
+            for (int s = 0; s < 64; ++s) {
+                const float2 v = up(a[s]);
+                __stcs(dst + l + 32 * s, make_float2(v.x, __uint_as_float(__float_as_uint(v.y) ^ 0x80000000u)));
+            }
+        } else {
+#pragma unroll
+            for (int s = 0; s < 64; ++s) __stcs(dst + l + 32 * s, up(mul2(a[s], oscale)));
+        }
     }
 }
 
