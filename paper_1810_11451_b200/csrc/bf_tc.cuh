@@ -1241,6 +1241,13 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             const bool valid = m < 120 && bsel < tl.cnt;
             const int64_t blk = valid ? block_of(J, tl.item + bsel) : 0;
             float *Rb = J.R + blk * (int64_t)(bfk::r_block_bytes(LAYOUT) / 4);
+            // the bulk-storing thread's block ids, loaded before the wait (routed order: global
+            // loads whose latency would otherwise delay the stores)
+            int64_t sblk[2] = {0, 0};
+            if (kStageR && e0) {
+                sblk[0] = block_of(J, tl.item);
+                if (tl.cnt > 1) sblk[1] = block_of(J, tl.item + 1);
+            }
             bfk::mbar_wait(bar_d_full + b, u & 1);
             tc::fence_after_sync();
             if (SRV && fresh) {
@@ -1341,7 +1348,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 epi_bar_sync();
                 if (e0) {
                     for (int b2 = 0; b2 < tl.cnt; ++b2)
-                        bulk_s2g(J.R + block_of(J, tl.item + b2) * (int64_t)rbf, Rst + b2 * rbf,
+                        bulk_s2g(J.R + sblk[b2] * (int64_t)rbf, Rst + b2 * rbf,
                                  (uint32_t)bfk::r_block_bytes(LAYOUT), pol_r);
                     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
