@@ -341,3 +341,49 @@ def test_subnormal_components_stay_on_the_tensor_path():
     R_ref, T, _ = oracle.beamform(W, S, None, n_threads=NT)
     worst = assert_parity(R, R_ref, T, what="subnormal components")
     assert worst <= TC_BOUND, worst
+
+
+@pytest.mark.parametrize("exact_w", [False, True], ids=["general_w", "exact_w"])
+def test_relative_range_edges(exact_w):
+    """The relative-range rule at its edges: a row whose smallest nonzero
+    element sits 14 binades below the row's largest component is inside the tensor domain,
+    15 binades is outside (the block is the FFMA kernel's bits); for exact W every nonzero
+    component must also lie within 15 binades (block 8: an element inside, one of its
+    components 16 binades below).  The emulation's row_in_domain decides every block the same
+    way, and in-domain blocks equal the emulated kernel bit for bit."""
+    f, n = 12, 9
+    if exact_w:
+        W = np.zeros((1, 64, f), np.complex64)
+        W[0, np.arange(64), np.arange(64) % f] = 1
+    else:
+        W = syn.precoders(71, 0, 1, 64, f, "none")
+    S = syn.qam_symbols(71, 0, np.arange(n), f, 60, 4)          # QPSK: components 2^-0.5
+    big = np.float32(2.0 ** 3)
+    for b, d in enumerate([13, 14, 15, 16]):                   # binades below the largest
+        S[2 * b, 0, 5] = big * (1 + 1j)
+        S[2 * b, 3, 5] = np.float32(2.0 ** (3 - d)) * (1 + 0j)
+        S[2 * b + 1, 0, 9] = big * (1 + 1j)
+        S[2 * b + 1, 4, 9] = np.float32(2.0 ** (3 - d)) * (1 + 0.5j)
+    S[8, 0, 5] = big * (1 + 1j)
+    S[8, 2, 5] = np.float32(2.0 ** -10) + 1j * np.float32(2.0 ** -13)
+    R, _ = run(W, S)
+    Rf, _ = run(W, S, variant=Variant.FFMA)
+    tau, exact, ok = tc_emulate.group_scale(W[0].real, W[0].imag)
+    assert ok and exact == exact_w
+    decisions = []
+    for b in range(n):
+        inside = bool(tc_emulate.row_in_domain(S[b].real.T, S[b].imag.T, exact).all())
+        decisions.append(inside)
+        if not inside:
+            assert_bitwise(R[b], Rf[b], f"block {b}: outside -> FFMA fix-up")
+            continue
+        sr = np.broadcast_to(S[b].real.T[None], (64, 60, f))
+        si = np.broadcast_to(S[b].imag.T[None], (64, 60, f))
+        wr = np.broadcast_to(W[0].real[:, None, :], (64, 60, f))
+        wi = np.broadcast_to(W[0].imag[:, None, :], (64, 60, f))
+        re, im = tc_emulate.kernel_element(sr, si, wr, wi, tau, exact)
+        assert_bitwise(R[b].real.copy(), re, f"block {b} re")
+        assert_bitwise(R[b].imag.copy(), im, f"block {b} im")
+    assert decisions == [True] * 4 + [False] * 4 + [not exact_w], decisions
+    R_ref, T, _ = oracle.beamform(W, S, None, n_threads=NT)
+    assert_parity(R, R_ref, T, what="relative-range edges")
