@@ -262,10 +262,13 @@ def test_fixup_list_overflow_rescans():
     assert_parity(Rt[sel], R_ref, T, what="overflow rescan")
 
 
-@pytest.mark.parametrize("value", [2.0 ** 45, 2.0 ** -45, float("inf")], ids=["huge", "tiny", "inf"])
+@pytest.mark.parametrize("value", [2.0 ** 45, 2.0 ** -45, 2.0 ** -17, float("inf")],
+                         ids=["huge", "tiny", "rel_small", "inf"])
 def test_out_of_domain_precoders(value):
-    """A group with a W entry outside the tensor domain: AUTO resolves to the FFMA kernel;
-    an explicit tensor plan fixes that group's blocks up (bitwise FFMA), others unchanged."""
+    """A group with a W entry outside the tensor domain (absolute range, or — rel_small — an
+    element far more than 2^14 below the group's largest component): AUTO resolves to the
+    FFMA kernel; an explicit tensor plan fixes that group's blocks up (bitwise FFMA), others
+    unchanged."""
     f, n, G = 12, 400, 3
     W = syn.precoders(17, f, G, 64, f, "unit_columns")
     W[1, 5, 3] = np.float32(value)
