@@ -16,7 +16,10 @@ if os.environ.get("TCX_W", "zero") == "random":
     W[72 * 128:] *= 2.0 ** -12          # second term ~ the W2 residual of a real split
 names = {0: "full", 1: "no-mma", 2: "no-store", 3: "no-mma,no-store", 4: "no-split", 5: "no-mma,no-split",
          6: "no-store,no-split", 7: "only-loads", 8: "no-loads", 10: "no-loads,no-store", 12: "no-loads,no-split",
-         14: "only-mma", 15: "nothing", 16: "main product as fp16 MMAs", 48: "fp16 MMAs + fp16-packed S1", 64: "correction products as fp16 MMAs", 240: "all products as fp16 MMAs on fp16-packed terms"}
+         14: "only-mma", 15: "nothing"}
+# (round-2 energy experiments on the tf32 kernel — DBG 16 / 48 / 64 / 240: products as fp16
+# MMAs on reinterpreted or fp16-packed terms — led to the fp16-term kernel, DESIGN.md §7;
+# their code paths went with the tf32 kernel)
 modes = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [0, 1, 2, 4, 8, 3, 6, 10, 12, 14, 5, 7, 15]
 for dbg in modes:
     rec = {}
