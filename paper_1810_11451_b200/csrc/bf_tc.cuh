@@ -310,8 +310,11 @@ struct TileIter {
     int G;
     int gi;
     int64_t item, end;
+    int64_t gend;         // end of the current group's run of items (cached: the fast path
+                          // of next() is one compare while a group lasts)
     __device__ void enter(int jj) {
         j = jj;
+        gend = -1;        // forces the group lookup
         if (jj < n_jobs) {
             offs = jobs[jj].offs;
             G = jobs[jj].n_groups;
@@ -321,9 +324,17 @@ struct TileIter {
         }
     }
     __device__ bool next(Tile &t) {
+        if (item < gend) {                                  // same group, same job
+            t.item = item;
+            t.g = offs ? gi : 0;
+            t.job = j;
+            t.cnt = (item + 1 < gend) ? 2 : 1;
+            item += t.cnt;
+            return true;
+        }
         while (j < n_jobs) {
             if (item < end) {
-                int64_t gend = end;
+                gend = end;
                 bool ok = true;
                 if (offs) {
                     while (gi < G && item >= offs[gi + 1]) ++gi;
@@ -818,7 +829,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = *tmem_slot;
-    TileIter it{jobs, n_jobs, 0, nullptr, 0, 0, 0, 0};
+    TileIter it{jobs, n_jobs, 0, nullptr, 0, 0, 0, 0, -1};
     it.enter(0);
     Tile tl;
     // The next tile of this role.  SRV: when the current slot is exhausted, the epilogue
@@ -869,7 +880,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 }
                 bfk::mbar_wait(bar_slot_full + e, (uint32_t)(((slot - 1) / kSrvRing) & 1));
                 if (jobs[e].end < 0) return false;
-                it = TileIter{jobs + e, 1, 0, nullptr, 0, 0, 0, 0};
+                it = TileIter{jobs + e, 1, 0, nullptr, 0, 0, 0, 0, -1};
                 it.enter(0);
             }
         }
@@ -1440,7 +1451,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 fix_block<LAYOUT>(jobs[en.y >> 16], en.x, en.y & 0xFFFF);
             }
         } else {
-            TileIter it2{jobs, n_jobs, 0, nullptr, 0, 0, 0, 0};
+            TileIter it2{jobs, n_jobs, 0, nullptr, 0, 0, 0, 0, -1};
             it2.enter(0);
             Tile t2;
             while (it2.next(t2)) {
