@@ -93,27 +93,15 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;"
                  ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
 }
-#ifndef BF_MBAR_SUSPEND_NS
-#define BF_MBAR_SUSPEND_NS 0
-#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    // (a suspend-time hint on try_wait measured no different: tools/sustained_exp.py)
     uint32_t done;
     do {
-        if (BF_MBAR_SUSPEND_NS > 0) {
-            // time-limit hint: a waiting warp sleeps until the phase completes (or the
-            // limit passes) instead of re-polling, leaving issue slots to working warps
-            asm volatile(
-                "{\n\t.reg .pred p;\n\t"
-                "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
-                "selp.u32 %0, 1, 0, p;\n\t}"
-                : "=r"(done) : "r"(smem_addr(bar)), "r"(parity), "n"(BF_MBAR_SUSPEND_NS) : "memory");
-        } else {
-            asm volatile(
-                "{\n\t.reg .pred p;\n\t"
-                "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
-                "selp.u32 %0, 1, 0, p;\n\t}"
-                : "=r"(done) : "r"(smem_addr(bar)), "r"(parity) : "memory");
-        }
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(smem_addr(bar)), "r"(parity) : "memory");
     } while (!done);
 }
 // TMA bulk copy global -> shared (no tensor map), completion on an mbarrier.

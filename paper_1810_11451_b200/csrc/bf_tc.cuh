@@ -78,9 +78,6 @@ constexpr int kMinSmem = 120 * 1024;   // forces one CTA (and one TMEM owner) pe
 #ifndef BFTC_EARLY_RELEASE
 #define BFTC_EARLY_RELEASE 0
 #endif
-#ifndef BFTC_SPLIT_ONEPASS
-#define BFTC_SPLIT_ONEPASS 1   // the split writes all terms of a chunk in one pass (x1 once)
-#endif
 #ifndef BFTC_ABUFS
 #define BFTC_ABUFS 2      // TMEM A-region buffers (2 where they fit)
 #endif
@@ -1005,21 +1002,21 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 // — x1 computed once — into the tile's A buffer (free since tile t - 2's MMAs).
                 // Up to f = 16 (<= 4 chunks) the second warp of each quarter only keeps the
                 // barrier counts.
-                if constexpr (BFTC_SPLIT_ONEPASS) {
+                {
                     const bool ex = (cur_wf & 1) != 0;     // S3 is only multiplied for exact W
                     bfk::mbar_wait(a_free + 1, par);
                     bfk::mbar_wait(a_free + 0, par);
                     bfk::mbar_wait(a_free + 2, par);
                     tc::fence_after_sync();
-    #pragma unroll
+        #pragma unroll
                     for (int i = 0; i < kSlots; ++i) {
                         const int c0 = c_beg0 + 8 * i;
                         if (c0 >= c_end0) break;
                         uint32_t h1[4], h2[4];
-    #pragma unroll
+        #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             float y1[2], y2[2];
-    #pragma unroll
+        #pragma unroll
                             for (int c = 0; c < 2; ++c) {
                                 const float x = xs[8 * i + 2 * e + c];
                                 y1[c] = tc::tf32_round(x);
@@ -1034,10 +1031,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                         }
                         if (ex) {
                             uint32_t h3[4];
-    #pragma unroll
+        #pragma unroll
                             for (int e = 0; e < 4; ++e) {
                                 float y3[2];
-    #pragma unroll
+        #pragma unroll
                                 for (int c = 0; c < 2; ++c) {
                                     const float x = xs[8 * i + 2 * e + c];
                                     const float x1 = tc::tf32_round(x);
@@ -1057,52 +1054,6 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                     mbar_arrive(a_full + 1);
                     mbar_arrive(a_full + 0);
                     mbar_arrive(a_full + 2);
-                } else {
-        #pragma unroll
-                    for (int pass = 0; pass < 3; ++pass) {
-                        const int term = pass == 2 ? 0 : pass + 1;
-                        bfk::mbar_wait(a_free + term, par);
-                        tc::fence_after_sync();
-                        if (term == 2 && !(cur_wf & 1)) {   // S3 is only multiplied for exact W
-                            tc::fence_before_sync();
-                            mbar_arrive(a_full + term);
-                            continue;
-                        }
-                        // this warp's K chunks; up to f = 16 (<= 4 chunks) the second warp of each
-                        // quarter only keeps the barrier counts
-        #pragma unroll
-                        for (int i = 0; i < kSlots; ++i) {
-                            const int c0 = c_beg0 + 8 * i;
-                            if (c0 >= c_end0) break;
-                            uint32_t h[4];
-        #pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                // exact 3-term split of the scaled values, each term rounded to
-                                // 11 significant bits (integer add + mask, 2 ops): x = x1 + x2 +
-                                // x3 exactly, |x - x1| <= 2^-11 |x|, |x3| <= 2^-22 |x|; packed
-                                // as fp16 pairs (exact in fp16's normal range)
-                                float y[2];
-        #pragma unroll
-                                for (int c = 0; c < 2; ++c) {
-                                    const float x = xs[8 * i + 2 * e + c];
-                                    const float x1 = tc::tf32_round(x);
-                                    const float r1 = x - x1;          // exact
-                                    const float x2 = tc::tf32_round(r1);
-                                    y[c] = term == 0 ? x1 : (term == 1 ? x2 : r1 - x2);
-                                    // exact W: all three terms exact in fp16 needs every nonzero
-                                    // scaled component >= 2^-1 (else the block is fixed up)
-                                    if (term == 2)
-                                        tiny = min(tiny, (__float_as_uint(x) & 0x7FFFFFFFu) - 1u);
-                                }
-                                h[e] = tc::pack_f16x2(y[0], y[1]);
-                            }
-                            if constexpr (!(DBG & 4)) tc::tmem_st4(a_base + term * kARegion + c0 / 2, h);
-                        }
-                        tc::tmem_st_wait();
-                        tc::fence_before_sync();
-                        mbar_arrive(a_full + term);
-                    }
-
                 }
                 out_dom |= tiny < 0x3EFFFFFFu;   // a nonzero scaled component below 2^-1
                 if (valid && ((cur_wf & 2) || out_dom)) {
