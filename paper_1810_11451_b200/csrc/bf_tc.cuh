@@ -966,7 +966,8 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                     }
                 }
                 // the row's other K half lives in the partner warp (warp ^ 4): exchange maxima
-                {
+                // (up to f = 16 the first warp of each quarter holds whole rows: nothing to do)
+                if constexpr (KPc > 32) {
                     float *xw = reinterpret_cast<float *>(xch) + (t & 1) * 256;
                     xw[warp * 32 + lane] = emx;
                     asm volatile("bar.sync %0, 64;" ::"r"(2 + (warp & 3)) : "memory");
