@@ -1354,12 +1354,14 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 epi_bar_sync();
                 if (valid) {
                     float *Rt = Rst + bsel * rbf;
-                    const float osc = J.out_scale;
+                    // int16 output: the row's unscale folds into the output scale (both powers
+                    // of two), one multiply per value instead of two
+                    const float osc = LAYOUT == 3 ? J.out_scale * us : J.out_scale;
 #pragma unroll
                     for (int aa = 0; aa < 32; ++aa) {
                         const int a = 32 * h + aa;
-                        const float2 z = tc::mul2f(make_float2(__uint_as_float(v[2 * aa]), __uint_as_float(v[2 * aa + 1])),
-                                                   make_float2(us, us));
+                        const float2 raw = make_float2(__uint_as_float(v[2 * aa]), __uint_as_float(v[2 * aa + 1]));
+                        const float2 z = LAYOUT == 3 ? raw : tc::mul2f(raw, make_float2(us, us));
                         const float re = z.x, im = z.y;
                         if (LAYOUT == 0)
                             *reinterpret_cast<float2 *>(Rt + 2 * (a * 60 + j)) = make_float2(re, im);
