@@ -1,5 +1,5 @@
 // Instantiations of the beamforming kernels for f = 31..36 (both layouts):
-// the CUDA-core FFMA kernel (bf_ffma.cuh) and the tcgen05 split-TF32 kernel (bf_tc.cuh).
+// the CUDA-core FFMA kernel (bf_ffma.cuh) and the tcgen05 split-precision kernel (bf_tc.cuh).
 #include "bf_dispatch.h"
 #include "bf_ffma.cuh"
 #include "bf_tc.cuh"
@@ -11,7 +11,7 @@ static void reg(BfKernelTable &t, BfKernelTable &tc) {
     tc[F][0] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 0>), bftc::TcSmem<F>::kBytes};
     tc[F][1] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 1>), bftc::TcSmem<F>::kBytes};
     t[F][2] = {reinterpret_cast<const void *>(&bfk::bf_ffma_kernel<F, 2>), bfk::Smem<F>::kBytes};
-    tc[F][2] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 2>), bftc::TcSmem<F>::kBytes};
+    tc[F][2] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 2>), bftc::TcSmem<F, false, true>::kBytes};
     t[F][3] = {reinterpret_cast<const void *>(&bfk::bf_ffma_kernel<F, 3>), bfk::Smem<F>::kBytes};
     tc[F][3] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 3>), bftc::TcSmem<F>::kBytes};
 }

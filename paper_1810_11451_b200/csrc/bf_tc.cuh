@@ -78,6 +78,12 @@ constexpr int kMinSmem = 120 * 1024;   // forces one CTA (and one TMEM owner) pe
 #ifndef BFTC_EARLY_RELEASE
 #define BFTC_EARLY_RELEASE 0
 #endif
+#ifndef BFTC_DEEP_RING_MAXF
+#define BFTC_DEEP_RING_MAXF 8    // S ring of kMaxStages up to this f, 2 stages above
+#endif
+#ifndef BFTC_RSTAGES
+#define BFTC_RSTAGES 2    // R stages where two fit (small f)
+#endif
 #ifndef BFTC_ABUFS
 #define BFTC_ABUFS 2      // TMEM A-region buffers (2 where they fit)
 #endif
@@ -215,7 +221,7 @@ template <int F>
 using TcParamsOf = TcParamsN<F == 0 ? kMaxJobs : 1>;
 static_assert(offsetof(TcParamsN<1>, job) == offsetof(TcParams, job), "TcParams prefix layout");
 
-template <int F, bool SRV = false>
+template <int F, bool SRV = false, bool R2 = false>   // R2: a second R stage where it fits
 struct TcSmem {
     static constexpr int FS = F > 0 ? F : 36;          // sizing flow count (36 for runtime f)
     static constexpr int KP = kp_of(FS);
@@ -245,12 +251,14 @@ struct TcSmem {
     static constexpr int kFixed = kWBufs * kWBytes + kMisc + (kStageR ? kRStageBytes + 128 : 0);
     static constexpr int kStagesFit = (kSmemLimit - kFixed) / (2 * kSBlock);
     // S ring depth: with the staged epilogue a deeper ring measured slower above f = 12
-    // (e.g. f = 20: 0.87 of the copy bandwidth with 4 stages, 0.94 with 2; f <= 12 gains
-    // from 4 — tools/sweep_f.py, BFTC_MAX_STAGES builds, profiles/r01_sweep_stages_v5.txt)
+    // (e.g. f = 20: 0.87 of the copy bandwidth with 4 stages, 0.94 with 2; f <= 12 gained
+    // from 4 — tools/sweep_f.py, BFTC_MAX_STAGES builds, profiles/r01_sweep_stages_v5.txt);
+    // round 2 (fp16 terms): 4 stages only up to f = 8 (f = 10-12: 0.85-0.90 with 4, 0.93
+    // with 2; profiles/r02_rstage_ring.txt)
     // (fp16 output, whose stores are half the bytes, keeps the deepest ring that fits)
     // (slot server: latency, not bandwidth — every stage that fits, so a CTA's few tiles of a
     // small slot all load at once)
-    static constexpr int kMaxS = (SRV || (F > 0 && F <= 12)) ? kMaxStages : (kMaxStages < 2 ? kMaxStages : 2);
+    static constexpr int kMaxS = (SRV || (F > 0 && F <= BFTC_DEEP_RING_MAXF)) ? kMaxStages : (kMaxStages < 2 ? kMaxStages : 2);
     static constexpr int kStagesAlloc = kStagesFit < kMaxStages ? kStagesFit : kMaxStages;
     static constexpr int kStages = kStagesFit < kMaxS ? kStagesFit : kMaxS;
     static_assert(kStages >= 2, "S ring needs two stages");
@@ -264,7 +272,11 @@ struct TcSmem {
     static constexpr int kOffSig = kOffJCost + kMaxJobs * 8;       // int32 [2][128]
     static constexpr int kOffXch = kOffSig + kSigBytes;            // uint32 [2][8][32]
     static constexpr int kOffR = (kOffXch + kXchBytes + 127) / 128 * 128;
-    static constexpr int kBytesUsed = kStageR ? kOffR + kRStageBytes : kOffXch + kXchBytes;
+    // two R stages where they fit (small f; fp16 output — R2 — only: the fp32 layouts measured
+    // slower with two, and the int16 direct path slower with the smaller L1 the allocation
+    // leaves): the epilogue writes tile t + 1's stage while tile t's bulk stores read theirs
+    static constexpr int kRStages = (R2 && kStageR && F > 0 && kOffR + 2 * kRStageBytes <= kSmemLimit) ? BFTC_RSTAGES : 1;
+    static constexpr int kBytesUsed = kStageR ? kOffR + kRStages * kRStageBytes : kOffXch + kXchBytes;
     static constexpr int kBytes = kBytesUsed > kMinSmem ? kBytesUsed : kMinSmem;
     static_assert(kBytesUsed <= kSmemLimit, "shared memory");
 };
@@ -530,8 +542,9 @@ __device__ __forceinline__ void cta_range(const int32_t *offs, int G, int64_t n,
 __device__ __forceinline__ void epi_bar_sync() {
     asm volatile("bar.sync 1, 256;" ::: "memory");
 }
-__device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+template <int N = 0>
+__device__ __forceinline__ void bulk_wait_read() {   // at most N bulk groups still reading smem
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -675,7 +688,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 template <int F, int LAYOUT, int DBG = 0, bool SRV = false>
 __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> p) {
     static_assert(!SRV || F == 0, "the slot server runs the runtime-f kernel");
-    using L = TcSmem<F, SRV>;
+    using L = TcSmem<F, SRV, LAYOUT == 2>;   // (fp16 output: two R stages where they fit)
     // TMEM column stride of the three A regions: fixed across the jobs of a launch
     // (the split of a job's first tile must not overlap the previous job's regions
     // that its last MMAs may still read).
@@ -688,7 +701,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     // f = 36 0.70 vs 0.84 — tools/sweep_f.py, profiles/r01_sweep_i16_v6.txt)
     constexpr bool kStageR = L::kStageR && (LAYOUT != 3 || F == 0 || F > 12);
     static_assert(kStageR || LAYOUT == 2 || LAYOUT == 3, "fp32 layouts always use the staged epilogue");
-    constexpr int kRing = LAYOUT == 2 ? L::kStagesAlloc : L::kStages;   // S ring depth used
+    // S ring depth used: 16-bit outputs (fp16, and int16 with the direct epilogue) keep the
+    // deepest ring that fits (int16 f = 9-12: 0.55-0.59 of copy BW with 2 stages, 0.66-0.71
+    // with 4; profiles/r02_rstage_ring.txt)
+    constexpr int kRing = (LAYOUT == 2 || (LAYOUT == 3 && !kStageR)) ? L::kStagesAlloc : L::kStages;
     extern __shared__ __align__(1024) unsigned char smem[];
     float *Wsm = reinterpret_cast<float *>(smem);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + L::kOffBar);
@@ -1349,8 +1365,12 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
                 // then one bulk store per block by the first epilogue thread.  The previous
                 // tile's stores must have read the stage first.
                 constexpr int rbf = bfk::r_block_bytes(LAYOUT) / 4;   // floats per block
-                float *Rst = reinterpret_cast<float *>(smem + L::kOffR);
-                if (e0) bulk_wait_read();
+                // two R stages for fp16 output (fp32 output measured slower with two: f = 4-12
+                // 0.85 vs 0.90 of copy BW; fp16 output f = 1-16 0.68-0.87 -> 0.79-0.92)
+                constexpr int kRUse = L::kRStages;
+                float *Rst = reinterpret_cast<float *>(smem + L::kOffR) +
+                             (kRUse == 2 ? (int)(t & 1) * (L::kRStageBytes / 4) : 0);
+                if (e0) bulk_wait_read<kRUse - 1>();   // this stage's previous stores read it
                 epi_bar_sync();
                 if (valid) {
                     float *Rt = Rst + bsel * rbf;
