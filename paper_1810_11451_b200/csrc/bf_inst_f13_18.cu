@@ -13,7 +13,7 @@ static void reg(BfKernelTable &t, BfKernelTable &tc) {
     t[F][2] = {reinterpret_cast<const void *>(&bfk::bf_ffma_kernel<F, 2>), bfk::Smem<F>::kBytes};
     tc[F][2] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 2>), bftc::TcSmem<F, false, true>::kBytes};
     t[F][3] = {reinterpret_cast<const void *>(&bfk::bf_ffma_kernel<F, 3>), bfk::Smem<F>::kBytes};
-    tc[F][3] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 3>), bftc::TcSmem<F>::kBytes};
+    tc[F][3] = {reinterpret_cast<const void *>(&bftc::bf_tc_kernel<F, 3>), bftc::TcSmem<F, false, BFTC_I16_R2 != 0>::kBytes};
 }
 
 void bf_register_f13_18(BfKernelTable &t, BfKernelTable &tc) {

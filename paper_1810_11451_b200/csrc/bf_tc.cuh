@@ -81,6 +81,16 @@ constexpr int kMinSmem = 120 * 1024;   // forces one CTA (and one TMEM owner) pe
 #ifndef BFTC_DEEP_RING_MAXF
 #define BFTC_DEEP_RING_MAXF 8    // S ring of kMaxStages up to this f, 2 stages above
 #endif
+// int16 output: direct register stores up to this f (round 1: faster than the staged epilogue
+// at f <= 12), and two R stages for the staged one; round 2 (fp16 terms): staged with two R
+// stages wins at every f (f = 1 0.53 -> 0.58, f = 8 0.61 -> 0.67, f = 16 0.69 -> 0.75 of copy
+// BW; profiles/r02_rstage_ring.txt)
+#ifndef BFTC_I16_DIRECT_MAXF
+#define BFTC_I16_DIRECT_MAXF 0
+#endif
+#ifndef BFTC_I16_R2
+#define BFTC_I16_R2 1
+#endif
 #ifndef BFTC_RSTAGES
 #define BFTC_RSTAGES 2    // R stages where two fit (small f)
 #endif
@@ -272,9 +282,9 @@ struct TcSmem {
     static constexpr int kOffSig = kOffJCost + kMaxJobs * 8;       // int32 [2][128]
     static constexpr int kOffXch = kOffSig + kSigBytes;            // uint32 [2][8][32]
     static constexpr int kOffR = (kOffXch + kXchBytes + 127) / 128 * 128;
-    // two R stages where they fit (small f; fp16 output — R2 — only: the fp32 layouts measured
-    // slower with two, and the int16 direct path slower with the smaller L1 the allocation
-    // leaves): the epilogue writes tile t + 1's stage while tile t's bulk stores read theirs
+    // two R stages where they fit (small f; 16-bit outputs — R2 — only: the fp32 layouts
+    // measured slower with two): the epilogue writes tile t + 1's stage while tile t's bulk
+    // stores read theirs
     static constexpr int kRStages = (R2 && kStageR && F > 0 && kOffR + 2 * kRStageBytes <= kSmemLimit) ? BFTC_RSTAGES : 1;
     static constexpr int kBytesUsed = kStageR ? kOffR + kRStages * kRStageBytes : kOffXch + kXchBytes;
     static constexpr int kBytes = kBytesUsed > kMinSmem ? kBytesUsed : kMinSmem;
@@ -688,7 +698,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 template <int F, int LAYOUT, int DBG = 0, bool SRV = false>
 __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> p) {
     static_assert(!SRV || F == 0, "the slot server runs the runtime-f kernel");
-    using L = TcSmem<F, SRV, LAYOUT == 2>;   // (fp16 output: two R stages where they fit)
+    using L = TcSmem<F, SRV, LAYOUT == 2 || (BFTC_I16_R2 && LAYOUT == 3)>;   // (16-bit outputs: two R stages where they fit)
     // TMEM column stride of the three A regions: fixed across the jobs of a launch
     // (the split of a job's first tile must not overlap the previous job's regions
     // that its last MMAs may still read).
@@ -699,7 +709,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     // staged R (see TcSmem::kStageR); int16 output at f <= 12 measured faster with the
     // warps storing independently (0.41 vs 0.50 ms per 10^5 blocks; staged wins above:
     // f = 36 0.70 vs 0.84 — tools/sweep_f.py, profiles/r01_sweep_i16_v6.txt)
-    constexpr bool kStageR = L::kStageR && (LAYOUT != 3 || F == 0 || F > 12);
+    constexpr bool kStageR = L::kStageR && (LAYOUT != 3 || F == 0 || F > BFTC_I16_DIRECT_MAXF);
     static_assert(kStageR || LAYOUT == 2 || LAYOUT == 3, "fp32 layouts always use the staged epilogue");
     // S ring depth used: 16-bit outputs (fp16, and int16 with the direct epilogue) keep the
     // deepest ring that fits (int16 f = 9-12: 0.55-0.59 of copy BW with 2 stages, 0.66-0.71
