@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work of the oracle baseline sample")
     ap.add_argument("--c5-chunks", type=int, default=0, help="c5: chunks per step (0 = all 2048)")
+    ap.add_argument("--timeline", default="", help="c5: write a chrome-trace timeline (torch.profiler "
+                    "over CUPTI: kernels per stream and the NVTX ranges libbf emits) of one replayed "
+                    "step after the timed ones to this path")
     ap.add_argument("--no-graph", action="store_true", help="c5: launch eagerly, no CUDA graph")
     ap.add_argument("--steady-seconds", type=float, default=10.0,
                     help="after the timed burst, back-to-back steps for this long: steady-state "
@@ -1125,6 +1128,14 @@ def run_c5(args, wl, world, rank, local, dev):
     kern_ms = shard.max_over_ranks(kern_ms, dev)
     launches = int(shard.sum_over_ranks(launches, dev))
     clk = clocks.stop() if clocks else None
+    if args.timeline and rank == 0:
+        # one more step under the profiler (outside the timed region): the kernels of the
+        # route stream and the two apply streams, and libbf's NVTX ranges
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+            run_step()
+            torch.cuda.synchronize()
+        prof.export_chrome_trace(args.timeline)
     # ---- parity: the ring still holds the R of this rank's last NSLOT windows of the last
     #      step; every 8th block of each of those chunks against the oracle
     def c5_inputs(cell, f):
