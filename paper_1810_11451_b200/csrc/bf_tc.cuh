@@ -46,7 +46,8 @@
 //              of the thread's D row half, release of the TMEM buffer, then the
 //              tile's two R blocks written into a shared-memory stage in their
 //              global layout and stored by one thread with one bulk copy per block
-//              (int16 output at f <= 12: direct 8-byte stores instead).
+//              (two R stages for 16-bit outputs at f <= 16; BFTC_I16_DIRECT_MAXF builds
+//              store int16 output directly from registers instead).
 // Shared memory per f: TcSmem (W buffers, S ring depth, R stage).
 // TMEM: two sets of A terms (fp16 pairs: KP / 2 columns per term; KP of f = 36 for the
 // batch kernel) at [0, 3 KP / 2) and [3 KP / 2, 3 KP), D double buffer at [256, 384),
@@ -706,9 +707,10 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
     // A regions double-buffered (the split of tile t + 1 overlaps tile t's MMAs) when both
     // sets of three terms fit below the D buffers
     constexpr int kABufs = (2 * 3 * kARegion <= kDCol0) ? BFTC_ABUFS : 1;
-    // staged R (see TcSmem::kStageR); int16 output at f <= 12 measured faster with the
-    // warps storing independently (0.41 vs 0.50 ms per 10^5 blocks; staged wins above:
-    // f = 36 0.70 vs 0.84 — tools/sweep_f.py, profiles/r01_sweep_i16_v6.txt)
+    // staged R (see TcSmem::kStageR); round 1 measured int16 output at f <= 12 faster with
+    // the warps storing independently (0.41 vs 0.50 ms per 10^5 blocks, profiles/
+    // r01_sweep_i16_v6.txt); round 2's two R stages make the staged epilogue faster at every f
+    // (BFTC_I16_DIRECT_MAXF = 0; the direct path stays for experiments)
     constexpr bool kStageR = L::kStageR && (LAYOUT != 3 || F == 0 || F > BFTC_I16_DIRECT_MAXF);
     static_assert(kStageR || LAYOUT == 2 || LAYOUT == 3, "fp32 layouts always use the staged epilogue");
     // S ring depth used: 16-bit outputs (fp16, and int16 with the direct epilogue) keep the
@@ -1315,7 +1317,7 @@ __global__ void __launch_bounds__(kThreads, 1) bf_tc_kernel(const TcParamsOf<F> 
             mbar_arrive(bar_sig_free + b);
             const uint32_t d = tmem + ((uint32_t)(q * 32) << 16) + kDCol0 + 128 * b + 64 * h;
             if constexpr (!(DBG & 2) && !kStageR && (LAYOUT == 2 || LAYOUT == 3)) {
-                // 16-bit output, direct stores (int16 output at f <= 12; see kStageR), in
+                // 16-bit output, direct stores (int16 output in BFTC_I16_DIRECT_MAXF builds), in
                 // two halves of 16 antennas to stay inside the register budget of 18 warps:
                 // load 32 D columns, pack, store; the TMEM buffer is released after the
                 // second load (the MMA needs it again only two tiles later).  Lane pairs
