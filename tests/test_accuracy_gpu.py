@@ -390,3 +390,35 @@ def test_relative_range_edges(exact_w):
     assert decisions == [True] * 4 + [False] * 4 + [not exact_w], decisions
     R_ref, T, _ = oracle.beamform(W, S, None, n_threads=NT)
     assert_parity(R, R_ref, T, what="relative-range edges")
+
+
+def test_batch_with_an_auto_plan_outside_the_domain():
+    """bf_apply_batch packs AUTO plans into its tensor launch unless their precoders leave the
+    tensor domain: such a job runs on its own (FFMA, bitwise its own apply_routed), the other
+    jobs stay bitwise equal to their tensor-variant apply_routed."""
+    jobs, refs = [], []
+    for i, f in enumerate((9, 20, 33)):
+        n, G = 300 + 17 * i, 3
+        W = syn.precoders(80 + i, f, G, 64, f, "unit_columns")
+        if i == 1:
+            W[2, 7, 4] = np.float32(2.0 ** -17)           # relative range: group 2 outside
+        S = syn.qam_symbols(80 + i, f, np.arange(n), f, 60, 64)
+        tags = torch.from_numpy(syn.subband_tags(80 + i, np.arange(n), G)).to(DEV)
+        p = Plan(f=f)                                      # AUTO
+        p.set_precoders(torch.from_numpy(W).to(DEV))
+        assert p.variant == (Variant.FFMA if i == 1 else Variant.TENSOR)
+        Sd = torch.from_numpy(S).to(DEV)
+        perm, offs = p.route(tags)
+        R = torch.empty(p.r_shape(n), dtype=p.r_dtype, device=DEV)
+        jobs.append((p, Sd, perm, offs, R))
+        q = Plan(f=f, variant=Variant.TENSOR if i != 1 else Variant.FFMA)
+        q.set_precoders(torch.from_numpy(W).to(DEV))
+        ref = torch.empty_like(R)
+        q.apply_routed(Sd, perm, offs, out=ref)
+        refs.append((q, ref))
+    bf.apply_batch(jobs)
+    torch.cuda.synchronize()
+    for i, ((p, _, _, _, R), (q, ref)) in enumerate(zip(jobs, refs)):
+        assert_bitwise(R.cpu().numpy(), ref.cpu().numpy(), f"job {i}")
+        p.close()
+        q.close()
