@@ -57,8 +57,11 @@ constexpr size_t kMaxProfEvents = 1 << 16;  // timed launches kept between kerne
 // within +-3 % up to f = 6, fp16 and int16 output FFMA ahead up to f = 4 (0.36 vs 0.37,
 // 0.45 vs 0.47 ms), the tensor kernel from f = 5; with two R stages for fp16 output the
 // tensor kernel leads there from f = 3 (0.307 vs 0.322 ms), and with the staged two-stage
-// int16 epilogue from f = 4 (0.429 vs 0.445 ms; profiles/r02_rstage_ring.txt).
-constexpr int kAutoTensorMinF[4] = {2, 7, 3, 4};   // [layout]
+// int16 epilogue from f = 4 (0.429 vs 0.445 ms; profiles/r02_rstage_ring.txt); after the
+// round-2 kernel work the tensor kernel also leads interleaved from f = 1 (0.548 vs 0.554 ms)
+// and planar from f = 2 (0.563 vs 0.571; f = 1 and 6 within 0.2 %; profiles/
+// r02_sweep_auto_final.txt).
+constexpr int kAutoTensorMinF[4] = {1, 2, 3, 4};   // [layout]
 // bf_apply_batch: 1 = one contiguous cost range of all the launch's jobs per CTA, 0 = every
 // job split over all CTAs
 constexpr int kBatchSplit = 1;
