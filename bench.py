@@ -843,7 +843,7 @@ def run_filter(args, wl, world, rank, local, dev):
     # DRAM bytes per signal from the committed ncu capture, scaled to this launch
     traffic, tbasis = None, None
     try:
-        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["bff::filter_warp_kernel<2>"]
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["bff::filter_warp_kernel<2, true>"]
         traffic = tr["dram_bytes_per_signal"] * n_loc
         tbasis = f"{tr['capture']}: {tr['dram_bytes_per_signal']:.0f} B/signal x {n_loc} signals"
     except (OSError, KeyError, ValueError):
@@ -935,7 +935,7 @@ def run_filter(args, wl, world, rank, local, dev):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                          "traffic_basis": tbasis,
-                         "kernel": "bff::filter_warp_kernel<2> (one warp per signal)", "kernel_ms": kavg,
+                         "kernel": "bff::filter_warp_kernel<2, true> (one warp per signal, twiddles folded into the butterflies)", "kernel_ms": kavg,
                          "algorithmic_bytes_per_launch": bytes_launch,
                          "peak_basis": peak_basis(peaks)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,

@@ -20,9 +20,10 @@ using bfh::fail;
 
 struct bff_plan_s {
     int n = bff::kN, device = 0, num_sms = 0, ctas_per_sm = 0;
-    // kernel: 3 (default) filter_warp_kernel<2> — one warp per signal, twiddle and H tables
-    // in shared memory, 2 CTAs per SM; 0 filter_warp_kernel<3> (no tables, 3 CTAs per SM);
-    // 1 / 2 the CTA-per-signal kernel filter_kernel<1 / 2> (kept for comparisons)
+    // kernel: 3 (default) filter_warp_kernel<2, true> — one warp per signal, twiddle and H
+    // tables in shared memory, 2 CTAs per SM, twiddles folded into the butterflies; 4 the same
+    // without the folding; 0 filter_warp_kernel<3> (no tables, 3 CTAs per SM); 1 / 2 the
+    // CTA-per-signal kernel filter_kernel<1 / 2> (kept for comparisons)
     int kind = 3;
     float2 *tw = nullptr, *H = nullptr;    // twiddles; DFT(h) / N
     float4 *tw3 = nullptr, *twp = nullptr; // pass-3 twiddle pairs; warp kernel's pass-2 bases
@@ -40,7 +41,7 @@ bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 bf_status launch(bff_plan_t p, const float2 *s, float2 *y, int64_t n, int mode, cudaStream_t st) {
     bff::FParams fp{s, y, p->H, p->tw, p->tw3, p->twp, n, mode};
     const int64_t cap = (int64_t)p->num_sms * std::max(1, p->ctas_per_sm);
-    const bool warpk = p->kind == 0 || p->kind == 3;   // 4 signals (warps) per CTA
+    const bool warpk = p->kind == 0 || p->kind >= 3;   // 4 signals (warps) per CTA
     const int64_t units = warpk ? (n + 3) / 4 : n;                 // warp kernel: 4 signals per CTA
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(units, cap));
     cudaEvent_t e1 = nullptr;
@@ -58,6 +59,8 @@ bf_status launch(bff_plan_t p, const float2 *s, float2 *y, int64_t n, int mode, 
     if (p->kind == 0)
         bff::filter_warp_kernel<3><<<grid, bff::kThreads, bff::warp_smem_bytes(false), st>>>(fp);
     else if (p->kind == 3)
+        bff::filter_warp_kernel<2, true><<<grid, bff::kThreads, bff::warp_smem_bytes(true), st>>>(fp);
+    else if (p->kind == 4)
         bff::filter_warp_kernel<2><<<grid, bff::kThreads, bff::warp_smem_bytes(true), st>>>(fp);
     else if (p->kind == 1)
         bff::filter_kernel<1><<<grid, bff::kThreads, bff::smem_bytes(1), st>>>(fp);
@@ -110,16 +113,17 @@ bf_status bff_plan_create(int n, bff_plan_t *out) {
                     prop.minor);
     }
     p->num_sms = prop.multiProcessorCount;
-    // BFF_FILTER_KERNEL=warp_tab|warp|cta1|cta2 selects a kernel for comparison experiments
+    // BFF_FILTER_KERNEL=warp_fold|warp_tab|warp|cta1|cta2 selects a kernel for comparison experiments
     if (const char *env = std::getenv("BFF_FILTER_KERNEL")) {
         const std::string k(env);
-        p->kind = k == "warp" ? 0 : k == "cta1" ? 1 : k == "cta2" ? 2 : 3;
+        p->kind = k == "warp" ? 0 : k == "cta1" ? 1 : k == "cta2" ? 2 : k == "warp_tab" ? 4 : 3;
     }
     const void *kern = p->kind == 0   ? (const void *)bff::filter_warp_kernel<3>
-                       : p->kind == 3 ? (const void *)bff::filter_warp_kernel<2>
+                       : p->kind == 3 ? (const void *)bff::filter_warp_kernel<2, true>
+                       : p->kind == 4 ? (const void *)bff::filter_warp_kernel<2>
                        : p->kind == 1 ? (const void *)bff::filter_kernel<1> : (const void *)bff::filter_kernel<2>;
     const int smem = p->kind == 0 ? bff::warp_smem_bytes(false)
-                     : p->kind == 3 ? bff::warp_smem_bytes(true) : bff::smem_bytes(p->kind);
+                     : p->kind >= 3 ? bff::warp_smem_bytes(true) : bff::smem_bytes(p->kind);
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) { delete p; return cuda_fail(e, "cudaFuncSetAttribute (filter)"); }
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->ctas_per_sm, kern, bff::kThreads, smem);

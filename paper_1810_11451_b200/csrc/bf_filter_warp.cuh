@@ -101,6 +101,103 @@ __device__ __forceinline__ void dft32s2(c2 (&a)[64]) {
     }
 }
 
+// ---- twiddle-folded butterflies (FOLD variant) -------------------------------------------
+// A twiddled radix-2 butterfly (x + w b, x - w b) costs four packed instructions as
+// multiply-then-add (FMUL2 + FFMA2 for w b, FADD2, FADD2); as p = x + w b (two FFMA2,
+// broadcast operands) and x - w b = 2 x - p (one FFMA2, ptxas folds the negation) it
+// costs three.  Twiddle kinds, compile-time after unrolling: 0 = 1, 1 = -i, 2 = general.
+__device__ __forceinline__ c2 neg2(c2 a) { const float2 v = up(a); return pk(-v.x, -v.y); }
+__device__ __forceinline__ c2 twb(int k, c2 x, float2 w) {
+    return k == 0 ? x : k == 1 ? mul2(swp(x), pk(1.0f, -1.0f)) : cmul(x, w);
+}
+__device__ __forceinline__ void bfly(int k, c2 &x, c2 &b, float2 w) {
+    if (k == 0) {
+        const c2 t = add2(x, b);
+        b = sub2(x, b);
+        x = t;
+    } else if (k == 1) {
+        const c2 t = add_mi(x, b);
+        b = sub_mi(x, b);
+        x = t;
+    } else {
+        const c2 p = fma2(swp(b), pk(-w.y, w.y), fma2(b, pk(w.x, w.x), x));
+        b = fma2(x, pk(2.0f, 2.0f), neg2(p));
+        x = p;
+    }
+}
+// forward DFT4 of (x0 w0, x1 w1, x2 w2, x3 w3) in place, kinds k0..k3
+__device__ __forceinline__ void dft4k(c2 &x0, c2 &x1, c2 &x2, c2 &x3, int k0, int k1, int k2,
+                                      int k3, float2 w0, float2 w1, float2 w2, float2 w3) {
+    x0 = twb(k0, x0, w0);
+    bfly(k2, x0, x2, w2);                // x0 = t0 = x0 + x2, x2 = t1 = x0 - x2
+    x1 = twb(k1, x1, w1);
+    bfly(k3, x1, x3, w3);                // x1 = t2, x3 = d
+    const c2 X0 = add2(x0, x1), X2 = sub2(x0, x1), X1 = add_mi(x2, x3), X3 = sub_mi(x2, x3);
+    x0 = X0; x1 = X1; x2 = X2; x3 = X3;
+}
+// kind of the twiddle W64^m
+__host__ __device__ constexpr int kind64(int m) { return (m & 63) == 0 ? 0 : (m & 63) == 16 ? 1 : 2; }
+// forward DFT8 of (v[r S] w[r]), r < 8, in place; kinds k[r].  W8 and W8^3 folded too:
+// e + W8 o = e + kH (o.x + o.y, o.y - o.x) — one FFMA2 for the bracket, one per output.
+template <int S>
+__device__ __forceinline__ void dft8k(c2 *v, const int (&k)[8], const float2 (&w)[8]) {
+    c2 e0 = v[0], e1 = v[2 * S], e2 = v[4 * S], e3 = v[6 * S];
+    c2 o0 = v[S], o1 = v[3 * S], o2 = v[5 * S], o3 = v[7 * S];
+    dft4k(e0, e1, e2, e3, k[0], k[2], k[4], k[6], w[0], w[2], w[4], w[6]);
+    dft4k(o0, o1, o2, o3, k[1], k[3], k[5], k[7], w[1], w[3], w[5], w[7]);
+    const c2 u1 = fma2(swp(o1), pk(1.0f, -1.0f), o1);           // sqrt2 W8 o1
+    const c2 u3 = fma2(swp(o3), pk(1.0f, -1.0f), neg2(o3));     // sqrt2 W8^3 o3
+    v[0] = add2(e0, o0); v[4 * S] = sub2(e0, o0);
+    v[S] = fma2(u1, pk(kH, kH), e1); v[5 * S] = fma2(u1, pk(-kH, -kH), e1);
+    v[2 * S] = add_mi(e2, o2); v[6 * S] = sub_mi(e2, o2);
+    v[3 * S] = fma2(u3, pk(kH, kH), e3); v[7 * S] = fma2(u3, pk(-kH, -kH), e3);
+}
+template <int S>
+__device__ __forceinline__ void dft8k0(c2 *v) {
+    constexpr int k[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const float2 w[8] = {};
+    dft8k<S>(v, k, w);
+}
+// dft64 with the inter-stage twiddles W64^(r0 k1) folded into the outer DFT8s
+__device__ __forceinline__ void dft64f(c2 (&a)[64]) {
+#pragma unroll
+    for (int r0 = 0; r0 < 8; ++r0) dft8k0<8>(a + r0);
+#pragma unroll
+    for (int k1 = 0; k1 < 8; ++k1) {
+        int k[8];
+        float2 w[8];
+#pragma unroll
+        for (int r0 = 0; r0 < 8; ++r0) {
+            k[r0] = kind64(r0 * k1);
+            w[r0] = kW64[(r0 * k1) & 63];
+        }
+        dft8k<1>(a + 8 * k1, k, w);
+    }
+}
+// dft32s2 with the pass-2 table twiddles w^(r j) (tws) folded into the DFT8s over r1 and
+// the inner twiddles W32^(r0 k1) into the DFT4s over r0
+template <int H>
+__device__ __forceinline__ void dft32s2f(c2 (&a)[64], const float2 *tws, int l) {
+#pragma unroll
+    for (int r0 = 0; r0 < 4; ++r0) {
+        int k[8];
+        float2 w[8];
+#pragma unroll
+        for (int r1 = 0; r1 < 8; ++r1) {
+            const int r = r0 + 4 * r1;
+            k[r1] = r == 0 ? 0 : 2;
+            w[r1] = r == 0 ? make_float2(1.0f, 0.0f) : tws[r * 64 + l + 32 * H];
+        }
+        dft8k<8>(a + H + 2 * r0, k, w);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < 8; ++k1) {
+        c2 *b = a + H + 8 * k1;
+        dft4k(b[0], b[2], b[4], b[6], 0, kind64(2 * k1), kind64(4 * k1), kind64(6 * k1),
+              make_float2(1.0f, 0.0f), kW64[(2 * k1) & 63], kW64[(4 * k1) & 63], kW64[(6 * k1) & 63]);
+    }
+}
+
 // One transform (forward, natural order in and out) of the signal a lane holds as
 // a[s] = x[l + 32 s]; buf: the warp's exchange slots.  On return a[s] = X[l + 32 s].
 // next: the input of the warp's next signal, fetched into buf once the last pass has read
@@ -109,12 +206,14 @@ __device__ __forceinline__ void fetch_signal(c2 *buf, const float2 *src, uint64_
     bfk::mbar_arrive_expect_tx(bar, (uint32_t)(kN * 8));
     bfk::bulk_g2s(buf, src, kN * 8, bar, bfk::policy_evict_first());
 }
-template <bool TAB>
+// FOLD: twiddles folded into the butterflies (needs TAB)
+template <bool TAB, bool FOLD = false>
 __device__ __forceinline__ void fft2048_warp(c2 (&a)[64], c2 *buf, const float4 *__restrict__ twp,
                                              const float2 *tws, int l, const float2 *next,
                                              uint64_t *bar) {
     // pass 1: radix 64, inputs a[r] = x[l + 32 r]; output y[64 l + k] = X1[k] (a[tr64(k)])
-    dft64(a);
+    if (FOLD) dft64f(a);
+    else dft64(a);
     __syncwarp();                       // every lane's reads of buf (input / last pass) are done
 #pragma unroll
     for (int k = 0; k < 64; ++k) sts64(buf + wpad(64 * l + k), a[tr64(k)]);
@@ -134,7 +233,11 @@ __device__ __forceinline__ void fft2048_warp(c2 (&a)[64], c2 *buf, const float4 
     // twiddles w^(r j): TAB — from the CTA's shared table tws[r][j] (rounded once);
     // otherwise r = 8 b + c from T1[c] = w^(c j), c < 8 and T2[b] = w^(8 b j), b < 4, with
     // twp[e][j] = (w^(2^e j)) for e < 5 (float2 pairs of j and j + 32 in one float4)
-    if (TAB) {
+    if (FOLD) {
+        static_assert(!FOLD || TAB, "the folded pass 2 reads the shared twiddle table");
+        dft32s2f<0>(a, tws, l);
+        dft32s2f<1>(a, tws, l);
+    } else if (TAB) {
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -163,8 +266,10 @@ __device__ __forceinline__ void fft2048_warp(c2 (&a)[64], c2 *buf, const float4 
         }
     }
     }
-    dft32s2<0>(a);
-    dft32s2<1>(a);
+    if (!FOLD) {
+        dft32s2<0>(a);
+        dft32s2<1>(a);
+    }
     // X[j + 64 k] is in a[h + 2 tr32(k)]: rename to a[h + 2 k] (compile-time permutation)
     c2 t[64];
 #pragma unroll
@@ -177,7 +282,7 @@ __device__ __forceinline__ void fft2048_warp(c2 (&a)[64], c2 *buf, const float4 
 
 // MINC: CTAs per SM the register budget is sized for (3: 168 registers, 12 warps per SM;
 // 2: 255 registers, 8 warps)
-template <int MINC>
+template <int MINC, bool FOLD = false>
 __global__ void __launch_bounds__(kThreads, MINC) filter_warp_kernel(const FParams p) {
     // with 255 registers (2 CTAs per SM) shared memory has room for the twiddle and H tables
     constexpr bool TAB = MINC == 2;
@@ -215,7 +320,8 @@ __global__ void __launch_bounds__(kThreads, MINC) filter_warp_kernel(const FPara
 #pragma unroll 1
         for (int trip = 0; trip < trips; ++trip) {
             const bool last = trip == trips - 1 && sig + nw < p.n_sig;
-            fft2048_warp<TAB>(a, buf, p.twp, tws, l, last ? p.s + (sig + nw) * kN : nullptr, bar);
+            const float2 *nx = last ? p.s + (sig + nw) * kN : nullptr;
+            fft2048_warp<TAB, FOLD>(a, buf, p.twp, tws, l, nx, bar);
             if (trip == 0 && trips == 2) {
 #pragma unroll
                 for (int s = 0; s < 64; ++s) a[s] = cmul_conj(a[s], TAB ? Hs[l + 32 * s] : __ldg(p.H + l + 32 * s));

@@ -67,6 +67,24 @@ def test_filter_matches_oracle(n_sig):
     assert worst < 1e-6
 
 
+@pytest.mark.parametrize("kernel", ["warp_tab", "warp", "cta1", "cta2"])
+def test_comparison_kernels_match_oracle(kernel, monkeypatch):
+    # the non-default kernels BFF_FILTER_KERNEL selects (read at plan creation) — forward
+    # FFT and filter, a ragged count of signals (not a multiple of 4 warps / 2 per CTA)
+    monkeypatch.setenv("BFF_FILTER_KERNEL", kernel)
+    wl = syn.filter_workload("fl0")
+    s = syn.filter_signals(wl.seed, 0, np.arange(37))
+    h = syn.filter_taps()
+    y_ref, bound = oracle.filter_apply(s, h, n_threads=NT)
+    assert check(run_filter(s, h), y_ref, bound, f"filter {kernel}") < 1e-6
+    plan = FilterPlan()
+    X = plan.fft(torch.from_numpy(s[:5]).to(DEV))
+    torch.cuda.synchronize()
+    plan.close()
+    bound = np.sqrt(2048) * np.linalg.norm(s[:5].astype(np.complex128), axis=1)
+    assert check(X.cpu().numpy(), oracle.dft(s[:5]), bound, f"fft {kernel}") < 1e-6
+
+
 def test_filter_equals_circular_convolution():
     s = syn.filter_signals(8, 0, np.arange(4))
     rng = np.random.default_rng(8)
