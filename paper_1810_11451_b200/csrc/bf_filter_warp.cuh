@@ -26,7 +26,10 @@
 
 namespace bff {
 
-constexpr int kWarpPad = kN + kN / 64;          // per-warp exchange slots: one pad per 64
+// per-warp exchange slots: one pad per 64 (pass 1's row stores and pass 2's column reads
+// both conflict-free).  Pairing the row stores as STS.128 (two pads per 64) measured 0.6 %
+// slower (profiles/r02_filter_fold.txt).
+constexpr int kWarpPad = kN + kN / 64;
 __device__ __forceinline__ int wpad(int i) { return i + (i >> 6); }
 // 4 warps per CTA: exchange buffers, their mbarriers, and (TAB variant) the CTA's copies
 // of the pass-2 twiddles w^(r j) (r < 32, j < 64) and of H
@@ -174,6 +177,11 @@ __device__ __forceinline__ void dft64f(c2 (&a)[64]) {
         dft8k<1>(a + 8 * k1, k, w);
     }
 }
+// the folded kernel's twiddle table: float2 slot i holds w^(r j) for j = (i / 2) % 64,
+// r = r0 + 4 (2 q + i % 2), (r0, q) = ((i / 128) / 4, (i / 128) % 4): the two twiddles a
+// lane needs for r1 = 2q, 2q + 1 of one DFT8 are one 16-byte load
+__host__ __device__ constexpr int tws_fold_r(int i) { return (i >> 9) + 4 * (2 * ((i >> 7) & 3) + (i & 1)); }
+__host__ __device__ constexpr int tws_fold_j(int i) { return (i >> 1) & 63; }
 // dft32s2 with the pass-2 table twiddles w^(r j) (tws) folded into the DFT8s over r1 and
 // the inner twiddles W32^(r0 k1) into the DFT4s over r0
 template <int H>
@@ -183,10 +191,12 @@ __device__ __forceinline__ void dft32s2f(c2 (&a)[64], const float2 *tws, int l) 
         int k[8];
         float2 w[8];
 #pragma unroll
-        for (int r1 = 0; r1 < 8; ++r1) {
-            const int r = r0 + 4 * r1;
-            k[r1] = r == 0 ? 0 : 2;
-            w[r1] = r == 0 ? make_float2(1.0f, 0.0f) : tws[r * 64 + l + 32 * H];
+        for (int q = 0; q < 4; ++q) {        // r1 = 2q, 2q + 1: one LDS.128 (tws_fold_index)
+            const float4 v = reinterpret_cast<const float4 *>(tws)[(r0 * 4 + q) * 64 + l + 32 * H];
+            w[2 * q] = make_float2(v.x, v.y);
+            w[2 * q + 1] = make_float2(v.z, v.w);
+            k[2 * q] = r0 + 8 * q == 0 ? 0 : 2;
+            k[2 * q + 1] = 2;
         }
         dft8k<8>(a + H + 2 * r0, k, w);
     }
@@ -222,7 +232,7 @@ __device__ __forceinline__ void fft2048_warp(c2 (&a)[64], c2 *buf, const float4 
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int r = 0; r < 32; ++r) a[h + 2 * r] = buf[l + 32 * h + 65 * r];
+        for (int r = 0; r < 32; ++r) a[h + 2 * r] = buf[wpad(l + 32 * h + 64 * r)];
     if (next) {                    // last transform of the signal: the buffer is free now
         __syncwarp();
         if (l == 0) {
@@ -294,8 +304,14 @@ __global__ void __launch_bounds__(kThreads, MINC) filter_warp_kernel(const FPara
     float2 *Hs = tws + kN;                                                      // [2048]
     if (TAB) {
         for (int i = threadIdx.x; i < kN; i += kThreads) {
-            tws[i] = p.tw[((i >> 6) * (i & 63)) & (kN - 1)];                     // w^(r j)
-            if (p.mode == 0) Hs[i] = p.H[i];
+            tws[i] = FOLD ? p.tw[(tws_fold_r(i) * tws_fold_j(i)) & (kN - 1)]       // w^(r j)
+                          : p.tw[((i >> 6) * (i & 63)) & (kN - 1)];
+            // H in lane pairs: float4 (H[l + 32 s], H[l + 32 (s + 1)]) at [s / 2][l], s even,
+            // so the MULT reads two values per LDS.128
+            if (p.mode == 0) {
+                const int pr = i >> 1, e = (pr & 31) + 32 * (2 * (pr >> 5) + (i & 1));
+                Hs[i] = p.H[e];
+            }
         }
         __syncthreads();
     }
@@ -324,7 +340,16 @@ __global__ void __launch_bounds__(kThreads, MINC) filter_warp_kernel(const FPara
             fft2048_warp<TAB, FOLD>(a, buf, p.twp, tws, l, nx, bar);
             if (trip == 0 && trips == 2) {
 #pragma unroll
-                for (int s = 0; s < 64; ++s) a[s] = cmul_conj(a[s], TAB ? Hs[l + 32 * s] : __ldg(p.H + l + 32 * s));
+                for (int s = 0; s < 64; s += 2) {
+                    if (TAB) {
+                        const float4 h = reinterpret_cast<const float4 *>(Hs)[(s >> 1) * 32 + l];
+                        a[s] = cmul_conj(a[s], make_float2(h.x, h.y));
+                        a[s + 1] = cmul_conj(a[s + 1], make_float2(h.z, h.w));
+                    } else {
+                        a[s] = cmul_conj(a[s], __ldg(p.H + l + 32 * s));
+                        a[s + 1] = cmul_conj(a[s + 1], __ldg(p.H + l + 32 * (s + 1)));
+                    }
+                }
             }
         }
         float2 *dst = p.y + sig * kN;
@@ -334,7 +359,9 @@ __global__ void __launch_bounds__(kThreads, MINC) filter_warp_kernel(const FPara
 #pragma unroll
             for (int s = 0; s < 64; ++s) {
                 const float2 v = up(a[s]);
-                __stcs(dst + l + 32 * s, make_float2(v.x, __uint_as_float(__float_as_uint(v.y) ^ 0x80000000u)));
+                uint32_t im;   // inline PTX: a C-level XOR becomes neg.f32 -> FADD on the FMA pipe
+                asm("xor.b32 %0, %1, 0x80000000;" : "=r"(im) : "r"(__float_as_uint(v.y)));
+                __stcs(dst + l + 32 * s, make_float2(v.x, __uint_as_float(im)));
             }
         } else {
 #pragma unroll
