@@ -396,3 +396,63 @@ def filter_workload(name: str) -> FilterWorkload:
         return FilterWorkload("fl1", FILTER_N, 1 << 18, 64, 6,
                               "2^18 signals of 2048 64-QAM samples (4.3 GB in + out), seed 6")
     raise ValueError(name)
+
+
+# --------------------------------------------------------------------------
+# OFDM output stage: symbols of nb consecutive blocks
+# --------------------------------------------------------------------------
+@dataclass(frozen=True)
+class OfdmWorkload:
+    name: str
+    n_sym: int          # OFDM symbols (each nb consecutive blocks of 60 REs)
+    nb: int             # blocks (subbands) per symbol: nb * 60 active subcarriers
+    f: int
+    n: int              # IFFT size
+    cp: int             # cyclic prefix samples
+    M: int
+    seed: int
+    desc: str = ""
+    n_ant: int = 64
+    b: int = 60
+
+    @property
+    def n_blocks(self) -> int:
+        return self.n_sym * self.nb
+
+    def symbol_bytes(self, out_bytes: int = 8, fused: bool = True) -> int:
+        """Algorithmic HBM bytes per symbol: S read + output write (+ R write and read when
+        the beamformed symbol goes through HBM between the two stages, fused=False)."""
+        s = self.nb * 8 * self.b * self.f
+        y = self.n_ant * (self.cp + self.n) * out_bytes
+        r = 0 if fused else 2 * self.nb * 8 * self.b * self.n_ant
+        return s + y + r
+
+
+def ofdm_workload(name: str) -> OfdmWorkload:
+    """of0 (tests), of1 (bench): 26 subbands x 60 REs = 1560 active subcarriers in a
+    2048-point IFFT (a 50 MHz carrier at 30 kHz spacing), normal cyclic prefix 144,
+    f = 36 flows, one unit-column precoder per subband (tag = block mod nb)."""
+    if name == "of0":
+        return OfdmWorkload("of0", 6, 26, 36, 2048, 144, 64, 7,
+                            "6 symbols x 26 subbands, f = 36, 64-QAM, seed 7")
+    if name == "of1":
+        return OfdmWorkload("of1", 1 << 15, 26, 36, 2048, 144, 64, 8,
+                            "2^15 symbols x 26 subbands (851 968 blocks), f = 36, 64-QAM, seed 8")
+    raise ValueError(name)
+
+
+def ofdm_tags(block_ids, nb: int) -> np.ndarray:
+    """Subband of each block: blocks of a symbol are its subbands in order (block mod nb)."""
+    return (np.asarray(block_ids, dtype=np.int64) % nb).astype(np.int32)
+
+
+def ofdm_inputs(wl: OfdmWorkload, sym_ids=None):
+    """(W complex64 [nb][64][f], S complex64 [len(sym_ids) * nb][f][60], tags int32) for the
+    given symbols (default: all)."""
+    if sym_ids is None:
+        sym_ids = np.arange(wl.n_sym, dtype=np.int64)
+    sym_ids = np.asarray(sym_ids, dtype=np.int64).reshape(-1)
+    ids = (sym_ids[:, None] * wl.nb + np.arange(wl.nb)[None, :]).reshape(-1)
+    W = precoders(wl.seed, 0, wl.nb, wl.n_ant, wl.f, "unit_columns")
+    S = qam_symbols(wl.seed, 0, ids, wl.f, wl.b, wl.M)
+    return W, S, ofdm_tags(ids, wl.nb)

@@ -6,9 +6,10 @@ package.  The product package ``paper_1810_11451_b200`` never imports it and
 shares no code with it; the only shared module is the input generator
 ``bf_synth`` (no arithmetic of the method).
 
-The arithmetic lives in ``bf_oracle.c`` (beamforming) and
-``filter_oracle.c`` (the filter stage IFFT(MULT(FFT(s)))): plain
-C, fp64, one rounding to fp32; see their headers for the passage-by-passage
+The arithmetic lives in ``bf_oracle.c`` (beamforming),
+``filter_oracle.c`` (the filter stage IFFT(MULT(FFT(s)))) and
+``ofdm_oracle.c`` (beamforming followed by the per-antenna OFDM IFFT, SURVEY.md
+§8(f) row 4): plain C, fp64, one rounding to fp32; see their headers for the passage-by-passage
 reading.  This file only builds the C library with gcc and marshals numpy arrays.
 
 Pins (tests/test_oracle_pins.py, ``-m "not gpu"``): hand-expanded golden
@@ -28,7 +29,8 @@ import tempfile
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRCS = [os.path.join(_HERE, "bf_oracle.c"), os.path.join(_HERE, "filter_oracle.c")]
+_SRCS = [os.path.join(_HERE, "bf_oracle.c"), os.path.join(_HERE, "filter_oracle.c"),
+         os.path.join(_HERE, "ofdm_oracle.c")]
 _LIB = os.path.join(_HERE, "libbforacle.so")
 _CFLAGS = ["-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math",
            "-pthread"]
@@ -67,6 +69,11 @@ def _load():
         lib.fo_filter.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                   ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
                                   ctypes.c_int]
+        lib.fm_ofdm.restype = ctypes.c_int
+        lib.fm_ofdm.argtypes = [
+            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
+            ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_void_p,
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
         _lib = lib
     return _lib
 
@@ -148,4 +155,38 @@ def filter_apply(s: np.ndarray, h: np.ndarray, n_threads: int = 1, direct: bool 
                            int(n_threads))
     if rc != 0:
         raise ValueError("oracle rejected the arguments")
+    return y, bound
+
+
+# ---------------------------------------------------------------------------
+# OFDM output: per-antenna IFFT of the beamformed symbol
+# ---------------------------------------------------------------------------
+def ofdm(W: np.ndarray, S: np.ndarray, nb: int, n: int = 2048, cp: int = 0, scale: float = 1.0,
+         group_idx: np.ndarray | None = None, n_threads: int = 1):
+    """y[m][a] = CP(scale * IDFT_unnormalised(map(R[m*nb : m*nb+nb][a]))) from fp64 R = W x S.
+
+    W: complex64 [G][A][F] (or [A][F]); S: complex64 [n_sym*nb][F][b]; group_idx int32
+    [n_sym*nb] or None.  Subcarrier q of a symbol (block q // b, element q % b) sits in bin
+    (q - nb*b/2) mod n.  Returns (y complex64 [n_sym][A][cp + n], bound float64 [n_sym][A]).
+    """
+    W = np.ascontiguousarray(W, dtype=np.complex64)
+    if W.ndim == 2:
+        W = W[None]
+    S = np.ascontiguousarray(S, dtype=np.complex64)
+    G, A, F = W.shape
+    nblk, F2, B = S.shape
+    if F2 != F or nblk % nb != 0:
+        raise ValueError("S must be [n_sym*nb][f][b] with W's f")
+    n_sym = nblk // nb
+    gi = None
+    if group_idx is not None:
+        gi = np.ascontiguousarray(group_idx, dtype=np.int32)
+        if gi.shape != (nblk,):
+            raise ValueError("group_idx must have one entry per block")
+    y = np.empty((n_sym, A, cp + n), dtype=np.complex64)
+    bound = np.empty((n_sym, A), dtype=np.float64)
+    rc = _load().fm_ofdm(A, F, B, G, n_sym, int(nb), int(n), int(cp), float(scale), _ptr(W),
+                         _ptr(S), _ptr(gi), _ptr(y), _ptr(bound), int(n_threads))
+    if rc != 0:
+        raise ValueError("oracle rejected the arguments (sizes or group index)")
     return y, bound
