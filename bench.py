@@ -36,7 +36,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c4", help="c2 | c3 | c4 (default) | c5")
+    ap.add_argument("--config", default="c4", help="c2 | c3 | c4 (default) | c5 | fl0 | fl1 | of0 | of1")
     ap.add_argument("--f", type=int, default=36, help="flow count for --config c3")
     ap.add_argument("--layout", default="interleaved",
                     choices=["interleaved", "planar", "interleaved_f16out", "interleaved_i16out"])
@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--parity-stride", type=int, default=16,
                     help="check every k-th block of each rank's output against the oracle after "
                          "the timed region (c4: 65 536 of 2^20 blocks; c2: every block)")
+    ap.add_argument("--ofdm-chunk", type=int, default=0,
+                    help="of*: symbols per bf_apply + IFFT pair inside bf_ofdm_apply (0 = libbf default)")
     ap.add_argument("--c5-batch", type=int, default=16,
                     help="c5: consecutive chunks per bf_apply_batch launch (1 = one bf_apply_routed per "
                          "chunk; 16 = two of every cell, the kernel's job limit)")
@@ -78,6 +80,8 @@ def dist_env():
 
 def workload_of(args):
     import bf_synth as syn
+    if args.config.startswith("of"):
+        return syn.ofdm_workload(args.config)
     if args.config.startswith("fl"):
         return syn.filter_workload(args.config)
     if args.config == "c3":
@@ -387,6 +391,8 @@ def run_ours(args):
     wl = workload_of(args)
     if isinstance(wl, syn.FilterWorkload):
         return run_filter(args, wl, world, rank, local, dev)
+    if isinstance(wl, syn.OfdmWorkload):
+        return run_ofdm(args, wl, world, rank, local, dev)
     if wl.f < 0:
         return run_c5(args, wl, world, rank, local, dev)
     planar = args.layout == "planar"
@@ -937,6 +943,204 @@ def run_filter(args, wl, world, rank, local, dev):
                          "traffic_basis": tbasis,
                          "kernel": "bff::filter_warp_kernel<2, true> (one warp per signal, twiddles folded into the butterflies)", "kernel_ms": kavg,
                          "algorithmic_bytes_per_launch": bytes_launch,
+                         "peak_basis": peak_basis(peaks)},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+            "parity": parity,
+        }
+        if parity["ok"]:
+            print(json.dumps(line), flush=True)
+        else:
+            refuse(line, parity)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0 if parity["ok"] else 3
+
+
+def run_ofdm(args, wl, world, rank, local, dev):
+    """OFDM output stage (include/bf_ofdm.h): beamform every block of
+    a symbol, then the per-antenna 2048-point IFFT with cyclic prefix
+    (readings O1-O5), through bf_ofdm_apply over the rank's share of the symbols."""
+    import torch
+    import torch.distributed as dist
+
+    import benchkit
+    import bf_synth as syn
+    import bf_synth.cuda as sync
+    import oracle
+    from paper_1810_11451_b200 import OfdmPlan, Plan, shard
+
+    first, n_loc = shard.even_range(wl.n_sym, rank, world)
+    nblk = n_loc * wl.nb
+    S = torch.empty((nblk, wl.f, wl.b), dtype=torch.complex64, device=dev)
+    sync.gen_symbols(S, wl.seed, 0, wl.f, wl.b, wl.M, first=first * wl.nb)
+    tags = (torch.arange(first * wl.nb, first * wl.nb + nblk, device=dev) % wl.nb).to(torch.int32)
+    W = syn.precoders(wl.seed, 0, wl.nb, wl.n_ant, wl.f, "unit_columns")
+    scale = float(np.float32(1.0 / np.sqrt(wl.n)))
+    plan = Plan(wl.f, variant=args.variant)
+    plan.set_precoders(torch.from_numpy(W).to(dev))
+    op = OfdmPlan(plan, wl.nb, n=wl.n, cp=wl.cp, scale=scale)
+    if args.ofdm_chunk > 0:
+        op.set_chunk(args.ofdm_chunk)
+    y = torch.empty(op.y_shape(n_loc), dtype=torch.complex64, device=dev)
+    for _ in range(max(args.warmup, 0)):
+        op.apply(S, tags, out=y)
+    torch.cuda.synchronize()
+    clocks = benchkit.ClockSampler(local, period_ms=25).start() if rank == 0 else None
+    plan.set_profiling(True)
+    op.set_profiling(True)
+    plan.kernel_time()
+    op.kernel_time()
+    l0 = plan.launch_count() + op.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    main = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(main)
+    for _ in range(args.steps):
+        op.apply(S, tags, out=y)
+    e1.record(main)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed = shard.max_over_ranks(e0.elapsed_time(e1), dev)
+    ifft_ms, ifft_n = op.kernel_time()
+    bf_ms, bf_n = plan.kernel_time()
+    ifft_ms = shard.max_over_ranks(ifft_ms, dev)
+    bf_ms = shard.max_over_ranks(bf_ms, dev)
+    launches = int(shard.sum_over_ranks(plan.launch_count() + op.launch_count() - l0, dev))
+    clk = clocks.stop() if clocks else None
+    plan.set_profiling(False)
+    op.set_profiling(False)
+    peaks = benchkit.measured_peaks()
+    hbm = peaks["hbm_gbs"]
+    ms_step = elapsed / args.steps
+    value = wl.n_sym * wl.nb * wl.b * args.steps / (elapsed * 1e-3)
+    # per-kernel algorithmic bytes (DESIGN.md §10 row 4): IFFT 8 Nsc read + 8 (cp + n) written
+    # per (symbol, antenna); beamforming 8 f b read + 8 n_ant b written per block
+    ifft_bytes = n_loc * wl.n_ant * 8 * (wl.nb * wl.b + wl.cp + wl.n) * args.steps
+    bf_bytes = nblk * 8 * wl.b * (wl.f + wl.n_ant) * args.steps
+    kern = {
+        "bfofdm::ofdm_ifft_kernel": {"ms_per_step": ifft_ms / args.steps, "launches": ifft_n,
+                                     "achieved_gbs": ifft_bytes / (ifft_ms * 1e-3) / 1e9},
+        "bftc::bf_tc_kernel (via bf_apply, incl. routing)": {
+            "ms_per_step": bf_ms / args.steps, "launches": bf_n,
+            "achieved_gbs": bf_bytes / (bf_ms * 1e-3) / 1e9},
+    }
+    dom = max(kern, key=lambda k: kern[k]["ms_per_step"])
+    ach = kern[dom]["achieved_gbs"]
+    fused_b = wl.symbol_bytes(fused=True) * n_loc
+    unfused_b = wl.symbol_bytes(fused=False) * n_loc
+    step_gbs = fused_b / (ms_step * 1e-3) / 1e9
+
+    # parity: every 1024th symbol of the rank (all 64 antennas) vs the fp64 oracle (O5)
+    t0p = time.perf_counter()
+    lp = np.arange(0, n_loc, max(1, min(1024, n_loc // 8 or 1)), dtype=np.int64)
+    Wp, Sp, tp = syn.ofdm_inputs(wl, first + lp)
+    y_ref, bnd = oracle.ofdm(Wp, Sp, wl.nb, n=wl.n, cp=wl.cp, scale=scale, group_idx=tp,
+                             n_threads=oracle.max_threads())
+    got = y[torch.from_numpy(lp).to(dev)].cpu().numpy()
+    rel = np.abs(got.astype(np.complex128) - y_ref.astype(np.complex128)).max(axis=2) / bnd
+    parity = {"blocks": int(len(lp) * wl.n_ant), "unit": "(symbol, antenna) signals",
+              "worst_err_over_bound": float(rel.max()), "ok": bool((rel <= TOL).all()), "tol": TOL,
+              "check_s": time.perf_counter() - t0p,
+              "sample": f"every {int(lp[1] - lp[0]) if len(lp) > 1 else 1}th symbol of each rank's "
+                        "output (all antennas) after the timed steps vs the fp64 oracle"}
+    parity = reduce_parity({**parity, "worst_err_over_T": parity["worst_err_over_bound"]}, dev, world)
+    del y_ref, got
+
+    # ---- e2e: pinned host S + tags -> H2D -> bf_ofdm_apply -> D2H y, 3 streams ----------
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        chunk = 256
+        n_e2e = min(n_loc, 2048 if args.e2e_blocks <= 0 else args.e2e_blocks)
+        Sh = torch.empty((n_e2e * wl.nb, wl.f, wl.b), dtype=torch.complex64).pin_memory()
+        Sh.copy_(S[:n_e2e * wl.nb])
+        th = tags[:n_e2e * wl.nb].cpu().pin_memory()
+        yh = torch.empty((n_e2e, wl.n_ant, wl.cp + wl.n), dtype=torch.complex64).pin_memory()
+        slots = 3
+        dS = [torch.empty((chunk * wl.nb, wl.f, wl.b), dtype=torch.complex64, device=dev) for _ in range(slots)]
+        dt_ = [torch.empty((chunk * wl.nb,), dtype=torch.int32, device=dev) for _ in range(slots)]
+        dy = [torch.empty(op.y_shape(chunk), dtype=torch.complex64, device=dev) for _ in range(slots)]
+        st_h2d, st_cmp, st_d2h = (torch.cuda.Stream(dev) for _ in range(3))
+        ev_h = [torch.cuda.Event() for _ in range(slots)]
+        ev_c = [torch.cuda.Event() for _ in range(slots)]
+        ev_d = [torch.cuda.Event() for _ in range(slots)]
+
+        def e2e_step():
+            for i, c0 in enumerate(range(0, n_e2e, chunk)):
+                k, nc = i % slots, min(chunk, n_e2e - c0)
+                with torch.cuda.stream(st_h2d):
+                    if i >= slots:
+                        st_h2d.wait_event(ev_d[k])
+                    dS[k][:nc * wl.nb].copy_(Sh[c0 * wl.nb:(c0 + nc) * wl.nb], non_blocking=True)
+                    dt_[k][:nc * wl.nb].copy_(th[c0 * wl.nb:(c0 + nc) * wl.nb], non_blocking=True)
+                    ev_h[k].record(st_h2d)
+                st_cmp.wait_event(ev_h[k])
+                op.apply(dS[k][:nc * wl.nb], dt_[k][:nc * wl.nb], out=dy[k][:nc], stream=st_cmp)
+                ev_c[k].record(st_cmp)
+                with torch.cuda.stream(st_d2h):
+                    st_d2h.wait_event(ev_c[k])
+                    yh[c0:c0 + nc].copy_(dy[k][:nc], non_blocking=True)
+                    ev_d[k].record(st_d2h)
+            main.wait_stream(st_d2h)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(main)
+        st_h2d.wait_stream(main)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+            st_h2d.wait_stream(main)
+        f1.record(main)
+        torch.cuda.synchronize()
+        e2e_ms = shard.max_over_ranks(f0.elapsed_time(f1), dev)
+        n_tot = int(shard.sum_over_ranks(n_e2e, dev))
+        e2e = {"value": n_tot * wl.nb * wl.b * args.e2e_steps / (e2e_ms * 1e-3), "unit": "REs/s",
+               "h2d_bytes_per_step": n_tot * wl.nb * (wl.f * wl.b * 8 + 4),
+               "d2h_bytes_per_step": n_tot * wl.n_ant * (wl.cp + wl.n) * 8,
+               "steps": args.e2e_steps, "symbols_per_step": n_tot,
+               "ms_per_step": e2e_ms / args.e2e_steps,
+               "path": "pinned host S + tags -> H2D -> OfdmPlan.apply (bf_ofdm_apply) -> D2H pinned "
+                       "y, 256-symbol chunks on three streams"}
+        del Sh, th, yh, dS, dt_, dy
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        thr = oracle.max_threads()
+        ns = max(1, thr // wl.n_ant)
+        Wc, Sc, tc = syn.ofdm_inputs(wl, np.arange(ns))
+        t0 = time.perf_counter()
+        oracle.ofdm(Wc, Sc, wl.nb, n=wl.n, cp=wl.cp, scale=scale, group_idx=tc, n_threads=thr)
+        per = (time.perf_counter() - t0) / ns
+        ns = int(min(wl.n_sym, max(1, args.cpu_seconds / max(per, 1e-9))))
+        Wc, Sc, tc = syn.ofdm_inputs(wl, np.arange(ns))
+        t0 = time.perf_counter()
+        oracle.ofdm(Wc, Sc, wl.nb, n=wl.n, cp=wl.cp, scale=scale, group_idx=tc, n_threads=thr)
+        dt = time.perf_counter() - t0
+        cpu = {"value": ns * wl.nb * wl.b / dt, "unit": "REs/s", "cores": thr, "kind": "oracle",
+               "sample": f"{ns} symbols of {wl.name} ({dt:.1f} s, fp64 W x S + O(n Nsc) IDFTs)"}
+    if rank == 0:
+        line = {
+            "metric": "beamformed + OFDM-modulated REs/s (W x S, 2048-pt IFFT + CP per antenna)",
+            "value": value, "unit": "REs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl.name, "desc": wl.desc, "n_sym": wl.n_sym, "nb": wl.nb,
+                       "f": wl.f, "n": wl.n, "cp": wl.cp, "scale": scale,
+                       "chunk_symbols": args.ofdm_chunk or 4096, "variant": args.variant,
+                       "parallelism": f"dp{world}", "l2": "inputs larger than L2",
+                       "gpu": torch.cuda.get_device_name(dev)},
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                         "frac": ach / hbm, "traffic": None, "kernel": dom,
+                         "kernel_ms_per_step": kern[dom]["ms_per_step"], "kernels": kern,
+                         "step": {"fused_bytes_per_step": fused_b, "unfused_bytes_per_step": unfused_b,
+                                  "achieved_gbs_fused_bytes": step_gbs, "frac_fused_bound": step_gbs / hbm,
+                                  "frac_unfused_bound": unfused_b / (ms_step * 1e-3) / 1e9 / hbm,
+                                  "note": "fused = S read + y written per symbol (no R round trip); "
+                                          "unfused = + R written and read back"},
                          "peak_basis": peak_basis(peaks)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
             "parity": parity,

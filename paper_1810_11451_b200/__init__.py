@@ -8,8 +8,9 @@ Python binding.  Importing it loads libbf.so and fails loudly if it is absent.
 from ._lib import BfError, Layout, Status, Variant, lib
 from .plan import MAX_F, N_ANT, N_RE, Plan, Server, apply_batch, plan_create_status
 from .filter import FILTER_N, FilterPlan, filter_plan_create_status
+from .ofdm import OFDM_N, OfdmPlan
 
 lib()   # load now: no silent fallback path exists
 
 __all__ = ["Plan", "Server", "apply_batch", "Layout", "Status", "Variant", "BfError", "plan_create_status", "N_ANT", "N_RE",
-           "MAX_F", "FilterPlan", "FILTER_N", "filter_plan_create_status"]
+           "MAX_F", "FilterPlan", "FILTER_N", "filter_plan_create_status", "OfdmPlan", "OFDM_N"]

@@ -74,7 +74,7 @@ def build(verbose: bool = False) -> list[str]:
     inc = os.path.join(ROOT, "include")
     nvcc_shared(sorted(glob.glob(os.path.join(csrc, "*.cu"))), LIBBF, [inc, csrc],
                 sorted(glob.glob(os.path.join(csrc, "*.cuh")) + glob.glob(os.path.join(csrc, "*.h"))
-                       + [os.path.join(inc, "bf.h")]),
+                       + sorted(glob.glob(os.path.join(inc, "*.h")))),
                 os.path.join(ROOT, "build", "libbf"), verbose)
     nvcc_shared([os.path.join(ROOT, "bf_synth", "csrc", "synth.cu")], LIBSYNTH, [], [],
                 os.path.join(ROOT, "build", "synth"), verbose)

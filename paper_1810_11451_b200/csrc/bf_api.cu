@@ -1070,6 +1070,20 @@ bf_status bf_plan_set_variant(bf_plan_t p, int variant) {
     return BF_OK;
 }
 
+}  // extern "C"
+
+bf_status bfh::plan_info(bf_plan_t p, int *n_ant, int *f, int *b, int *layout, int *device) {
+    if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
+    *n_ant = p->n_ant;
+    *f = p->f;
+    *b = p->b;
+    *layout = p->layout;
+    *device = p->device;
+    return BF_OK;
+}
+
+extern "C" {
+
 bf_status bf_plan_get_variant(bf_plan_t p, int *resolved) {
     if (!p || !resolved) return fail(BF_ERR_INVALID_VALUE, "NULL argument");
     *resolved = p->f == 0 ? BF_VARIANT_AUTO : (use_tensor(p) ? BF_VARIANT_TENSOR : BF_VARIANT_FFMA);

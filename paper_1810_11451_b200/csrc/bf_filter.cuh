@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas(kNS)) filter_kernel(const F
 }
 
 // tw[m] = e^{-2 pi i m / N}, evaluated in fp64 and rounded once.
-__global__ void twiddle_kernel(float2 *tw) {
+static __global__ void twiddle_kernel(float2 *tw) {
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= kTwN) return;
     double s, c;
@@ -359,7 +359,7 @@ __global__ void twiddle_kernel(float2 *tw) {
 }
 
 // tw3[e 128 + t] = (w^(r t), w^(r (t + 128))) with r = 2^e, fp64-evaluated, rounded once.
-__global__ void twiddle3_kernel(float4 *tw3) {
+static __global__ void twiddle3_kernel(float4 *tw3) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= kTw3N) return;
     const int r = 1 << (i / 128), t = i % 128;

@@ -216,11 +216,11 @@ __device__ __forceinline__ void fetch_signal(c2 *buf, const float2 *src, uint64_
     bfk::mbar_arrive_expect_tx(bar, (uint32_t)(kN * 8));
     bfk::bulk_g2s(buf, src, kN * 8, bar, bfk::policy_evict_first());
 }
-// FOLD: twiddles folded into the butterflies (needs TAB)
-template <bool TAB, bool FOLD = false>
-__device__ __forceinline__ void fft2048_warp(c2 (&a)[64], c2 *buf, const float4 *__restrict__ twp,
-                                             const float2 *tws, int l, const float2 *next,
-                                             uint64_t *bar) {
+// FOLD: twiddles folded into the butterflies (needs TAB).  fetch(): called by every lane
+// once pass 2 has read the exchange buffer (it may refill buf with the next input)
+template <bool TAB, bool FOLD, class Fetch>
+__device__ __forceinline__ void fft2048_warp_x(c2 (&a)[64], c2 *buf, const float4 *__restrict__ twp,
+                                               const float2 *tws, int l, Fetch &&fetch) {
     // pass 1: radix 64, inputs a[r] = x[l + 32 r]; output y[64 l + k] = X1[k] (a[tr64(k)])
     if (FOLD) dft64f(a);
     else dft64(a);
@@ -233,13 +233,7 @@ __device__ __forceinline__ void fft2048_warp(c2 (&a)[64], c2 *buf, const float4 
     for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int r = 0; r < 32; ++r) a[h + 2 * r] = buf[wpad(l + 32 * h + 64 * r)];
-    if (next) {                    // last transform of the signal: the buffer is free now
-        __syncwarp();
-        if (l == 0) {
-            bfk::fence_proxy_async_smem();             // generic reads before the async write
-            fetch_signal(buf, next, bar);
-        }
-    }
+    fetch();
     // twiddles w^(r j): TAB — from the CTA's shared table tws[r][j] (rounded once);
     // otherwise r = 8 b + c from T1[c] = w^(c j), c < 8 and T2[b] = w^(8 b j), b < 4, with
     // twp[e][j] = (w^(2^e j)) for e < 5 (float2 pairs of j and j + 32 in one float4)
@@ -288,6 +282,20 @@ __device__ __forceinline__ void fft2048_warp(c2 (&a)[64], c2 *buf, const float4 
         for (int k = 0; k < 32; ++k) t[h + 2 * k] = a[h + 2 * tr32(k)];
 #pragma unroll
     for (int s = 0; s < 64; ++s) a[s] = t[s];
+}
+template <bool TAB, bool FOLD = false>
+__device__ __forceinline__ void fft2048_warp(c2 (&a)[64], c2 *buf, const float4 *__restrict__ twp,
+                                             const float2 *tws, int l, const float2 *next,
+                                             uint64_t *bar) {
+    fft2048_warp_x<TAB, FOLD>(a, buf, twp, tws, l, [&] {
+        if (next) {                // last transform of the signal: the buffer is free now
+            __syncwarp();
+            if (l == 0) {
+                bfk::fence_proxy_async_smem();         // generic reads before the async write
+                fetch_signal(buf, next, bar);
+            }
+        }
+    });
 }
 
 // MINC: CTAs per SM the register budget is sized for (3: 168 registers, 12 warps per SM;
@@ -373,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, MINC) filter_warp_kernel(const FPara
 // pass-2 base twiddles of the warp kernel: twp[e 32 + l] = (w^(2^e l), w^(2^e (l + 32))),
 // e < 5, fp64-evaluated, rounded once.
 constexpr int kTwpN = 5 * 32;
-__global__ void twiddle_warp_kernel(float4 *twp) {
+static __global__ void twiddle_warp_kernel(float4 *twp) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= kTwpN) return;
     const int e = i / 32, l = i % 32;

@@ -29,6 +29,9 @@ inline bf_status cuda_fail(cudaError_t e, const char *what) {
     return fail(BF_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
 }
 
+// Plan facts for the other stages of the library (bf_ofdm_api.cu); defined in bf_api.cu.
+bf_status plan_info(bf_plan_t p, int *n_ant, int *f, int *b, int *layout, int *device);
+
 // Makes `dev` current for the scope of a call and restores the caller's device.
 struct DeviceGuard {
     int prev = -1;

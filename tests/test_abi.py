@@ -21,7 +21,7 @@ def bf():
 
 def _declared_functions():
     names = set()
-    for hdr in ("bf.h", "bf_filter.h"):
+    for hdr in ("bf.h", "bf_filter.h", "bf_ofdm.h"):
         src = open(os.path.join(ROOT, "include", hdr)).read()
         src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
         names |= set(re.findall(r"\b(bff?_[a-z_]+)\s*\(", src))
