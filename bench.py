@@ -1029,6 +1029,15 @@ def run_ofdm(args, wl, world, rank, local, dev):
     }
     dom = max(kern, key=lambda k: kern[k]["ms_per_step"])
     ach = kern[dom]["achieved_gbs"]
+    traffic, tbasis = None, None
+    if dom.startswith("bfofdm"):
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))["bfofdm::ofdm_ifft_kernel"]
+            traffic = tr["dram_bytes_per_signal"] * n_loc * wl.n_ant
+            tbasis = (f"{tr['capture']}: {tr['dram_bytes_per_signal']:.0f} B/signal (algorithmic "
+                      f"{tr['algorithmic_bytes_per_signal']}) x {n_loc * wl.n_ant} signals per step")
+        except (OSError, KeyError, ValueError):
+            pass
     fused_b = wl.symbol_bytes(fused=True) * n_loc
     unfused_b = wl.symbol_bytes(fused=False) * n_loc
     step_gbs = fused_b / (ms_step * 1e-3) / 1e9
@@ -1134,7 +1143,9 @@ def run_ofdm(args, wl, world, rank, local, dev):
                        "parallelism": f"dp{world}", "l2": "inputs larger than L2",
                        "gpu": torch.cuda.get_device_name(dev)},
             "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                         "frac": ach / hbm, "traffic": None, "kernel": dom,
+                         "frac": ach / hbm, "traffic": traffic, "traffic_basis": tbasis,
+                         "algorithmic_bytes_per_step": ifft_bytes // args.steps if dom.startswith("bfofdm")
+                         else bf_bytes // args.steps, "kernel": dom,
                          "kernel_ms_per_step": kern[dom]["ms_per_step"], "kernels": kern,
                          "step": {"fused_bytes_per_step": fused_b, "unfused_bytes_per_step": unfused_b,
                                   "achieved_gbs_fused_bytes": step_gbs, "frac_fused_bound": step_gbs / hbm,
