@@ -37,9 +37,11 @@ struct OParams {
     float scale;
 };
 
-constexpr int kThreads = 128;   // 4 warps, one signal each at a time
-// exchange buffers, their mbarriers, the CTA's copy of the pass-2 twiddles (folded order)
-__host__ __device__ constexpr int smem_bytes() { return 4 * kWarpPad * 8 + 4 * 8 + kN * 8; }
+// per CTA: NW warps x NBUF (exchange / input buffer + its mbarrier), the CTA's copy of the
+// pass-2 twiddles (folded order)
+__host__ __device__ constexpr int smem_bytes(int nbuf, int nw) {
+    return nw * nbuf * (kWarpPad * 8 + 8) + kN * 8 + 64 * 16;   // + the run table (cp.async)
+}
 
 // One bulk copy of a signal's fetch: a run of subcarriers of one block -> its bins (O2).
 // The runs of blocks at or above the middle go to bins 0, 1, ..., those below to bins
@@ -100,40 +102,89 @@ __device__ __forceinline__ void fetch_symbol(c2 *buf, const OParams &p, int64_t 
     if (d1.bytes) bfk::bulk_g2s(buf + d1.dst, src + d1.src_off, d1.bytes, bar, pol);
 }
 
-__global__ void __launch_bounds__(kThreads, 2) ofdm_ifft_kernel(const OParams p) {
+// NBUF buffers per warp, NW warps per CTA.  NBUF = 1 (4 warps, 2 CTAs per SM): the next
+// signal's runs can be fetched only once the current transform's pass 2 has read the
+// buffer (the exchange reuses it).  NBUF = 2 (6 warps, 1 CTA per SM, 216 KB of shared
+// memory): signal j's input and exchange live in buffer j % 2, and signal j + 1's fetch is
+// issued as soon as signal j's input is in registers — a whole signal of lead time, for 6
+// warps per SM instead of 8.
+// The same fetch with per-lane 16-byte cp.async (LDGSTS) instead of bulk copies: the bulk
+// copies of 480 B are served one at a time per SM (~60 cycles each, i.e. 26 per signal
+// about as long as the signal's whole compute: ncu shows the warps waiting on the fetch
+// even with a second buffer and a whole signal of lead time).  Lane l moves chunk l of
+// every run (30 chunks per 480-B run); the plan-constant run table (tab) is in shared
+// memory and read as broadcasts; each lane's copies arrive on the warp's mbarrier
+// (count 32) through cp.async.mbarrier.arrive.noinc.
+__device__ __forceinline__ void fetch_symbol_cpa(c2 *buf, const OParams &p, int64_t sig, uint64_t *bar,
+                                                 int l, const CopyDesc *tab, int n_copies) {
+    const int half = p.half;
+    float4 *z = reinterpret_cast<float4 *>(buf + half);
+    const int nz = (kN - 2 * half) / 2;
+    for (int i = l; i < nz; i += 32) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t m = sig / p.A;
+    const int a = (int)(sig - m * p.A);
+    const float2 *src = p.R + ((m * p.nb) * (int64_t)p.A + a) * p.B + 2 * l;   // chunk l: 2 points
+    const uint32_t dst0 = bfk::smem_addr(buf) + 16u * l;
+    for (int c = 0; c < n_copies; ++c) {
+        const CopyDesc d = tab[c];
+        if (16u * l < d.bytes)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                         ::"r"(dst0 + 8u * d.dst), "l"(src + d.src_off) : "memory");
+    }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bfk::smem_addr(bar))
+                 : "memory");
+}
+
+template <int NBUF, int NW, bool CPA = false>
+__global__ void __launch_bounds__(NW * 32, NBUF == 1 ? 2 : 1) ofdm_ifft_kernel(const OParams p) {
     extern __shared__ __align__(128) unsigned char osm[];
     const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
-    c2 *buf = reinterpret_cast<c2 *>(osm) + warp * kWarpPad;
-    uint64_t *bar = reinterpret_cast<uint64_t *>(osm + 4 * kWarpPad * 8) + warp;
-    float2 *tws = reinterpret_cast<float2 *>(osm + 4 * kWarpPad * 8 + 4 * 8);   // folded order
-    for (int i = threadIdx.x; i < kN; i += kThreads)
-        tws[i] = p.tw[(bff::tws_fold_r(i) * bff::tws_fold_j(i)) & (kN - 1)];   // w^(r j)
-    const int64_t gw = (int64_t)blockIdx.x * 4 + warp, nw = (int64_t)gridDim.x * 4;
+    c2 *bufs = reinterpret_cast<c2 *>(osm) + warp * NBUF * kWarpPad;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(osm + NW * NBUF * kWarpPad * 8) + warp * NBUF;
+    float2 *tws = reinterpret_cast<float2 *>(osm + NW * NBUF * kWarpPad * 8 + NW * NBUF * 8);
+    for (int i = threadIdx.x; i < kN; i += NW * 32)
+        tws[i] = p.tw[(bff::tws_fold_r(i) * bff::tws_fold_j(i)) & (kN - 1)];   // w^(r j), folded order
+    const int64_t gw = (int64_t)blockIdx.x * NW + warp, nw = (int64_t)gridDim.x * NW;
     if (l == 0) {
-        bfk::mbar_init(bar, 1);
+        for (int b = 0; b < NBUF; ++b) bfk::mbar_init(bars + b, CPA ? 32 : 1);
         bfk::mbar_fence_init();
     }
     __syncwarp();
     const CopyDesc d0 = copy_desc(p, l), d1 = copy_desc(p, l + 32);
-    if (gw < p.n_sig) fetch_symbol(buf, p, gw, bar, l, d0, d1);
+    CopyDesc *tab = reinterpret_cast<CopyDesc *>(osm + NW * NBUF * kWarpPad * 8 + NW * NBUF * 8 + kN * 8);
+    const int n_copies = p.nb + ((p.half % p.B) ? 1 : 0);
+    if (CPA) {
+        for (int c = threadIdx.x; c < 64; c += NW * 32) tab[c] = copy_desc(p, c);
+        __syncthreads();
+    }
+    auto fetch = [&](c2 *b, int64_t sg, uint64_t *br) {
+        if (CPA) fetch_symbol_cpa(b, p, sg, br, l, tab, n_copies);
+        else fetch_symbol(b, p, sg, br, l, d0, d1);
+    };
+    if (gw < p.n_sig) fetch(bufs, gw, bars);
     __syncthreads();                                    // the twiddle table
     const int L = p.cp + kN, cp = p.cp;
     const c2 osc = bff::pk(p.scale, p.scale);
-    uint32_t phase = 0;
-    for (int64_t sig = gw; sig < p.n_sig; sig += nw) {
+    uint32_t j = 0;                                     // this warp's signal counter
+    for (int64_t sig = gw; sig < p.n_sig; sig += nw, ++j) {
+        const int cur = NBUF == 1 ? 0 : (int)(j & 1);
+        c2 *buf = bufs + cur * kWarpPad;
         c2 a[64];
-        bfk::mbar_wait(bar, phase);
-        phase ^= 1u;
+        bfk::mbar_wait(bars + cur, NBUF == 1 ? (j & 1) : ((j >> 1) & 1));
         __syncwarp();                                   // the other lanes' zero-bin stores
 #pragma unroll
         for (int s = 0; s < 64; ++s) a[s] = buf[l + 32 * s];              // X[bin], bin = l + 32 s
         const int64_t nxt = sig + nw;
+        if (NBUF == 2 && nxt < p.n_sig) {               // the other buffer: free since signal j - 1
+            c2 *nbuf = bufs + (cur ^ 1) * kWarpPad;
+            fetch(nbuf, nxt, bars + (cur ^ 1));
+        }
         // x[t] = scale sum_bin X[bin] e^{+2 pi i bin t / n} = scale F[(n - t) mod n], F the
         // forward DFT of X: the inverse without conjugations, the time reversal in the stores
         bff::fft2048_warp_x<true, true>(a, buf, nullptr, tws, l, [&] {
-            if (nxt < p.n_sig) {
+            if (NBUF == 1 && nxt < p.n_sig) {
                 __syncwarp();
-                fetch_symbol(buf, p, nxt, bar, l, d0, d1);
+                fetch(buf, nxt, bars);
             }
         });
         float2 *dst = p.y + sig * L;

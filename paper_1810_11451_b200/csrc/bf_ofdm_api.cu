@@ -3,7 +3,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <new>
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -25,6 +27,10 @@ struct bf_ofdm_plan_s {
     int n = bfofdm::kN, cp = 0, nb = 0, A = 64, B = 60, f = 0, device = 0;
     float scale = 1.0f;
     int num_sms = 0, ctas_per_sm = 0;
+    // IFFT kernel (BFO_OFDM_KERNEL): 1 sb ofdm_ifft_kernel<1, 4> (bulk-copy fetch), 2 db
+    // <2, 6>, 3 cpa <1, 4, true> (cp.async fetch; the default: of1 0.855 of copy BW vs 0.84 sb,
+    // 0.83 db, 0.72 cpa_db — profiles/r02_of1_kernels.jsonl), 4 cpa_db <2, 6, true>
+    int kind = 3;
     int64_t chunk = kDefaultChunk;
     float2 *tw = nullptr;
     float2 *R = nullptr;        // workspace [chunk nb][A][B]
@@ -50,7 +56,8 @@ size_t r_bytes(bf_ofdm_plan_t p, int64_t n_sym) { return (size_t)n_sym * p->nb *
 bf_status launch_ifft(bf_ofdm_plan_t p, const float2 *R, int64_t n_sym, float2 *y, cudaStream_t st) {
     bfofdm::OParams op{R, y, p->tw, n_sym * p->A, p->A, p->nb, p->B, p->nb * p->B / 2, p->cp, p->scale};
     const int64_t cap = (int64_t)p->num_sms * std::max(1, p->ctas_per_sm);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((op.n_sig + 3) / 4, cap));
+    const int nwarps = (p->kind == 2 || p->kind == 4) ? 6 : 4;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((op.n_sig + nwarps - 1) / nwarps, cap));
     cudaEvent_t e1 = nullptr;
     if (p->profiling) {
         if (p->prof_used == p->prof_events.size()) {
@@ -63,7 +70,14 @@ bf_status launch_ifft(bf_ofdm_plan_t p, const float2 *R, int64_t n_sym, float2 *
         e1 = p->prof_events[p->prof_used].second;
         ++p->prof_used;
     }
-    bfofdm::ofdm_ifft_kernel<<<grid, bfofdm::kThreads, bfofdm::smem_bytes(), st>>>(op);
+    if (p->kind == 2)
+        bfofdm::ofdm_ifft_kernel<2, 6><<<grid, 6 * 32, bfofdm::smem_bytes(2, 6), st>>>(op);
+    else if (p->kind == 3)
+        bfofdm::ofdm_ifft_kernel<1, 4, true><<<grid, 4 * 32, bfofdm::smem_bytes(1, 4), st>>>(op);
+    else if (p->kind == 4)
+        bfofdm::ofdm_ifft_kernel<2, 6, true><<<grid, 6 * 32, bfofdm::smem_bytes(2, 6), st>>>(op);
+    else
+        bfofdm::ofdm_ifft_kernel<1, 4><<<grid, 4 * 32, bfofdm::smem_bytes(1, 4), st>>>(op);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "ofdm_ifft_kernel launch");
     ++p->launches;
@@ -110,13 +124,21 @@ bf_status bf_ofdm_plan_create(bf_plan_t bf, int n, int cp, int nb, float scale, 
     p->f = f;
     p->device = dev;
     p->scale = scale;
+    // BFO_OFDM_KERNEL=sb|db selects the IFFT kernel for comparison experiments (default below)
+    if (const char *env = std::getenv("BFO_OFDM_KERNEL")) {
+        const std::string k(env);
+        p->kind = k == "db" ? 2 : k == "sb" ? 1 : k == "cpa_db" ? 4 : 3;
+    }
+    const bool db = p->kind == 2 || p->kind == 4;
+    const void *kern = p->kind == 2   ? (const void *)bfofdm::ofdm_ifft_kernel<2, 6>
+                       : p->kind == 3 ? (const void *)bfofdm::ofdm_ifft_kernel<1, 4, true>
+                       : p->kind == 4 ? (const void *)bfofdm::ofdm_ifft_kernel<2, 6, true>
+                                      : (const void *)bfofdm::ofdm_ifft_kernel<1, 4>;
+    const int smem = db ? bfofdm::smem_bytes(2, 6) : bfofdm::smem_bytes(1, 4);
+    const int threads = db ? 6 * 32 : 4 * 32;
     cudaError_t e = cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(bfofdm::ofdm_ifft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 bfofdm::smem_bytes());
-    if (e == cudaSuccess)
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->ctas_per_sm, bfofdm::ofdm_ifft_kernel,
-                                                          bfofdm::kThreads, bfofdm::smem_bytes());
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->ctas_per_sm, kern, threads, smem);
     if (e == cudaSuccess) e = cudaMalloc(&p->tw, bff::kTwN * sizeof(float2));
     if (e == cudaSuccess) {
         bff::twiddle_kernel<<<(bff::kTwN + 255) / 256, 256>>>(p->tw);

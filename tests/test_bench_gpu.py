@@ -112,6 +112,30 @@ def test_bench_c5_two_ranks_windows():
     assert par["ok"] and len(par["per_rank"]) == 2 and all(r["blocks"] > 0 for r in par["per_rank"])
 
 
+def test_bench_ofdm_contract():
+    d = _run(["--config", "of0", "--steps", "3", "--warmup", "3", "--cpu-seconds", "1",
+              "--e2e-steps", "1"])
+    for k in KEYS:
+        assert k in d, k
+    assert d["unit"] == "REs/s" and d["value"] > 0 and d["config"]["workload"] == "of0"
+    assert d["parity"]["ok"] and d["parity"]["blocks"] == 6 * 64      # every symbol, all antennas
+    assert d["roofline"]["kernel"] in d["roofline"]["kernels"]
+    assert d["e2e"]["d2h_bytes_per_step"] == 6 * 64 * (144 + 2048) * 8
+    assert d["gpu_launches"] >= 2 * 3
+
+
+def test_bench_ofdm_two_ranks_share_gpu():
+    d = _run(["--config", "of0", "--steps", "2", "--warmup", "3", "--no-e2e"], world=2)
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["cpu_baseline"] is None
+    par = d["parity"]
+    assert par["ok"] and len(par["per_rank"]) == 2 and all(r["blocks"] == 3 * 64 for r in par["per_rank"])
+
+
+def test_bench_ofdm_reference_arm():
+    d = _run(["--impl", "reference", "--config", "of0", "--steps", "1", "--warmup", "3"])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["config"]["workload"] == "of0"
+
+
 def test_bench_reference_arm():
     d = _run(["--impl", "reference", "--config", "c2", "--steps", "2", "--warmup", "3",
               "--cpu-seconds", "1"])

@@ -92,6 +92,21 @@ def test_many_signals_per_warp():
     assert check(y, y_ref, bound, "many signals") < 1e-6
 
 
+@pytest.mark.parametrize("kernel", ["sb", "db", "cpa", "cpa_db"])
+def test_each_ifft_kernel_matches_oracle(kernel, monkeypatch):
+    # every selectable IFFT kernel (BFO_OFDM_KERNEL, read at plan creation): one buffer per
+    # warp (4 warps, 2 CTAs per SM) and two (6 warps, 1 CTA per SM); odd nb, many signals
+    # per warp, a ragged signal count (not a multiple of the warps per CTA)
+    monkeypatch.setenv("BFO_OFDM_KERNEL", kernel)
+    rng = np.random.default_rng(14)
+    nb, n_sym, f = 3, 401, 5
+    W = gaussian(rng, (64, f))
+    S = gaussian(rng, (n_sym * nb, f, 60))
+    y_ref, bound = oracle.ofdm(W, S, nb, n=2048, cp=160, scale=0.75, n_threads=NT)
+    y = run(W, S, None, nb, 160, 0.75, chunk=100)
+    assert check(y, y_ref, bound, f"kernel {kernel}") < 1e-6
+
+
 def test_maximum_band_and_prefix():
     # nb = 34: 2040 of 2048 bins active (4 zero bins either side of n/2); cp = 2047 (max)
     rng = np.random.default_rng(13)
