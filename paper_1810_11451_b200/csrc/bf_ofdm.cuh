@@ -39,8 +39,11 @@ struct OParams {
 
 // per CTA: NW warps x NBUF (exchange / input buffer + its mbarrier), the CTA's copy of the
 // pass-2 twiddles (folded order)
+// mbarrier region rounded up to 16 B: the twiddle table and the run table after it are read
+// with 16-byte loads
+__host__ __device__ constexpr int bar_bytes(int nbuf, int nw) { return (nw * nbuf * 8 + 15) / 16 * 16; }
 __host__ __device__ constexpr int smem_bytes(int nbuf, int nw) {
-    return nw * nbuf * (kWarpPad * 8 + 8) + kN * 8 + 64 * 16;   // + the run table (cp.async)
+    return nw * nbuf * kWarpPad * 8 + bar_bytes(nbuf, nw) + kN * 8 + 64 * 16;   // + run table
 }
 
 // One bulk copy of a signal's fetch: a run of subcarriers of one block -> its bins (O2).
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(NW * 32, NBUF == 1 ? 2 : 1) ofdm_ifft_kernel(c
     const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
     c2 *bufs = reinterpret_cast<c2 *>(osm) + warp * NBUF * kWarpPad;
     uint64_t *bars = reinterpret_cast<uint64_t *>(osm + NW * NBUF * kWarpPad * 8) + warp * NBUF;
-    float2 *tws = reinterpret_cast<float2 *>(osm + NW * NBUF * kWarpPad * 8 + NW * NBUF * 8);
+    float2 *tws = reinterpret_cast<float2 *>(osm + NW * NBUF * kWarpPad * 8 + bar_bytes(NBUF, NW));
     for (int i = threadIdx.x; i < kN; i += NW * 32)
         tws[i] = p.tw[(bff::tws_fold_r(i) * bff::tws_fold_j(i)) & (kN - 1)];   // w^(r j), folded order
     const int64_t gw = (int64_t)blockIdx.x * NW + warp, nw = (int64_t)gridDim.x * NW;
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(NW * 32, NBUF == 1 ? 2 : 1) ofdm_ifft_kernel(c
     }
     __syncwarp();
     const CopyDesc d0 = copy_desc(p, l), d1 = copy_desc(p, l + 32);
-    CopyDesc *tab = reinterpret_cast<CopyDesc *>(osm + NW * NBUF * kWarpPad * 8 + NW * NBUF * 8 + kN * 8);
+    CopyDesc *tab = reinterpret_cast<CopyDesc *>(osm + NW * NBUF * kWarpPad * 8 + bar_bytes(NBUF, NW) + kN * 8);
     const int n_copies = p.nb + ((p.half % p.B) ? 1 : 0);
     if (CPA) {
         for (int c = threadIdx.x; c < 64; c += NW * 32) tab[c] = copy_desc(p, c);
