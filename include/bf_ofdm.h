@@ -72,6 +72,18 @@ bf_status bf_ofdm_apply(bf_ofdm_plan_t p, const void *S_dev, const int32_t *tags
 bf_status bf_ofdm_ifft(bf_ofdm_plan_t p, const void *R_dev, int64_t n_sym, void *y_dev,
                        void *stream);
 
+/* Output sample format of later bf_ofdm_apply / bf_ofdm_ifft calls.
+ *   BF_OFDM_OUT_F32  complex fp32 (re, im), 8 bytes per sample (the default);
+ *   BF_OFDM_OUT_I16  int16 (re, im) time-domain fronthaul samples, 4 bytes per sample:
+ *                    sat(rne(y * 2^exponent)) per component from the fp32 sample (the
+ *                    scaling by 2^exponent is exact), saturated to [-32768, 32767], NaN -> 0;
+ *                    y_dev then holds int16 pairs [n_sym][n_ant][cp + n].
+ * exponent in [-126, 127] (used by BF_OFDM_OUT_I16 only; 12 is a good default for
+ * scale = 1/sqrt(n): |y| < 8 at 2^-12 resolution).  BF_ERR_UNSUPPORTED when a comparison
+ * IFFT kernel (BFO_OFDM_KERNEL) is selected. */
+enum { BF_OFDM_OUT_F32 = 0, BF_OFDM_OUT_I16 = 1 };
+bf_status bf_ofdm_plan_set_output(bf_ofdm_plan_t p, int format, int exponent);
+
 /* Symbols per chunk of bf_ofdm_apply (0 = the default, 4096 symbols: a 3.3 GB workspace at
  * nb = 26). */
 bf_status bf_ofdm_plan_set_chunk(bf_ofdm_plan_t p, int64_t symbols);

@@ -22,7 +22,7 @@ EXPORTS = ("bf_plan_create", "bf_set_precoders", "bf_apply", "bf_apply_host", "b
            "bf_server_slot_time", "bf_server_trace", "bf_server_stop", "bf_server_destroy",
            "bff_plan_create", "bff_set_taps", "bff_apply", "bff_fft", "bff_destroy",
            "bff_plan_set_profiling", "bff_plan_kernel_time", "bff_plan_launch_count",
-           "bf_ofdm_plan_create", "bf_ofdm_apply", "bf_ofdm_ifft", "bf_ofdm_plan_set_chunk",
+           "bf_ofdm_plan_create", "bf_ofdm_apply", "bf_ofdm_ifft", "bf_ofdm_plan_set_chunk", "bf_ofdm_plan_set_output",
            "bf_ofdm_destroy", "bf_ofdm_plan_set_profiling", "bf_ofdm_plan_kernel_time",
            "bf_ofdm_plan_launch_count",
            "bf_status_string", "bf_last_error", "bf_version")

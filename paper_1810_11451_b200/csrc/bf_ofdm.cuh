@@ -29,12 +29,12 @@ using bff::kWarpPad;
 
 struct OParams {
     const float2 *R;      // [n_sym nb][A][B] complex fp32
-    float2 *y;            // [n_sym][A][cp + n]
+    float2 *y;            // [n_sym][A][cp + n] complex fp32 (or int16 pairs, OUT16)
     const float2 *tw;     // tw[m] = w^m, w = e^{-2 pi i / n} (bff::twiddle_kernel)
     int64_t n_sig;        // n_sym A
     int A, nb, B, half;   // half = nb B / 2
     int cp;
-    float scale;
+    float scale;          // OUT16: scale 2^e
 };
 
 // per CTA: NW warps x NBUF (exchange / input buffer + its mbarrier), the CTA's copy of the
@@ -138,7 +138,22 @@ __device__ __forceinline__ void fetch_symbol_cpa(c2 *buf, const OParams &p, int6
                  : "memory");
 }
 
-template <int NBUF, int NW, bool CPA = false>
+// the time samples of one output position: complex fp32, or (OUT16) int16 (re, im)
+// fronthaul samples sat(rne(y 2^e)) — 2^e is folded into the scale (exact), cvt.rni.sat
+// maps NaN to 0
+template <bool OUT16>
+__device__ __forceinline__ void store_sample(float2 *y, int64_t i, float2 v) {
+    if (OUT16) {
+        short a, b;
+        asm("cvt.rni.sat.s16.f32 %0, %1;" : "=h"(a) : "f"(v.x));
+        asm("cvt.rni.sat.s16.f32 %0, %1;" : "=h"(b) : "f"(v.y));
+        __stcs(reinterpret_cast<unsigned int *>(y) + i, (uint32_t)(uint16_t)a | ((uint32_t)(uint16_t)b << 16));
+    } else {
+        __stcs(y + i, v);
+    }
+}
+
+template <int NBUF, int NW, bool CPA = false, bool OUT16 = false>
 __global__ void __launch_bounds__(NW * 32, NBUF == 1 ? 2 : 1) ofdm_ifft_kernel(const OParams p) {
     extern __shared__ __align__(128) unsigned char osm[];
     const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -190,20 +205,20 @@ __global__ void __launch_bounds__(NW * 32, NBUF == 1 ? 2 : 1) ofdm_ifft_kernel(c
                 fetch(buf, nxt, bars);
             }
         });
-        float2 *dst = p.y + sig * L;
-        float2 *body = dst + cp + kN - l;               // F[k], k = l + 32 s -> t = n - k
+        const int64_t dst = sig * L;                    // sample index of the signal's start
+        const int64_t body = dst + cp + kN - l;         // F[k], k = l + 32 s -> t = n - k
 #pragma unroll
         for (int s = 0; s < 64; ++s) {
             const float2 v = bff::up(bff::mul2(a[s], osc));
-            if (s == 0) __stcs(l == 0 ? dst + cp : body, v);             // k = 0 -> t = 0
-            else __stcs(body - 32 * s, v);
+            if (s == 0) store_sample<OUT16>(p.y, l == 0 ? dst + cp : body, v);   // k = 0 -> t = 0
+            else store_sample<OUT16>(p.y, body - 32 * s, v);
         }
         // cyclic prefix (O4): y[t'] = x[n - cp + t'] — t = n - k >= n - cp, i.e. 1 <= k <= cp
 #pragma unroll
         for (int s = 0; s < 64; ++s) {
             if (32 * s > cp) break;                     // warp-uniform
             const int k = l + 32 * s;
-            if (k >= 1 && k <= cp) __stcs(dst + (cp - k), bff::up(bff::mul2(a[s], osc)));
+            if (k >= 1 && k <= cp) store_sample<OUT16>(p.y, dst + (cp - k), bff::up(bff::mul2(a[s], osc)));
         }
     }
 }

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <new>
 #include <string>
@@ -31,6 +32,8 @@ struct bf_ofdm_plan_s {
     // <2, 6>, 3 cpa <1, 4, true> (cp.async fetch; the default: of1 0.855 of copy BW vs 0.84 sb,
     // 0.83 db, 0.72 cpa_db — profiles/r02_of1_kernels.jsonl), 4 cpa_db <2, 6, true>
     int kind = 3;
+    bool out16 = false;         // bf_ofdm_plan_set_output: int16 samples x 2^out_exp
+    int out_exp = 12;
     int64_t chunk = kDefaultChunk;
     float2 *tw = nullptr;
     float2 *R = nullptr;        // workspace [chunk nb][A][B]
@@ -50,11 +53,14 @@ bool overlap(const void *a, size_t na, const void *b, size_t nb) {
     return a && b && na && nb && a0 < b0 + nb && b0 < a0 + na;
 }
 
-size_t y_bytes(bf_ofdm_plan_t p, int64_t n_sym) { return (size_t)n_sym * p->A * (p->cp + p->n) * 8; }
+size_t y_bytes(bf_ofdm_plan_t p, int64_t n_sym) {
+    return (size_t)n_sym * p->A * (p->cp + p->n) * (p->out16 ? 4 : 8);
+}
 size_t r_bytes(bf_ofdm_plan_t p, int64_t n_sym) { return (size_t)n_sym * p->nb * p->A * p->B * 8; }
 
 bf_status launch_ifft(bf_ofdm_plan_t p, const float2 *R, int64_t n_sym, float2 *y, cudaStream_t st) {
-    bfofdm::OParams op{R, y, p->tw, n_sym * p->A, p->A, p->nb, p->B, p->nb * p->B / 2, p->cp, p->scale};
+    bfofdm::OParams op{R, y, p->tw, n_sym * p->A, p->A, p->nb, p->B, p->nb * p->B / 2, p->cp,
+                       p->out16 ? ldexpf(p->scale, p->out_exp) : p->scale};
     const int64_t cap = (int64_t)p->num_sms * std::max(1, p->ctas_per_sm);
     const int nwarps = (p->kind == 2 || p->kind == 4) ? 6 : 4;
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((op.n_sig + nwarps - 1) / nwarps, cap));
@@ -72,6 +78,8 @@ bf_status launch_ifft(bf_ofdm_plan_t p, const float2 *R, int64_t n_sym, float2 *
     }
     if (p->kind == 2)
         bfofdm::ofdm_ifft_kernel<2, 6><<<grid, 6 * 32, bfofdm::smem_bytes(2, 6), st>>>(op);
+    else if (p->kind == 3 && p->out16)
+        bfofdm::ofdm_ifft_kernel<1, 4, true, true><<<grid, 4 * 32, bfofdm::smem_bytes(1, 4), st>>>(op);
     else if (p->kind == 3)
         bfofdm::ofdm_ifft_kernel<1, 4, true><<<grid, 4 * 32, bfofdm::smem_bytes(1, 4), st>>>(op);
     else if (p->kind == 4)
@@ -124,19 +132,23 @@ bf_status bf_ofdm_plan_create(bf_plan_t bf, int n, int cp, int nb, float scale, 
     p->f = f;
     p->device = dev;
     p->scale = scale;
+    cudaError_t e0_ = cudaSuccess;
     // BFO_OFDM_KERNEL=sb|db selects the IFFT kernel for comparison experiments (default below)
     if (const char *env = std::getenv("BFO_OFDM_KERNEL")) {
         const std::string k(env);
         p->kind = k == "db" ? 2 : k == "sb" ? 1 : k == "cpa_db" ? 4 : 3;
     }
     const bool db = p->kind == 2 || p->kind == 4;
+    e0_ = cudaFuncSetAttribute(bfofdm::ofdm_ifft_kernel<1, 4, true, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, bfofdm::smem_bytes(1, 4));
     const void *kern = p->kind == 2   ? (const void *)bfofdm::ofdm_ifft_kernel<2, 6>
                        : p->kind == 3 ? (const void *)bfofdm::ofdm_ifft_kernel<1, 4, true>
                        : p->kind == 4 ? (const void *)bfofdm::ofdm_ifft_kernel<2, 6, true>
                                       : (const void *)bfofdm::ofdm_ifft_kernel<1, 4>;
     const int smem = db ? bfofdm::smem_bytes(2, 6) : bfofdm::smem_bytes(1, 4);
     const int threads = db ? 6 * 32 : 4 * 32;
-    cudaError_t e = cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = e0_;
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p->ctas_per_sm, kern, threads, smem);
     if (e == cudaSuccess) e = cudaMalloc(&p->tw, bff::kTwN * sizeof(float2));
@@ -199,9 +211,23 @@ bf_status bf_ofdm_apply(bf_ofdm_plan_t p, const void *S_dev, const int32_t *tags
         s = bf_apply(p->bf, S ? S + m0 * s_sym : nullptr, tags_dev ? tags_dev + m0 * p->nb : nullptr,
                      p->R, c * p->nb, stream);
         if (s != BF_OK) return s;
-        s = launch_ifft(p, p->R, c, static_cast<float2 *>(y_dev) + m0 * p->A * (p->cp + p->n), st);
+        s = launch_ifft(p, p->R, c,
+                        reinterpret_cast<float2 *>(static_cast<char *>(y_dev) +
+                                                   y_bytes(p, m0)), st);
         if (s != BF_OK) return s;
     }
+    return BF_OK;
+}
+
+bf_status bf_ofdm_plan_set_output(bf_ofdm_plan_t p, int format, int exponent) {
+    if (!p) return fail(BF_ERR_INVALID_VALUE, "plan is NULL");
+    if (format != BF_OFDM_OUT_F32 && format != BF_OFDM_OUT_I16)
+        return fail(BF_ERR_INVALID_VALUE, "unknown output format %d", format);
+    if (exponent < -126 || exponent > 127) return fail(BF_ERR_INVALID_VALUE, "exponent out of range");
+    if (format == BF_OFDM_OUT_I16 && p->kind != 3)
+        return fail(BF_ERR_UNSUPPORTED, "int16 output is built for the default IFFT kernel only");
+    p->out16 = format == BF_OFDM_OUT_I16;
+    p->out_exp = exponent;
     return BF_OK;
 }
 

@@ -27,6 +27,7 @@ def _sig(L):
         "bf_ofdm_apply": [vp, vp, vp, i64, vp, vp],
         "bf_ofdm_ifft": [vp, vp, i64, vp, vp],
         "bf_ofdm_plan_set_chunk": [vp, i64],
+        "bf_ofdm_plan_set_output": [vp, i32, i32],
         "bf_ofdm_destroy": [vp],
         "bf_ofdm_plan_set_profiling": [vp, i32],
         "bf_ofdm_plan_kernel_time": [vp, P(ctypes.c_double), P(i64)],
@@ -59,9 +60,23 @@ class OfdmPlan:
         check(_lib().bf_ofdm_plan_create(plan._h, self.n, self.cp, self.nb, self.scale,
                                          ctypes.byref(self._h)))
         self.device = plan.device
+        self.out16, self.out_exp = False, 12
 
     def y_shape(self, n_sym: int):
+        if self.out16:     # int16 (re, im) pairs
+            return (n_sym, self.plan.n_ant, self.cp + self.n, 2)
         return (n_sym, self.plan.n_ant, self.cp + self.n)
+
+    @property
+    def y_dtype(self):
+        return torch.int16 if self.out16 else torch.complex64
+
+    def set_output(self, fmt: str = "f32", exponent: int = 12) -> None:
+        """bf_ofdm_plan_set_output: "f32" (complex64 samples) or "i16" (int16 (re, im) pairs,
+        sat(rne(y 2^exponent)))."""
+        code = {"f32": 0, "i16": 1}[fmt]
+        check(_lib().bf_ofdm_plan_set_output(self._h, code, int(exponent)))
+        self.out16, self.out_exp = code == 1, int(exponent)
 
     def _check(self, t, name, shape, dtype):
         if t.dtype != dtype or tuple(t.shape) != tuple(shape):
@@ -71,8 +86,8 @@ class OfdmPlan:
 
     def _out(self, n_sym, out):
         if out is None:
-            out = torch.empty(self.y_shape(n_sym), dtype=torch.complex64, device=self.device)
-        self._check(out, "out", self.y_shape(n_sym), torch.complex64)
+            out = torch.empty(self.y_shape(n_sym), dtype=self.y_dtype, device=self.device)
+        self._check(out, "out", self.y_shape(n_sym), self.y_dtype)
         return out
 
     def apply(self, S: torch.Tensor, tags: torch.Tensor | None = None,

@@ -175,3 +175,74 @@ def test_host_argument_errors():
     assert _lib().bf_ofdm_ifft(op._h, _ptr(R), 2, _ptr(R), None) == Status.INVALID_VALUE
     with pytest.raises(bf.BfError):
         op.set_chunk(-1)
+
+
+def test_of1_full_size_sampled():
+    # BASELINE-scale workload in the bench's launch configuration (of1: 2^15 symbols, the
+    # default 4096-symbol chunks, AUTO -> tensor kernel at f = 36): every 512th symbol (all
+    # antennas, 64 symbols, incl. the last one) vs the oracle
+    import bf_synth.cuda as sync
+    wl = syn.ofdm_workload("of1")
+    S = torch.empty((wl.n_blocks, wl.f, wl.b), dtype=torch.complex64, device=DEV)
+    sync.gen_symbols(S, wl.seed, 0, wl.f, wl.b, wl.M)
+    tags = (torch.arange(wl.n_blocks, device=DEV) % wl.nb).to(torch.int32)
+    W = syn.precoders(wl.seed, 0, wl.nb, wl.n_ant, wl.f, "unit_columns")
+    scale = float(np.float32(1.0 / np.sqrt(wl.n)))
+    plan = Plan(wl.f)
+    plan.set_precoders(torch.from_numpy(W).to(DEV))
+    op = OfdmPlan(plan, wl.nb, cp=wl.cp, scale=scale)
+    y = op.apply(S, tags)
+    del S
+    ids = np.unique(np.append(np.arange(0, wl.n_sym, 512), wl.n_sym - 1))
+    got = y[torch.from_numpy(ids).to(DEV)].cpu().numpy()
+    Wp, Sp, tp = syn.ofdm_inputs(wl, ids)
+    y_ref, bound = oracle.ofdm(Wp, Sp, wl.nb, n=wl.n, cp=wl.cp, scale=scale, group_idx=tp, n_threads=NT)
+    assert check(got, y_ref, bound, "of1 sampled") < 1e-6
+    del y
+    op.close()
+    plan.close()
+
+
+def test_int16_output_is_the_rounded_fp32_output():
+    # BF_OFDM_OUT_I16: sat(rne(y 2^e)) of the fp32 samples, bit for bit, at e = 12 (the
+    # bench's), 3 and 22 (mostly saturated); within 2^-(e+1) + the O5 bound of the oracle
+    wl = syn.ofdm_workload("of0")
+    W, S, tags = syn.ofdm_inputs(wl)
+    scale = float(np.float32(1.0 / np.sqrt(wl.n)))
+    plan = Plan(wl.f)
+    plan.set_precoders(torch.from_numpy(W).to(DEV))
+    op = OfdmPlan(plan, wl.nb, cp=wl.cp, scale=scale)
+    Sd, td = torch.from_numpy(S).to(DEV), torch.from_numpy(tags).to(DEV)
+    y32 = op.apply(Sd, td).cpu().numpy()
+    y_ref, bound = oracle.ofdm(W, S, wl.nb, n=wl.n, cp=wl.cp, scale=scale, group_idx=tags, n_threads=NT)
+    for e in (12, 3, 22):
+        op.set_output("i16", e)
+        y16 = op.apply(Sd, td)
+        torch.cuda.synchronize()
+        assert y16.dtype == torch.int16 and tuple(y16.shape) == (6, 64, 2192, 2)
+        got = y16.cpu().numpy()
+        comp = np.stack([y32.real, y32.imag], axis=-1).astype(np.float32) * np.float32(2.0 ** e)
+        want = np.clip(np.rint(comp), -32768, 32767).astype(np.int16)     # rint: half to even
+        assert (got == want).all(), e
+        if e == 12:
+            assert np.abs(comp).max() < 32767            # no saturation at the bench's exponent
+            yq = (got[..., 0].astype(np.float64) + 1j * got[..., 1]) / 2.0 ** e
+            err = np.abs(yq - y_ref.astype(np.complex128)).max(axis=2)
+            assert (err <= 2.0 ** -(e + 1) * np.sqrt(2) + TOL * bound).all()
+        if e == 22:
+            assert (np.abs(got) == 32767).any() or (got == -32768).any()
+    op.set_output("f32")
+    assert op.apply(Sd, td).dtype == torch.complex64
+    from paper_1810_11451_b200.ofdm import _lib
+    assert _lib().bf_ofdm_plan_set_output(op._h, 2, 0) == Status.INVALID_VALUE
+    assert _lib().bf_ofdm_plan_set_output(op._h, 1, 200) == Status.INVALID_VALUE
+    op.close()
+    plan.close()
+
+
+def test_int16_output_needs_the_default_kernel(monkeypatch):
+    monkeypatch.setenv("BFO_OFDM_KERNEL", "sb")
+    plan = Plan(4)
+    op = OfdmPlan(plan, 2)
+    from paper_1810_11451_b200.ofdm import _lib
+    assert _lib().bf_ofdm_plan_set_output(op._h, 1, 12) == Status.UNSUPPORTED
