@@ -27,6 +27,11 @@ using bff::c2;
 using bff::kN;
 using bff::kWarpPad;
 
+#ifndef BFO_CPA_UNROLL
+#define BFO_CPA_UNROLL 4
+#endif
+constexpr int kCpaUnroll = BFO_CPA_UNROLL;   // the cp.async fetch loop: 4 batches the table loads (0.846 -> 0.860, profiles/r02_of1_unroll.jsonl)
+
 struct OParams {
     const float2 *R;      // [n_sym nb][A][B] complex fp32
     float2 *y;            // [n_sym][A][cp + n] complex fp32 (or int16 pairs, OUT16)
@@ -128,6 +133,7 @@ __device__ __forceinline__ void fetch_symbol_cpa(c2 *buf, const OParams &p, int6
     const int a = (int)(sig - m * p.A);
     const float2 *src = p.R + ((m * p.nb) * (int64_t)p.A + a) * p.B + 2 * l;   // chunk l: 2 points
     const uint32_t dst0 = bfk::smem_addr(buf) + 16u * l;
+#pragma unroll(kCpaUnroll)
     for (int c = 0; c < n_copies; ++c) {
         const CopyDesc d = tab[c];
         if (16u * l < d.bytes)
