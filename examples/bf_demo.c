@@ -4,19 +4,24 @@
  * (row i of W is antenna i), beamforms 3 blocks of S and checks
  * the result exactly: antenna rows 0..3 reproduce S's rows bit for bit and rows
  * 4..63 are +0.0 (BASELINE.json north_star item 4: bit-exact identity cases).
- * Also exercises the synchronous argument checks.
+ * Also exercises the synchronous argument checks, and the OFDM output stage
+ * (include/bf_ofdm.h): one active subcarrier through W = [I_4; 0] gives antenna 0 the
+ * complex exponential e^{+2 pi i bin t / n} (readings O2-O3) behind its cyclic prefix (O4)
+ * and every other antenna exact zeros.
  *
  *   gcc -std=c99 -Iinclude -I/usr/local/cuda/include examples/bf_demo.c \
- *       -Lpaper_1810_11451_b200 -lbf -L/usr/local/cuda/lib64 -lcudart -o build/bf_demo
+ *       -Lpaper_1810_11451_b200 -lbf -L/usr/local/cuda/lib64 -lcudart -lm -o build/bf_demo
  *
  * Exit status: 0 = all checks passed, 1 = a check failed, 2 = no CUDA device.
  */
+#include <math.h>
 #include <stdio.h>
 #include <stdint.h>
 #include <string.h>
 #include <cuda_runtime_api.h>
 
 #include "bf.h"
+#include "bf_ofdm.h"
 
 #define N_ANT 64
 #define B 60
@@ -85,6 +90,47 @@ int main(void) {
     if (mismatches) {
         fprintf(stderr, "identity beamforming: %ld elements differ\n", mismatches);
         bad = 1;
+    }
+    /* OFDM output: one symbol of NB blocks, 2048-point IFFT, 16-sample cyclic prefix; S has
+     * a single 1 at flow 0 of subcarrier q0, which sits in bin (q0 - NB B / 2) mod 2048 */
+    {
+        enum { N = 2048, CP = 16, L = CP + N };
+        const int q0 = 137, bin = ((q0 - NB * B / 2) % N + N) % N;
+        static float S1[NB * F * B * 2], Y[N_ANT * L * 2];
+        memset(S1, 0, sizeof S1);
+        S1[((q0 / B) * F * B + q0 % B) * 2] = 1.0f;
+        void *dY = NULL;
+        bf_ofdm_plan_t op = NULL;
+        bad |= check(bf_ofdm_plan_create(plan, 1024, CP, NB, 1.0f, &op), BF_ERR_UNSUPPORTED, "n = 1024");
+        bad |= check(bf_ofdm_plan_create(plan, N, N, NB, 1.0f, &op), BF_ERR_INVALID_VALUE, "cp = n");
+        bad |= check(bf_ofdm_plan_create(plan, N, CP, NB, 1.0f, &op), BF_OK, "bf_ofdm_plan_create");
+        if (cudaMalloc(&dY, sizeof Y)) {
+            fprintf(stderr, "cudaMalloc failed\n");
+            return 1;
+        }
+        cudaMemcpy(dS, S1, sizeof S1, cudaMemcpyHostToDevice);
+        bad |= check(bf_ofdm_apply(op, dS, NULL, 1, dY, NULL), BF_OK, "bf_ofdm_apply");
+        if (cudaDeviceSynchronize() != cudaSuccess) {
+            fprintf(stderr, "device error (ofdm)\n");
+            return 1;
+        }
+        cudaMemcpy(Y, dY, sizeof Y, cudaMemcpyDeviceToHost);
+        double worst = 0.0;
+        long nonzero = 0, prefix = 0;
+        for (int t = 0; t < N; ++t) {
+            const double ang = 6.283185307179586 * (double)((long)bin * t % N) / N;
+            const double dr = Y[(CP + t) * 2] - cos(ang), di = Y[(CP + t) * 2 + 1] - sin(ang);
+            const double e = sqrt(dr * dr + di * di);
+            if (e > worst) worst = e;
+        }
+        for (int u = 0; u < CP * 2; ++u) prefix += memcmp(&Y[u], &Y[N * 2 + u], 4) != 0;
+        for (int i = L * 2; i < N_ANT * L * 2; ++i) nonzero += Y[i] != 0.0f;
+        if (worst > 1e-5 || prefix || nonzero) {   /* O5 bound here: 1e-5 (1 + sqrt(n)) */
+            fprintf(stderr, "ofdm: worst %.3e, prefix mismatches %ld, nonzero %ld\n", worst, prefix, nonzero);
+            bad = 1;
+        }
+        bad |= check(bf_ofdm_destroy(op), BF_OK, "bf_ofdm_destroy");
+        cudaFree(dY);
     }
     bad |= check(bf_destroy(plan), BF_OK, "bf_destroy");
     cudaFree(dW);

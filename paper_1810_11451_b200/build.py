@@ -82,11 +82,12 @@ def build(verbose: bool = False) -> list[str]:
                 os.path.join(ROOT, "build", "probe"), verbose)
     # a plain-C99 consumer of the C ABI (examples/bf_demo.c; run by tests/test_c_demo.py)
     demo_src = os.path.join(ROOT, "examples", "bf_demo.c")
-    if shutil.which("gcc") and _stale(DEMO, [demo_src, LIBBF, os.path.join(inc, "bf.h")]):
+    if shutil.which("gcc") and _stale(DEMO, [demo_src, LIBBF, os.path.join(inc, "bf.h"),
+                                            os.path.join(inc, "bf_ofdm.h")]):
         os.makedirs(os.path.dirname(DEMO), exist_ok=True)
         _run(["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", f"-I{inc}",
               f"-I{os.path.join(CUDA_HOME, 'include')}", demo_src, f"-L{PKG}", "-lbf",
-              f"-L{os.path.join(CUDA_HOME, 'lib64')}", "-lcudart",
+              f"-L{os.path.join(CUDA_HOME, 'lib64')}", "-lcudart", "-lm",
               "-Wl,-rpath,$ORIGIN/../paper_1810_11451_b200", "-o", DEMO])
     return [LIBBF, LIBSYNTH, LIBPROBE, DEMO]
 

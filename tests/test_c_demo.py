@@ -1,5 +1,7 @@
 """The C ABI from plain C99 (examples/bf_demo.c, built by build()): argument checks,
-identity beamforming bit-exact through cudaMalloc'd buffers, no Python on the path."""
+identity beamforming bit-exact through cudaMalloc'd buffers, and the OFDM output stage
+(bf_ofdm_*: one active subcarrier -> a complex exponential behind its cyclic prefix), no
+Python on the path."""
 import os
 import subprocess
 
