@@ -37,7 +37,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c4", help="c2 | c3 | c4 (default) | c5 | fl0 | fl1 | of0 | of1")
-    ap.add_argument("--f", type=int, default=36, help="flow count for --config c3")
+    ap.add_argument("--f", type=int, default=36, help="flow count for --config c3 (and of*: 36 is theirs)")
     ap.add_argument("--layout", default="interleaved",
                     choices=["interleaved", "planar", "interleaved_f16out", "interleaved_i16out"])
     ap.add_argument("--variant", default="auto", choices=["auto", "ffma", "tensor"],
@@ -83,7 +83,13 @@ def dist_env():
 def workload_of(args):
     import bf_synth as syn
     if args.config.startswith("of"):
-        return syn.ofdm_workload(args.config)
+        import dataclasses
+        wl = syn.ofdm_workload(args.config)
+        f = getattr(args, "f", wl.f)
+        if f != wl.f:         # --f: the same symbols with another flow count (sweeps)
+            wl = dataclasses.replace(wl, f=int(f), name=f"{wl.name}-f{int(f)}",
+                                     desc=wl.desc.replace("f = 36", f"f = {int(f)}"))
+        return wl
     if args.config.startswith("fl"):
         return syn.filter_workload(args.config)
     if args.config == "c3":
