@@ -123,12 +123,23 @@ __device__ __forceinline__ void fetch_symbol(c2 *buf, const OParams &p, int64_t 
 // every run (30 chunks per 480-B run); the plan-constant run table (tab) is in shared
 // memory and read as broadcasts; each lane's copies arrive on the warp's mbarrier
 // (count 32) through cp.async.mbarrier.arrive.noinc.
+// HALF > 0: the kernel is specialised for half = HALF (the loads skip the rows of 32 bins
+// that are zero as a whole, so only the two partial rows at the band edges are zero-filled)
+template <int HALF = 0>
 __device__ __forceinline__ void fetch_symbol_cpa(c2 *buf, const OParams &p, int64_t sig, uint64_t *bar,
                                                  int l, const CopyDesc *tab, int n_copies) {
-    const int half = p.half;
-    float4 *z = reinterpret_cast<float4 *>(buf + half);
-    const int nz = (kN - 2 * half) / 2;
-    for (int i = l; i < nz; i += 32) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int half = HALF > 0 ? HALF : p.half;
+    if (HALF > 0) {
+        constexpr int e0 = (HALF + 31) / 32 * 32, b1 = (kN - HALF) / 32 * 32;   // partial rows
+        constexpr int n0 = (e0 - HALF) / 2, n1 = (kN - HALF - b1) / 2;        // float4 counts
+        if (l < n0) reinterpret_cast<float4 *>(buf + HALF)[l] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (l < n1) reinterpret_cast<float4 *>(buf + b1)[l] = make_float4(0.f, 0.f, 0.f, 0.f);
+        static_assert(n0 <= 32 && n1 <= 32, "partial rows");
+    } else {
+        float4 *z = reinterpret_cast<float4 *>(buf + half);
+        const int nz = (kN - 2 * half) / 2;
+        for (int i = l; i < nz; i += 32) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     const int64_t m = sig / p.A;
     const int a = (int)(sig - m * p.A);
     const float2 *src = p.R + ((m * p.nb) * (int64_t)p.A + a) * p.B + 2 * l;   // chunk l: 2 points
@@ -159,7 +170,7 @@ __device__ __forceinline__ void store_sample(float2 *y, int64_t i, float2 v) {
     }
 }
 
-template <int NBUF, int NW, bool CPA = false, bool OUT16 = false>
+template <int NBUF, int NW, bool CPA = false, bool OUT16 = false, int HALF = 0>
 __global__ void __launch_bounds__(NW * 32, NBUF == 1 ? 2 : 1) ofdm_ifft_kernel(const OParams p) {
     extern __shared__ __align__(128) unsigned char osm[];
     const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -182,7 +193,7 @@ __global__ void __launch_bounds__(NW * 32, NBUF == 1 ? 2 : 1) ofdm_ifft_kernel(c
         __syncthreads();
     }
     auto fetch = [&](c2 *b, int64_t sg, uint64_t *br) {
-        if (CPA) fetch_symbol_cpa(b, p, sg, br, l, tab, n_copies);
+        if (CPA) fetch_symbol_cpa<HALF>(b, p, sg, br, l, tab, n_copies);
         else fetch_symbol(b, p, sg, br, l, d0, d1);
     };
     if (gw < p.n_sig) fetch(bufs, gw, bars);
@@ -197,7 +208,10 @@ __global__ void __launch_bounds__(NW * 32, NBUF == 1 ? 2 : 1) ofdm_ifft_kernel(c
         bfk::mbar_wait(bars + cur, NBUF == 1 ? (j & 1) : ((j >> 1) & 1));
         __syncwarp();                                   // the other lanes' zero-bin stores
 #pragma unroll
-        for (int s = 0; s < 64; ++s) a[s] = buf[l + 32 * s];              // X[bin], bin = l + 32 s
+        for (int s = 0; s < 64; ++s) {                  // X[bin], bin = l + 32 s
+            if (HALF > 0 && 32 * s >= HALF && 32 * s + 31 < kN - HALF) a[s] = 0ull;   // zero row
+            else a[s] = buf[l + 32 * s];
+        }
         const int64_t nxt = sig + nw;
         if (NBUF == 2 && nxt < p.n_sig) {               // the other buffer: free since signal j - 1
             c2 *nbuf = bufs + (cur ^ 1) * kWarpPad;

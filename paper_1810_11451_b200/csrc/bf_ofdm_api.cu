@@ -21,6 +21,9 @@ using bfh::fail;
 
 namespace {
 constexpr int64_t kDefaultChunk = 4096;   // symbols per bf_apply + IFFT pair
+// nb = 26 (1560 subcarriers, e.g. 50 MHz at 30 kHz): the IFFT kernel specialised for this
+// half band skips the all-zero rows of bins at compile time
+constexpr int kHalf26 = 26 * 60 / 2;
 }
 
 struct bf_ofdm_plan_s {
@@ -32,6 +35,7 @@ struct bf_ofdm_plan_s {
     // <2, 6>, 3 cpa <1, 4, true> (cp.async fetch; the default: of1 0.855 of copy BW vs 0.84 sb,
     // 0.83 db, 0.72 cpa_db — profiles/r02_of1_kernels.jsonl), 4 cpa_db <2, 6, true>
     int kind = 3;
+    bool spec = true;           // use the nb = 26 specialisation when it applies (BFO_OFDM_SPEC=0: off)
     bool out16 = false;         // bf_ofdm_plan_set_output: int16 samples x 2^out_exp
     int out_exp = 12;
     int64_t chunk = kDefaultChunk;
@@ -78,6 +82,10 @@ bf_status launch_ifft(bf_ofdm_plan_t p, const float2 *R, int64_t n_sym, float2 *
     }
     if (p->kind == 2)
         bfofdm::ofdm_ifft_kernel<2, 6><<<grid, 6 * 32, bfofdm::smem_bytes(2, 6), st>>>(op);
+    else if (p->kind == 3 && op.half == kHalf26 && p->spec)
+        (p->out16 ? bfofdm::ofdm_ifft_kernel<1, 4, true, true, kHalf26>
+                  : bfofdm::ofdm_ifft_kernel<1, 4, true, false, kHalf26>)
+            <<<grid, 4 * 32, bfofdm::smem_bytes(1, 4), st>>>(op);
     else if (p->kind == 3 && p->out16)
         bfofdm::ofdm_ifft_kernel<1, 4, true, true><<<grid, 4 * 32, bfofdm::smem_bytes(1, 4), st>>>(op);
     else if (p->kind == 3)
@@ -141,6 +149,11 @@ bf_status bf_ofdm_plan_create(bf_plan_t bf, int n, int cp, int nb, float scale, 
     const bool db = p->kind == 2 || p->kind == 4;
     e0_ = cudaFuncSetAttribute(bfofdm::ofdm_ifft_kernel<1, 4, true, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, bfofdm::smem_bytes(1, 4));
+    for (const void *k : {(const void *)bfofdm::ofdm_ifft_kernel<1, 4, true, false, kHalf26>,
+                          (const void *)bfofdm::ofdm_ifft_kernel<1, 4, true, true, kHalf26>})
+        if (e0_ == cudaSuccess)
+            e0_ = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bfofdm::smem_bytes(1, 4));
+    if (const char *env = std::getenv("BFO_OFDM_SPEC")) p->spec = std::atoi(env) != 0;
     const void *kern = p->kind == 2   ? (const void *)bfofdm::ofdm_ifft_kernel<2, 6>
                        : p->kind == 3 ? (const void *)bfofdm::ofdm_ifft_kernel<1, 4, true>
                        : p->kind == 4 ? (const void *)bfofdm::ofdm_ifft_kernel<2, 6, true>

@@ -55,7 +55,10 @@ def gaussian(rng, shape, scale=1.0):
     return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)).astype(np.complex64) * np.float32(scale)
 
 
-def test_of0_workload_matches_oracle():
+@pytest.mark.parametrize("spec", ["1", "0"])
+def test_of0_workload_matches_oracle(spec, monkeypatch):
+    # nb = 26: the kernel specialised for its half band (the default) and the generic one
+    monkeypatch.setenv("BFO_OFDM_SPEC", spec)
     wl = syn.ofdm_workload("of0")
     W, S, tags = syn.ofdm_inputs(wl)
     scale = float(np.float32(1.0 / np.sqrt(wl.n)))
