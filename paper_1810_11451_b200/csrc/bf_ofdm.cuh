@@ -125,7 +125,10 @@ __device__ __forceinline__ void fetch_symbol(c2 *buf, const OParams &p, int64_t 
 // (count 32) through cp.async.mbarrier.arrive.noinc.
 // HALF > 0: the kernel is specialised for half = HALF (the loads skip the rows of 32 bins
 // that are zero as a whole, so only the two partial rows at the band edges are zero-filled)
-template <int HALF = 0>
+// CT (with HALF): the run table at compile time — measured faster for the int16 output
+// (0.68 -> 0.81 of copy BW) and slower for fp32 output (0.86 -> 0.825,
+// profiles/r02_of1_spec2.jsonl), so the kernel takes it for OUT16 only
+template <int HALF = 0, bool CT = false>
 __device__ __forceinline__ void fetch_symbol_cpa(c2 *buf, const OParams &p, int64_t sig, uint64_t *bar,
                                                  int l, const CopyDesc *tab, int n_copies) {
     const int half = HALF > 0 ? HALF : p.half;
@@ -144,6 +147,23 @@ __device__ __forceinline__ void fetch_symbol_cpa(c2 *buf, const OParams &p, int6
     const int a = (int)(sig - m * p.A);
     const float2 *src = p.R + ((m * p.nb) * (int64_t)p.A + a) * p.B + 2 * l;   // chunk l: 2 points
     const uint32_t dst0 = bfk::smem_addr(buf) + 16u * l;
+    if (CT && HALF > 0) {
+        // the run table at compile time (n_ant 64, b 60, nb = 2 HALF / 60 blocks, none
+        // straddling the middle): one cp.async per run and lane, immediate offsets
+        static_assert(HALF % 60 == 0, "specialisation for whole blocks per half");
+        if (l < 30) {
+#pragma unroll
+            for (int c = 0; c < 2 * HALF / 60; ++c) {
+                constexpr int kB = 60, kRun = 64 * 60;     // points per run, per block of R
+                const int bin = c * kB >= HALF ? c * kB - HALF : c * kB + kN - HALF;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                             ::"r"(dst0 + 8u * bin), "l"(src + (int64_t)c * kRun) : "memory");
+            }
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bfk::smem_addr(bar))
+                     : "memory");
+        return;
+    }
 #pragma unroll(kCpaUnroll)
     for (int c = 0; c < n_copies; ++c) {
         const CopyDesc d = tab[c];
@@ -193,7 +213,7 @@ __global__ void __launch_bounds__(NW * 32, NBUF == 1 ? 2 : 1) ofdm_ifft_kernel(c
         __syncthreads();
     }
     auto fetch = [&](c2 *b, int64_t sg, uint64_t *br) {
-        if (CPA) fetch_symbol_cpa<HALF>(b, p, sg, br, l, tab, n_copies);
+        if (CPA) fetch_symbol_cpa<HALF, OUT16>(b, p, sg, br, l, tab, n_copies);
         else fetch_symbol(b, p, sg, br, l, d0, d1);
     };
     if (gw < p.n_sig) fetch(bufs, gw, bars);

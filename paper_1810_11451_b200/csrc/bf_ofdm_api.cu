@@ -82,7 +82,7 @@ bf_status launch_ifft(bf_ofdm_plan_t p, const float2 *R, int64_t n_sym, float2 *
     }
     if (p->kind == 2)
         bfofdm::ofdm_ifft_kernel<2, 6><<<grid, 6 * 32, bfofdm::smem_bytes(2, 6), st>>>(op);
-    else if (p->kind == 3 && op.half == kHalf26 && p->spec)
+    else if (p->kind == 3 && op.half == kHalf26 && p->A == 64 && p->B == 60 && p->spec)
         (p->out16 ? bfofdm::ofdm_ifft_kernel<1, 4, true, true, kHalf26>
                   : bfofdm::ofdm_ifft_kernel<1, 4, true, false, kHalf26>)
             <<<grid, 4 * 32, bfofdm::smem_bytes(1, 4), st>>>(op);
